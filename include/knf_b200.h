@@ -1,0 +1,211 @@
+/*
+ * knf_b200.h -- C-ABI of libknf_b200.so: the B200-native (sm_100a) replacement for the
+ * KiloNeuS render hot path of the reference package `kilofield`
+ * (/root/reference/pkg/src/kilofield).  Plain pointers and sizes only; no torch types.
+ *
+ * Every entry point names the reference function it stands in for (file:line relative to
+ * /root/reference/pkg/src/kilofield/).  INTEGRATION.md shows the ctypes binding a
+ * reference maintainer would add.
+ *
+ * Conventions
+ *   - return value: 0 on success, negative KNF_E_* on failure; knf_last_error() returns a
+ *     thread-local message for the last failing call on this thread.
+ *   - `mem` says where EVERY array argument of that call lives: KNF_MEM_DEVICE (device
+ *     pointers on the field's GPU, nothing is copied, the call is asynchronous on `stream`)
+ *     or KNF_MEM_HOST (ordinary host memory; the library stages host->device, runs, copies
+ *     device->host and synchronises `stream` before returning).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).
+ *   - arrays are C-contiguous; "(n,3) f64" means n rows of 3 doubles.
+ *   - the library owns only the opaque handles and their internal scratch; callers own
+ *     every buffer they pass.  A handle serialises concurrent calls internally, so it may be
+ *     shared between host threads (reference contract: SPEC.md:190-191).
+ *   - there is no CPU fallback: without a CUDA device every compute call fails with
+ *     KNF_E_CUDA.
+ */
+#ifndef KNF_B200_H
+#define KNF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KNF_ABI_VERSION 1
+
+enum {
+  KNF_OK = 0,
+  KNF_E_INVALID = -1,     /* contract violation -> Python ValueError (surface.py:72-75, grid.py:409) */
+  KNF_E_UNSUPPORTED = -2, /* field architecture the kernels are not compiled for */
+  KNF_E_CUDA = -3,        /* CUDA runtime / no device */
+  KNF_E_IO = -4,          /* .knf file problems (modelio.py:30-47) */
+  KNF_E_NOMEM = -5
+};
+
+enum { KNF_MEM_DEVICE = 0, KNF_MEM_HOST = 1 };
+
+typedef struct knf_field_s* knf_field_t;
+typedef struct knf_scene_s* knf_scene_t;
+
+/* grid.py:32-154 GridConfig + MlpGrid stacks, exactly as the reference holds them in host
+ * memory: weights[k] is (n_cells, out_k, in_k) row-major fp32, biases[k] is (n_cells, out_k). */
+typedef struct {
+  int32_t resolution;
+  double bbox_min[3];
+  double bbox_max[3];
+  int32_t sdf_freqs;   /* L_x, 6 */
+  int32_t dir_freqs;   /* L_v, 4 */
+  int32_t feature_dim; /* F, 8 */
+  double fd_step;      /* h, 1e-3 */
+  const float* sdf_w[3];
+  const float* sdf_b[3];
+  const float* color_w[3];
+  const float* color_b[3];
+} KnfFieldDesc;
+
+/* cameras.py:10-36 CameraPose */
+typedef struct {
+  double position[3];
+  double rotation[9]; /* row-major 3x3, columns = right/up/back */
+  double fov_y;
+  int32_t width;
+  int32_t height;
+} KnfCamera;
+
+/* surface.py:64-75 RenderSettings (render_pass is host-side only) */
+typedef struct {
+  double eps_hit;
+  int32_t max_steps;
+  double step_scale;
+} KnfSettings;
+
+/* device-side statistics of the last march/render call on a handle (for roofline accounting) */
+typedef struct {
+  int64_t sdf_evals;    /* SDF MLP evaluations issued (march + refinement + shading probes) */
+  int64_t color_evals;  /* colour MLP evaluations */
+  int64_t rays;         /* rays marched */
+  int64_t hits;
+  int64_t wavefronts;   /* march iterations executed */
+  int64_t kernel_launches;
+} KnfStats;
+
+int knf_abi_version(void);
+const char* knf_last_error(void);
+/* number of CUDA devices visible, or KNF_E_CUDA */
+int knf_device_count(void);
+
+/* ---- field lifetime --------------------------------------------------------------------- */
+/* Packs the stacks into cell-major, k-major blobs and uploads them to `device`
+ * (replaces nothing in the reference: this is the one-time upload of grid.KiloField). */
+int knf_field_create(const KnfFieldDesc* desc, int device, knf_field_t* out);
+/* modelio.load_model (modelio.py:127-165) straight to the device layout;
+ * same magic / version / truncation / CRC32 checks. */
+int knf_field_create_from_knf(const char* path, int device, knf_field_t* out);
+int knf_field_destroy(knf_field_t f);
+/* fills the GridConfig part of `desc` (pointers are set to NULL) */
+int knf_field_describe(knf_field_t f, KnfFieldDesc* desc);
+int knf_field_stats(knf_field_t f, KnfStats* out);
+
+/* ---- routing: grid.py:176-213 ------------------------------------------------------------ */
+/* grid.cell_index_flat (grid.py:182-185) on fp32 points (fp64 arithmetic, bit-exact). */
+int knf_cell_index(knf_field_t f, const float* pts, int64_t n, int32_t* cell, int mem, void* stream);
+/* same for fp64 points (grid.cell_index, grid.py:166-173, passes fp64 straight through). */
+int knf_cell_index_f64(knf_field_t f, const double* pts, int64_t n, int32_t* cell, int mem, void* stream);
+/* grid.route (grid.py:207-213): cell ids, a sort-by-cell permutation (`order[r]` = input row of
+ * sorted row r; rows of one cell are contiguous, order inside a cell is unspecified), and the
+ * occupied segments.  seg_cell/seg_start need room for min(n, n_cells) entries (+1 for
+ * seg_start, which gets the closing n); *n_seg receives the count. Any output may be NULL. */
+int knf_route(knf_field_t f, const float* pts, int64_t n, int32_t* cell, int32_t* order,
+              int32_t* seg_cell, int32_t* seg_start, int32_t* n_seg, int mem, void* stream);
+
+/* ---- batched multi-network forward: grid.py:373-409 -------------------------------------- */
+/* grid.sdf_query (grid.py:373-380): out is (n, 1+F) fp32, column 0 = distance. */
+int knf_sdf_forward(knf_field_t f, const float* pts, int64_t n, float* out, int mem, void* stream);
+/* grid.sdf_values (grid.py:383-384): distances only. */
+int knf_sdf_values(knf_field_t f, const float* pts, int64_t n, float* dist, int mem, void* stream);
+/* grid.color_query (grid.py:387-400): x,v,nrm (n,3) fp32, z (n,F) fp32 -> rgb (n,3) fp32. */
+int knf_color_forward(knf_field_t f, const float* x, const float* v, const float* nrm, const float* z,
+                      int64_t n, float* rgb, int mem, void* stream);
+
+/* ---- FD normals: grid.py:416-461 ---------------------------------------------------------- */
+/* grid.grad_fd (grid.py:440-451): pts (n,3) f64 -> grad (n,3) f64. */
+int knf_fd_gradient(knf_field_t f, const double* pts, int64_t n, double* grad, int mem, void* stream);
+/* grid.normal_batch (grid.py:454-461): unit normals or zeros, ok mask. */
+int knf_fd_normals(knf_field_t f, const double* pts, int64_t n, double eps, double* nrm, uint8_t* ok,
+                   int mem, void* stream);
+
+/* ---- rays: cameras.py:57-76, surface.py:131-149 ------------------------------------------- */
+/* cameras.pixel_rays: pixel_xy (n,2) int32 (col,row) or NULL for the full raster (n = W*H);
+ * jitter (n,2) f64 or NULL for pixel centres. */
+int knf_pixel_rays(const KnfCamera* cam, const int32_t* pixel_xy, const double* jitter, int64_t n,
+                   double* origins, double* dirs, int device, int mem, void* stream);
+/* surface.ray_aabb_batch. */
+int knf_ray_aabb(const double* origins, const double* dirs, int64_t n, const double bbox_min[3],
+                 const double bbox_max[3], double* t_near, double* t_far, uint8_t* hit, int device, int mem,
+                 void* stream);
+
+/* ---- sphere tracing + shading: surface.py:82-99, 162-258 ---------------------------------- */
+/* surface.march_rays(FieldSurface(field), ...): hit (n) u8, t (n) f64, position (n,3) f64,
+ * steps (n) i32.  position/steps may be NULL. */
+int knf_march(knf_field_t f, const double* origins, const double* dirs, const double* t_near,
+              const double* t_far, int64_t n, const KnfSettings* s, uint8_t* hit, double* t, double* position,
+              int32_t* steps, int mem, void* stream);
+/* FieldSurface.shade (surface.py:93-99): FD normals (fallback -view_dir), feature re-query,
+ * colour MLP.  colors/normals (n,3) f64. */
+int knf_shade(knf_field_t f, const double* pts, const double* view_dirs, int64_t n, double* colors,
+              double* normals, int mem, void* stream);
+/* surface.trace_and_shade (surface.py:229-241): AABB -> march -> shade; colours clipped to
+ * [0,1], zeros at misses. */
+int knf_trace_and_shade(knf_field_t f, const double* origins, const double* dirs, int64_t n,
+                        const KnfSettings* s, uint8_t* hit, double* t, double* position, int32_t* steps,
+                        double* normals, double* colors, int mem, void* stream);
+
+/* ---- frame driver: surface.py:273-336 ------------------------------------------------------ */
+/* Rows [row0,row1) of surface.render_frame: ray generation, AABB, march, shade, background
+ * composite and supersample reduction, all on the device.  Buffers cover ONLY the requested
+ * rows: color (rows,W,3) f32, depth (rows,W) f32 (+inf at misses), normal (rows,W,3) f32,
+ * hit (rows,W) u8. */
+int knf_render_frame(knf_field_t f, const KnfCamera* cam, const KnfSettings* s, const double background[3],
+                     int supersample, int row0, int row1, float* color, float* depth, float* normal,
+                     uint8_t* hit, int mem, void* stream);
+
+/* ---- path tracer: pathtrace.py -------------------------------------------------------------- */
+enum { KNF_OBJ_SPHERE = 0, KNF_OBJ_QUAD = 1, KNF_OBJ_BOX = 2, KNF_OBJ_NEURAL = 3 };
+enum { KNF_MAT_LAMBERTIAN = 0, KNF_MAT_EMISSIVE = 1 };
+
+/* One entry of pathtrace.Scene.objects (pathtrace.py:115-280), in scene order. */
+typedef struct {
+  int32_t kind;
+  int32_t material;  /* analytic objects only */
+  double rgb[3];     /* albedo or radiance */
+  /* sphere: a = centre, s = radius.  quad: a = corner, b = edge_u, c = edge_v.
+   * box: a = bmin, b = bmax.  neural: a = translation, rot = rotation (row-major), s = scale. */
+  double a[3];
+  double b[3];
+  double c[3];
+  double rot[9];
+  double s;
+  knf_field_t field;    /* neural only */
+  KnfSettings settings; /* neural only */
+} KnfObject;
+
+/* pathtrace.Scene with a ConstantEnv (pathtrace.py:76-84, 277-280). */
+int knf_scene_create(const KnfObject* objects, int32_t n_objects, const double env_rgb[3], int device,
+                     knf_scene_t* out);
+int knf_scene_destroy(knf_scene_t sc);
+/* pathtrace.Rng.uniform (pathtrace.py:37-49), bit-exact: u[i] = hash(seed, pixel[i], sample[i], slot[i]). */
+int knf_rng_uniform(uint64_t seed, const uint64_t* pixel, const uint64_t* sample, const uint64_t* slot,
+                    int64_t n, double* u, int device, int mem, void* stream);
+/* Rows [row0,row1) of pathtrace.render_pathtraced (pathtrace.py:436-471): hdr (rows,W,3) f64 mean
+ * radiance over samples sample_offset .. sample_offset+spp-1. */
+int knf_pathtrace(knf_scene_t sc, const KnfCamera* cam, int32_t spp, uint64_t seed, int32_t max_bounces,
+                  int32_t sample_offset, int row0, int row1, double* hdr, int mem, void* stream);
+/* pathtrace._trace_batch (pathtrace.py:340-420) for caller-supplied rays (trace_path is n = 1). */
+int knf_trace_paths(knf_scene_t sc, const double* origins, const double* dirs, const uint64_t* pixel_ids,
+                    int64_t n, uint64_t sample, uint64_t seed, int32_t max_bounces, double* radiance, int mem,
+                    void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KNF_B200_H */

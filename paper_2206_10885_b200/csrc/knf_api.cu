@@ -1,0 +1,732 @@
+// knf_api.cu -- the extern "C" surface declared in include/knf_b200.h.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "knf_engine.h"
+#include "knf_rays.cuh"
+
+using namespace knf;
+
+namespace knf {
+const std::string& last_error();
+}
+
+#define KNF_TRY(expr)         \
+  do {                        \
+    int _rc = (expr);         \
+    if (_rc != 0) return _rc; \
+  } while (0)
+
+namespace {
+
+inline int blocks_for(size_t n, int threads = 256) {
+  size_t b = (n + threads - 1) / threads;
+  return (int)std::max<size_t>(1, std::min<size_t>(b, 148 * 16));
+}
+
+// Host<->device staging for KNF_MEM_HOST calls.  in(): device mirror of a host input;
+// out(): device buffer whose contents are copied back by finish().
+struct Stager {
+  Field* F;  // may be null (field-less entry points use own buffers)
+  int mem;
+  cudaStream_t st;
+  std::vector<DevBuf> own;
+  struct Pending {
+    void* host;
+    void* dev;
+    size_t bytes;
+  };
+  std::vector<Pending> outs;
+  int slot = 0;
+  int rc = 0;
+
+  Stager(Field* f, int m, cudaStream_t s) : F(f), mem(m), st(s) { own.reserve(16); }
+  ~Stager() {
+    for (DevBuf& b : own) b.release();
+  }
+  void* buffer(size_t bytes) {
+    if (F && slot < 12) {
+      DevBuf& b = F->ws.stage[slot++];
+      if (b.ensure(std::max<size_t>(bytes, 16)) != 0) {
+        rc = KNF_E_NOMEM;
+        return nullptr;
+      }
+      return b.p;
+    }
+    own.emplace_back();
+    if (own.back().ensure(std::max<size_t>(bytes, 16)) != 0) {
+      rc = KNF_E_NOMEM;
+      return nullptr;
+    }
+    return own.back().p;
+  }
+  template <class T>
+  const T* in(const T* p, size_t count) {
+    if (mem == KNF_MEM_DEVICE || p == nullptr) return p;
+    void* d = buffer(count * sizeof(T));
+    if (!d) return nullptr;
+    cudaError_t e = cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "H2D staging copy");
+    return reinterpret_cast<const T*>(d);
+  }
+  template <class T>
+  T* out(T* p, size_t count) {
+    if (mem == KNF_MEM_DEVICE || p == nullptr) return p;
+    void* d = buffer(count * sizeof(T));
+    if (!d) return nullptr;
+    outs.push_back({p, d, count * sizeof(T)});
+    return reinterpret_cast<T*>(d);
+  }
+  int finish() {
+    if (rc) return rc;
+    if (mem == KNF_MEM_DEVICE) return 0;
+    for (auto& o : outs) {
+      cudaError_t e = cudaMemcpyAsync(o.host, o.dev, o.bytes, cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) return cuda_fail(e, "D2H staging copy");
+    }
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    return 0;
+  }
+};
+
+int check_field(knf_field_t f) {
+  if (!f) return fail(KNF_E_INVALID, "null field handle");
+  return 0;
+}
+
+int check_settings(const KnfSettings* s) {
+  if (!s) return fail(KNF_E_INVALID, "null settings");
+  if (!(s->step_scale > 0.0 && s->step_scale <= 1.0)) return fail(KNF_E_INVALID, "step_scale must be in (0, 1]");
+  if (s->max_steps < 0) return fail(KNF_E_INVALID, "max_steps must be >= 0");
+  return 0;
+}
+
+CameraDev make_camera(const KnfCamera& c, int ss) {
+  CameraDev d;
+  for (int i = 0; i < 3; i++) d.pos[i] = c.position[i];
+  for (int i = 0; i < 9; i++) d.rot[i] = c.rotation[i];
+  d.width = c.width * ss;
+  d.height = c.height * ss;
+  d.scale = 2.0 * std::tan(c.fov_y / 2) / d.height;  // cameras.py:68-69
+  return d;
+}
+
+// Pack one family into cell-major, k-major blobs (see knf_common.cuh BlobLayout).
+template <int K1, int N3, int N3P>
+void pack_family(int n_cells, const float* const w[3], const float* const b[3], std::vector<float>& out) {
+  using L = BlobLayout<K1, N3P>;
+  out.assign((size_t)n_cells * L::floats, 0.0f);
+  for (int c = 0; c < n_cells; c++) {
+    float* blob = out.data() + (size_t)c * L::floats;
+    const float* w1 = w[0] + (size_t)c * kHidden * K1;  // (32, K1)
+    for (int j = 0; j < kHidden; j++)
+      for (int k = 0; k < K1; k++) blob[L::w1 + k * kHidden + j] = w1[j * K1 + k];
+    std::memcpy(blob + L::b1, b[0] + (size_t)c * kHidden, kHidden * sizeof(float));
+    const float* w2 = w[1] + (size_t)c * kHidden * kHidden;
+    for (int j = 0; j < kHidden; j++)
+      for (int k = 0; k < kHidden; k++) blob[L::w2 + k * kHidden + j] = w2[j * kHidden + k];
+    std::memcpy(blob + L::b2, b[1] + (size_t)c * kHidden, kHidden * sizeof(float));
+    const float* w3 = w[2] + (size_t)c * N3 * kHidden;  // (N3, 32)
+    for (int j = 0; j < N3; j++)
+      for (int k = 0; k < kHidden; k++) blob[L::w3 + k * N3P + j] = w3[j * kHidden + k];
+    std::memcpy(blob + L::b3, b[2] + (size_t)c * N3, N3 * sizeof(float));
+  }
+}
+
+int validate_desc(const KnfFieldDesc* d) {
+  if (!d) return fail(KNF_E_INVALID, "null field description");
+  if (d->resolution < 1) return fail(KNF_E_INVALID, "resolution must be >= 1");
+  if ((int64_t)d->resolution * d->resolution * d->resolution > (1 << 24))
+    return fail(KNF_E_UNSUPPORTED, "resolution^3 exceeds 2^24 cells");
+  for (int a = 0; a < 3; a++)
+    if (!(d->bbox_min[a] < d->bbox_max[a])) return fail(KNF_E_INVALID, "bbox_min must be < bbox_max componentwise");
+  if (!(d->fd_step > 0)) return fail(KNF_E_INVALID, "fd_step must be > 0");
+  if (d->sdf_freqs != kSdfFreqs || d->dir_freqs != kDirFreqs || d->feature_dim != kFeat)
+    return fail(KNF_E_UNSUPPORTED,
+                "kernels are compiled for the reference widths only: sdf_freqs=6, dir_freqs=4, feature_dim=8 "
+                "(39-32-32-9 / 41-32-32-3)");
+  for (int k = 0; k < 3; k++)
+    if (!d->sdf_w[k] || !d->sdf_b[k] || !d->color_w[k] || !d->color_b[k])
+      return fail(KNF_E_INVALID, "null weight/bias stack");
+  return 0;
+}
+
+int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(KNF_E_CUDA, "no CUDA device available: libknf_b200 has no CPU fallback");
+  }
+  if (device < 0 || device >= ndev) return fail(KNF_E_INVALID, "device index out of range");
+  KNF_CUDA(cudaSetDevice(device));
+  std::unique_ptr<knf_field_s> h(new knf_field_s());
+  Field& F = h->f;
+  F.device = device;
+  F.geom.resolution = d->resolution;
+  F.geom.n_cells = d->resolution * d->resolution * d->resolution;
+  for (int a = 0; a < 3; a++) {
+    F.geom.lo[a] = d->bbox_min[a];
+    F.geom.hi[a] = d->bbox_max[a];
+  }
+  F.geom.fd_step = d->fd_step;
+  std::vector<float> packed;
+  pack_family<kSdfIn, kSdfOut, kSdfOutPad>(F.geom.n_cells, d->sdf_w, d->sdf_b, packed);
+  KNF_CUDA(cudaMalloc(&F.sdf_blobs, packed.size() * sizeof(float)));
+  KNF_CUDA(cudaMemcpy(F.sdf_blobs, packed.data(), packed.size() * sizeof(float), cudaMemcpyHostToDevice));
+  pack_family<kColIn, kColOut, kColOutPad>(F.geom.n_cells, d->color_w, d->color_b, packed);
+  KNF_CUDA(cudaMalloc(&F.col_blobs, packed.size() * sizeof(float)));
+  KNF_CUDA(cudaMemcpy(F.col_blobs, packed.data(), packed.size() * sizeof(float), cudaMemcpyHostToDevice));
+  *out = h.release();
+  return 0;
+}
+
+// zlib-compatible CRC32 (modelio.py:124, 153)
+uint32_t crc32_bytes(const unsigned char* p, size_t n) {
+  static uint32_t table[256];
+  static bool init = false;
+  if (!init) {
+    for (uint32_t i = 0; i < 256; i++) {
+      uint32_t c = i;
+      for (int k = 0; k < 8; k++) c = (c & 1) ? (0xEDB88320u ^ (c >> 1)) : (c >> 1);
+      table[i] = c;
+    }
+    init = true;
+  }
+  uint32_t c = 0xFFFFFFFFu;
+  for (size_t i = 0; i < n; i++) c = table[(c ^ p[i]) & 0xFF] ^ (c >> 8);
+  return c ^ 0xFFFFFFFFu;
+}
+
+}  // namespace
+
+extern "C" {
+
+int knf_abi_version(void) { return KNF_ABI_VERSION; }
+const char* knf_last_error(void) { return knf::last_error().c_str(); }
+
+int knf_device_count(void) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(KNF_E_CUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+  }
+  return n;
+}
+
+int knf_field_create(const KnfFieldDesc* desc, int device, knf_field_t* out) {
+  if (!out) return fail(KNF_E_INVALID, "null output handle");
+  *out = nullptr;
+  KNF_TRY(validate_desc(desc));
+  return create_from_stacks(desc, device, out);
+}
+
+// modelio.load_model (modelio.py:127-165): header, layer specs, payload, CRC32 trailer.
+int knf_field_create_from_knf(const char* path, int device, knf_field_t* out) {
+  if (!out) return fail(KNF_E_INVALID, "null output handle");
+  *out = nullptr;
+  if (!path) return fail(KNF_E_INVALID, "null path");
+  FILE* fh = std::fopen(path, "rb");
+  if (!fh) return fail(KNF_E_IO, std::string("cannot open ") + path);
+  std::vector<unsigned char> buf;
+  std::fseek(fh, 0, SEEK_END);
+  long size = std::ftell(fh);
+  std::fseek(fh, 0, SEEK_SET);
+  buf.resize(size > 0 ? (size_t)size : 0);
+  size_t got = buf.empty() ? 0 : std::fread(buf.data(), 1, buf.size(), fh);
+  std::fclose(fh);
+  if (got != buf.size()) return fail(KNF_E_IO, "short read");
+  auto u32 = [&](size_t off) {
+    uint32_t v;
+    std::memcpy(&v, buf.data() + off, 4);
+    return v;
+  };
+  if (buf.size() < 48 || std::memcmp(buf.data(), "KNSF", 4) != 0) return fail(KNF_E_IO, "bad magic: expected KNSF");
+  if (u32(4) != 1) return fail(KNF_E_IO, "format version mismatch: supported 1");
+  KnfFieldDesc d{};
+  d.resolution = (int32_t)u32(8);
+  float bbox[6];
+  std::memcpy(bbox, buf.data() + 12, 24);
+  for (int a = 0; a < 3; a++) {
+    d.bbox_min[a] = bbox[a];
+    d.bbox_max[a] = bbox[3 + a];
+  }
+  d.feature_dim = (int32_t)u32(36);
+  d.sdf_freqs = (int32_t)u32(40);
+  d.dir_freqs = (int32_t)u32(44);
+  d.fd_step = 1e-3;  // not stored in the file; GridConfig default (grid.py:40)
+  size_t off = 48;
+  int dims[2][4];
+  for (int fam = 0; fam < 2; fam++) {
+    if (off + 4 > buf.size()) return fail(KNF_E_IO, "truncated header");
+    uint32_t nl = u32(off);
+    off += 4;
+    if (nl != 3) return fail(KNF_E_UNSUPPORTED, "only 3-layer MLPs are supported");
+    if (off + 4 * 7 > buf.size()) return fail(KNF_E_IO, "truncated header");
+    for (int k = 0; k < 4; k++) dims[fam][k] = (int)u32(off + 4 * k);
+    off += 16;
+    uint32_t acts[3] = {u32(off), u32(off + 4), u32(off + 8)};
+    off += 12;
+    const uint32_t want_sdf[3] = {2, 2, 0}, want_col[3] = {1, 1, 3};  // nn.py:22 codes
+    const uint32_t* want = fam == 0 ? want_sdf : want_col;
+    for (int k = 0; k < 3; k++)
+      if (acts[k] != want[k]) return fail(KNF_E_UNSUPPORTED, "unsupported activation sequence");
+  }
+  const int want_dims[2][4] = {{kSdfIn, kHidden, kHidden, kSdfOut}, {kColIn, kHidden, kHidden, kColOut}};
+  for (int fam = 0; fam < 2; fam++)
+    for (int k = 0; k < 4; k++)
+      if (dims[fam][k] != want_dims[fam][k]) return fail(KNF_E_UNSUPPORTED, "unsupported layer widths");
+  if (d.resolution < 1 || (int64_t)d.resolution * d.resolution * d.resolution > (1 << 24))
+    return fail(KNF_E_UNSUPPORTED, "unsupported resolution");
+  const size_t n_cells = (size_t)d.resolution * d.resolution * d.resolution;
+  const size_t per_sdf = kSdfIn * kHidden + kHidden + kHidden * kHidden + kHidden + kHidden * kSdfOut + kSdfOut;
+  const size_t per_col = kColIn * kHidden + kHidden + kHidden * kHidden + kHidden + kHidden * kColOut + kColOut;
+  const size_t payload = 4 * (1 + n_cells * (per_sdf + per_col));
+  if (buf.size() < off + payload + 4) return fail(KNF_E_IO, "truncated payload");
+  if (crc32_bytes(buf.data() + off, payload) != u32(off + payload)) return fail(KNF_E_IO, "payload CRC32 mismatch");
+  // Payload rows are cell-major [W1 | b1 | W2 | b2 | W3 | b3] (modelio.py:72-78); split them into the
+  // stacked layout knf_field_create expects.
+  const float* vals = reinterpret_cast<const float*>(buf.data() + off) + 1;
+  std::vector<float> w[2][3], b[2][3];
+  const float* cursor = vals;
+  for (int fam = 0; fam < 2; fam++) {
+    const int* dm = want_dims[fam];
+    for (int k = 0; k < 3; k++) {
+      w[fam][k].resize(n_cells * dm[k + 1] * dm[k]);
+      b[fam][k].resize(n_cells * dm[k + 1]);
+    }
+    for (size_t c = 0; c < n_cells; c++)
+      for (int k = 0; k < 3; k++) {
+        size_t nw = (size_t)dm[k + 1] * dm[k], nb = dm[k + 1];
+        std::memcpy(w[fam][k].data() + c * nw, cursor, nw * 4);
+        cursor += nw;
+        std::memcpy(b[fam][k].data() + c * nb, cursor, nb * 4);
+        cursor += nb;
+      }
+  }
+  for (int k = 0; k < 3; k++) {
+    d.sdf_w[k] = w[0][k].data();
+    d.sdf_b[k] = b[0][k].data();
+    d.color_w[k] = w[1][k].data();
+    d.color_b[k] = b[1][k].data();
+  }
+  KNF_TRY(validate_desc(&d));
+  return create_from_stacks(&d, device, out);
+}
+
+int knf_field_destroy(knf_field_t f) {
+  if (!f) return 0;
+  cudaSetDevice(f->f.device);
+  {
+    std::lock_guard<std::mutex> lk(f->f.mu);
+    f->f.ws.release_all();
+    if (f->f.sdf_blobs) cudaFree(f->f.sdf_blobs);
+    if (f->f.col_blobs) cudaFree(f->f.col_blobs);
+  }
+  delete f;
+  return 0;
+}
+
+int knf_field_describe(knf_field_t f, KnfFieldDesc* desc) {
+  KNF_TRY(check_field(f));
+  if (!desc) return fail(KNF_E_INVALID, "null desc");
+  std::memset(desc, 0, sizeof(*desc));
+  desc->resolution = f->f.geom.resolution;
+  for (int a = 0; a < 3; a++) {
+    desc->bbox_min[a] = f->f.geom.lo[a];
+    desc->bbox_max[a] = f->f.geom.hi[a];
+  }
+  desc->sdf_freqs = f->f.sdf_freqs;
+  desc->dir_freqs = f->f.dir_freqs;
+  desc->feature_dim = f->f.feature_dim;
+  desc->fd_step = f->f.geom.fd_step;
+  return 0;
+}
+
+int knf_field_stats(knf_field_t f, KnfStats* out) {
+  KNF_TRY(check_field(f));
+  if (!out) return fail(KNF_E_INVALID, "null stats");
+  std::lock_guard<std::mutex> lk(f->f.mu);
+  KNF_CUDA(cudaSetDevice(f->f.device));
+  KNF_CUDA(cudaDeviceSynchronize());
+  if (f->f.ws.counters.p) KNF_TRY(finish_stats(f->f, 0));
+  *out = f->f.stats;
+  return 0;
+}
+
+// ---- routing ---------------------------------------------------------------------------------------
+extern "C++" {
+template <class T>
+static int cell_index_impl(knf_field_t f, const T* pts, int64_t n, int32_t* cell, int mem, void* stream) {
+  KNF_TRY(check_field(f));
+  if (n < 0 || (n > 0 && (!pts || !cell))) return fail(KNF_E_INVALID, "bad arguments to knf_cell_index");
+  if (n == 0) return 0;
+  if (n > INT32_MAX / 4) return fail(KNF_E_INVALID, "too many points for one call");
+  Field& F = f->f;
+  std::lock_guard<std::mutex> lk(F.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  KNF_TRY(begin_call(F, st));
+  Stager S(&F, mem, st);
+  const T* dp = S.in(pts, (size_t)n * 3);
+  int32_t* dc = S.out(cell, (size_t)n);
+  if (S.rc) return S.rc;
+  cell_index_kernel<T><<<blocks_for((size_t)n), 256, 0, st>>>(F.geom, dp, (int)n, dc);
+  F.stats.kernel_launches += 1;
+  KNF_CUDA(cudaGetLastError());
+  return S.finish();
+}
+}  // extern "C++"
+
+int knf_cell_index(knf_field_t f, const float* pts, int64_t n, int32_t* cell, int mem, void* stream) {
+  return cell_index_impl<float>(f, pts, n, cell, mem, stream);
+}
+int knf_cell_index_f64(knf_field_t f, const double* pts, int64_t n, int32_t* cell, int mem, void* stream) {
+  return cell_index_impl<double>(f, pts, n, cell, mem, stream);
+}
+
+int knf_route(knf_field_t f, const float* pts, int64_t n, int32_t* cell, int32_t* order, int32_t* seg_cell,
+              int32_t* seg_start, int32_t* n_seg, int mem, void* stream) {
+  KNF_TRY(check_field(f));
+  if (n < 0 || (n > 0 && !pts)) return fail(KNF_E_INVALID, "bad arguments to knf_route");
+  if ((seg_cell == nullptr) != (seg_start == nullptr)) return fail(KNF_E_INVALID, "seg_cell and seg_start go together");
+  if (n > INT32_MAX / 16) return fail(KNF_E_INVALID, "too many points for one call");
+  Field& F = f->f;
+  std::lock_guard<std::mutex> lk(F.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  KNF_TRY(begin_call(F, st));
+  Stager S(&F, mem, st);
+  size_t nseg_cap = std::min<size_t>((size_t)std::max<int64_t>(n, 1), (size_t)F.geom.n_cells);
+  const float* dp = S.in(pts, (size_t)n * 3);
+  int32_t* dcell = S.out(cell, (size_t)n);
+  int32_t* dorder = S.out(order, (size_t)n);
+  int32_t* dsc = S.out(seg_cell, nseg_cap);
+  int32_t* dss = S.out(seg_start, nseg_cap + 1);
+  int32_t* dns = S.out(n_seg, 1);
+  if (S.rc) return S.rc;
+  KNF_TRY(ensure_requests(F, (size_t)std::max<int64_t>(n, 1)));
+  RouteBuffers R = route_buffers(F, 2, -1);
+  route_emit_points_kernel<<<blocks_for((size_t)std::max<int64_t>(n, 1)), 256, 0, st>>>(R, F.geom, dp, (int)n, dcell);
+  F.stats.kernel_launches += 1;
+  KNF_TRY(launch_scan_scatter(F, R, (size_t)std::max<int64_t>(n, 1), st, dsc, dss, dns));
+  if (dorder && n > 0)
+    KNF_CUDA(cudaMemcpyAsync(dorder, R.perm, (size_t)n * sizeof(int), cudaMemcpyDeviceToDevice, st));
+  return S.finish();
+}
+
+// ---- batched forward -----------------------------------------------------------------------------------
+int knf_sdf_forward(knf_field_t f, const float* pts, int64_t n, float* out, int mem, void* stream) {
+  KNF_TRY(check_field(f));
+  if (n < 0 || (n > 0 && (!pts || !out))) return fail(KNF_E_INVALID, "bad arguments to knf_sdf_forward");
+  if (n == 0) return 0;
+  if (n > INT32_MAX / 16) return fail(KNF_E_INVALID, "too many points for one call");
+  Field& F = f->f;
+  std::lock_guard<std::mutex> lk(F.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  KNF_TRY(begin_call(F, st));
+  Stager S(&F, mem, st);
+  const float* dp = S.in(pts, (size_t)n * 3);
+  float* dout = S.out(out, (size_t)n * kSdfOut);
+  if (S.rc) return S.rc;
+  KNF_TRY(sdf_forward_device(F, dp, n, dout, nullptr, nullptr, st));
+  return S.finish();
+}
+
+int knf_sdf_values(knf_field_t f, const float* pts, int64_t n, float* dist, int mem, void* stream) {
+  KNF_TRY(check_field(f));
+  if (n < 0 || (n > 0 && (!pts || !dist))) return fail(KNF_E_INVALID, "bad arguments to knf_sdf_values");
+  if (n == 0) return 0;
+  if (n > INT32_MAX / 16) return fail(KNF_E_INVALID, "too many points for one call");
+  Field& F = f->f;
+  std::lock_guard<std::mutex> lk(F.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  KNF_TRY(begin_call(F, st));
+  Stager S(&F, mem, st);
+  const float* dp = S.in(pts, (size_t)n * 3);
+  float* dd = S.out(dist, (size_t)n);
+  if (S.rc) return S.rc;
+  KNF_TRY(sdf_forward_device(F, dp, n, nullptr, dd, nullptr, st));
+  return S.finish();
+}
+
+int knf_color_forward(knf_field_t f, const float* x, const float* v, const float* nrm, const float* z, int64_t n,
+                      float* rgb, int mem, void* stream) {
+  KNF_TRY(check_field(f));
+  if (n < 0 || (n > 0 && (!x || !v || !nrm || !z || !rgb))) return fail(KNF_E_INVALID, "bad arguments to knf_color_forward");
+  if (n == 0) return 0;
+  if (n > INT32_MAX / 16) return fail(KNF_E_INVALID, "too many points for one call");
+  Field& F = f->f;
+  std::lock_guard<std::mutex> lk(F.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  KNF_TRY(begin_call(F, st));
+  Stager S(&F, mem, st);
+  const float* dx = S.in(x, (size_t)n * 3);
+  const float* dv = S.in(v, (size_t)n * 3);
+  const float* dn = S.in(nrm, (size_t)n * 3);
+  const float* dz = S.in(z, (size_t)n * kFeat);
+  float* drgb = S.out(rgb, (size_t)n * 3);
+  if (S.rc) return S.rc;
+  KNF_TRY(color_forward_device(F, dx, dv, dn, dz, n, drgb, st));
+  return S.finish();
+}
+
+// ---- FD normals -----------------------------------------------------------------------------------------
+int knf_fd_gradient(knf_field_t f, const double* pts, int64_t n, double* grad, int mem, void* stream) {
+  KNF_TRY(check_field(f));
+  if (n < 0 || (n > 0 && (!pts || !grad))) return fail(KNF_E_INVALID, "bad arguments to knf_fd_gradient");
+  if (n == 0) return 0;
+  if (n > INT32_MAX / 128) return fail(KNF_E_INVALID, "too many points for one call");
+  Field& F = f->f;
+  std::lock_guard<std::mutex> lk(F.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  KNF_TRY(begin_call(F, st));
+  Stager S(&F, mem, st);
+  const double* dp = S.in(pts, (size_t)n * 3);
+  double* dg = S.out(grad, (size_t)n * 3);
+  if (S.rc) return S.rc;
+  ShadeTargets T;
+  T.grad = dg;
+  KNF_TRY(shade_points_device(F, dp, nullptr, n, T, st));
+  return S.finish();
+}
+
+int knf_fd_normals(knf_field_t f, const double* pts, int64_t n, double eps, double* nrm, uint8_t* ok, int mem,
+                   void* stream) {
+  KNF_TRY(check_field(f));
+  if (n < 0 || (n > 0 && (!pts || !nrm))) return fail(KNF_E_INVALID, "bad arguments to knf_fd_normals");
+  if (n == 0) return 0;
+  if (n > INT32_MAX / 128) return fail(KNF_E_INVALID, "too many points for one call");
+  Field& F = f->f;
+  std::lock_guard<std::mutex> lk(F.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  KNF_TRY(begin_call(F, st));
+  Stager S(&F, mem, st);
+  const double* dp = S.in(pts, (size_t)n * 3);
+  double* dn = S.out(nrm, (size_t)n * 3);
+  uint8_t* dok = S.out(ok, (size_t)n);
+  if (S.rc) return S.rc;
+  ShadeTargets T;
+  T.normals = dn;
+  T.ok = dok;
+  T.eps = eps;
+  KNF_TRY(shade_points_device(F, dp, nullptr, n, T, st));
+  return S.finish();
+}
+
+// ---- rays -------------------------------------------------------------------------------------------------
+int knf_pixel_rays(const KnfCamera* cam, const int32_t* pixel_xy, const double* jitter, int64_t n, double* origins,
+                   double* dirs, int device, int mem, void* stream) {
+  if (!cam || n < 0 || (n > 0 && (!origins || !dirs))) return fail(KNF_E_INVALID, "bad arguments to knf_pixel_rays");
+  if (cam->width <= 0 || cam->height <= 0) return fail(KNF_E_INVALID, "image dimensions must be positive");
+  if (!pixel_xy && n != (int64_t)cam->width * cam->height)
+    return fail(KNF_E_INVALID, "n must equal width*height when pixel_xy is NULL");
+  if (n == 0) return 0;
+  KNF_CUDA(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager S(nullptr, mem, st);
+  const int32_t* dpx = S.in(pixel_xy, (size_t)n * 2);
+  const double* dj = S.in(jitter, (size_t)n * 2);
+  double* dorig = S.out(origins, (size_t)n * 3);
+  double* ddir = S.out(dirs, (size_t)n * 3);
+  if (S.rc) return S.rc;
+  pixel_rays_kernel<<<blocks_for((size_t)n), 256, 0, st>>>(make_camera(*cam, 1), dpx, dj, (long long)n, dorig, ddir);
+  KNF_CUDA(cudaGetLastError());
+  int rc = S.finish();
+  if (rc == 0 && mem == KNF_MEM_HOST) return 0;
+  return rc;
+}
+
+int knf_ray_aabb(const double* origins, const double* dirs, int64_t n, const double bbox_min[3],
+                 const double bbox_max[3], double* t_near, double* t_far, uint8_t* hit, int device, int mem,
+                 void* stream) {
+  if (n < 0 || (n > 0 && (!origins || !dirs || !t_near || !t_far)) || !bbox_min || !bbox_max)
+    return fail(KNF_E_INVALID, "bad arguments to knf_ray_aabb");
+  if (n == 0) return 0;
+  KNF_CUDA(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager S(nullptr, mem, st);
+  const double* dorig = S.in(origins, (size_t)n * 3);
+  const double* ddir = S.in(dirs, (size_t)n * 3);
+  double* dtn = S.out(t_near, (size_t)n);
+  double* dtf = S.out(t_far, (size_t)n);
+  uint8_t* dh = S.out(hit, (size_t)n);
+  if (S.rc) return S.rc;
+  GridGeom box{};
+  for (int a = 0; a < 3; a++) {
+    box.lo[a] = bbox_min[a];
+    box.hi[a] = bbox_max[a];
+  }
+  ray_aabb_kernel<<<blocks_for((size_t)n), 256, 0, st>>>(dorig, ddir, (long long)n, box, dtn, dtf, dh, 0);
+  KNF_CUDA(cudaGetLastError());
+  return S.finish();
+}
+
+// ---- sphere tracing + shading ----------------------------------------------------------------------------------
+int knf_march(knf_field_t f, const double* origins, const double* dirs, const double* t_near, const double* t_far,
+              int64_t n, const KnfSettings* s, uint8_t* hit, double* t, double* position, int32_t* steps, int mem,
+              void* stream) {
+  KNF_TRY(check_field(f));
+  KNF_TRY(check_settings(s));
+  if (n < 0 || (n > 0 && (!origins || !dirs || !t_near || !t_far || !hit || !t)))
+    return fail(KNF_E_INVALID, "bad arguments to knf_march");
+  if (n == 0) return 0;
+  Field& F = f->f;
+  std::lock_guard<std::mutex> lk(F.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  KNF_TRY(begin_call(F, st));
+  Stager S(&F, mem, st);
+  const double* dorig = S.in(origins, (size_t)n * 3);
+  const double* ddir = S.in(dirs, (size_t)n * 3);
+  const double* dtn = S.in(t_near, (size_t)n);
+  const double* dtf = S.in(t_far, (size_t)n);
+  uint8_t* dh = S.out(hit, (size_t)n);
+  double* dt = S.out(t, (size_t)n);
+  double* dpos = S.out(position, (size_t)n * 3);
+  int32_t* dsteps = S.out(steps, (size_t)n);
+  if (S.rc) return S.rc;
+  KNF_TRY(march_device(F, dorig, ddir, dtn, dtf, n, *s, dh, dt, dpos, dsteps, false, st));
+  return S.finish();
+}
+
+int knf_shade(knf_field_t f, const double* pts, const double* view_dirs, int64_t n, double* colors, double* normals,
+              int mem, void* stream) {
+  KNF_TRY(check_field(f));
+  if (n < 0 || (n > 0 && (!pts || !view_dirs || !colors || !normals)))
+    return fail(KNF_E_INVALID, "bad arguments to knf_shade");
+  if (n == 0) return 0;
+  if (n > INT32_MAX / 128) return fail(KNF_E_INVALID, "too many points for one call");
+  Field& F = f->f;
+  std::lock_guard<std::mutex> lk(F.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  KNF_TRY(begin_call(F, st));
+  Stager S(&F, mem, st);
+  const double* dp = S.in(pts, (size_t)n * 3);
+  const double* dv = S.in(view_dirs, (size_t)n * 3);
+  double* dc = S.out(colors, (size_t)n * 3);
+  double* dn = S.out(normals, (size_t)n * 3);
+  if (S.rc) return S.rc;
+  ShadeTargets T;
+  T.normals = dn;
+  T.colors = dc;
+  T.fallback = true;
+  KNF_TRY(shade_points_device(F, dp, dv, n, T, st));
+  return S.finish();
+}
+
+// Shared by knf_trace_and_shade and knf_render_frame: march, then shade the hits in chunks.
+static int trace_shade_device(Field& F, const double* o, const double* d, const double* tn, const double* tf, int64_t n,
+                              const KnfSettings& s, uint8_t* hit, double* t, double* pos, int32_t* steps,
+                              double* normals, double* colors, cudaStream_t st) {
+  KNF_TRY(march_device(F, o, d, tn, tf, n, s, hit, t, pos, steps, true, st));
+  KNF_CUDA(cudaMemsetAsync(normals, 0, (size_t)n * 3 * sizeof(double), st));
+  KNF_CUDA(cudaMemsetAsync(colors, 0, (size_t)n * 3 * sizeof(double), st));
+  int m = 0;
+  KNF_TRY(read_hit_count(F, st, &m));
+  if (m > 0) {
+    ShadeTargets T;
+    T.normals = normals;
+    T.colors = colors;
+    T.fallback = true;
+    T.scatter_by_ray = true;
+    T.clip_colors = true;
+    // chunk so that 7 * chunk requests stay within 32-bit routing indices and modest scratch
+    const int64_t chunk = 1 << 20;
+    for (int64_t base = 0; base < m; base += chunk) {
+      int64_t cnt = std::min<int64_t>(chunk, m - base);
+      KNF_TRY(shade_hits_device(F, o, d, base, cnt, T, st));
+    }
+  }
+  return 0;
+}
+
+int knf_trace_and_shade(knf_field_t f, const double* origins, const double* dirs, int64_t n, const KnfSettings* s,
+                        uint8_t* hit, double* t, double* position, int32_t* steps, double* normals, double* colors,
+                        int mem, void* stream) {
+  KNF_TRY(check_field(f));
+  KNF_TRY(check_settings(s));
+  if (n < 0 || (n > 0 && (!origins || !dirs || !hit || !t || !normals || !colors)))
+    return fail(KNF_E_INVALID, "bad arguments to knf_trace_and_shade");
+  if (n == 0) return 0;
+  Field& F = f->f;
+  std::lock_guard<std::mutex> lk(F.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  KNF_TRY(begin_call(F, st));
+  Stager S(&F, mem, st);
+  const double* dorig = S.in(origins, (size_t)n * 3);
+  const double* ddir = S.in(dirs, (size_t)n * 3);
+  uint8_t* dh = S.out(hit, (size_t)n);
+  double* dt = S.out(t, (size_t)n);
+  double* dpos = S.out(position, (size_t)n * 3);
+  int32_t* dsteps = S.out(steps, (size_t)n);
+  double* dnrm = S.out(normals, (size_t)n * 3);
+  double* dcol = S.out(colors, (size_t)n * 3);
+  if (S.rc) return S.rc;
+  Workspace& W = F.ws;
+  KNF_TRY(W.t_near.ensure((size_t)n * 8));
+  KNF_TRY(W.t_far.ensure((size_t)n * 8));
+  ray_aabb_kernel<<<blocks_for((size_t)n), 256, 0, st>>>(dorig, ddir, (long long)n, F.geom, W.t_near.as<double>(),
+                                                       W.t_far.as<double>(), nullptr, 1);
+  F.stats.kernel_launches += 1;
+  KNF_TRY(trace_shade_device(F, dorig, ddir, W.t_near.as<double>(), W.t_far.as<double>(), n, *s, dh, dt, dpos, dsteps,
+                             dnrm, dcol, st));
+  return S.finish();
+}
+
+int knf_render_frame(knf_field_t f, const KnfCamera* cam, const KnfSettings* s, const double background[3],
+                     int supersample, int row0, int row1, float* color, float* depth, float* normal, uint8_t* hit,
+                     int mem, void* stream) {
+  KNF_TRY(check_field(f));
+  KNF_TRY(check_settings(s));
+  if (!cam || !background || !color || !depth || !normal || !hit) return fail(KNF_E_INVALID, "null argument to knf_render_frame");
+  if (supersample < 1) return fail(KNF_E_INVALID, "supersample must be >= 1");
+  if (cam->width <= 0 || cam->height <= 0) return fail(KNF_E_INVALID, "image dimensions must be positive");
+  if (row0 < 0 || row1 > cam->height || row0 >= row1) return fail(KNF_E_INVALID, "row range out of bounds");
+  Field& F = f->f;
+  std::lock_guard<std::mutex> lk(F.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  KNF_TRY(begin_call(F, st));
+  const int W_ = cam->width, ss = supersample;
+  const int rows = row1 - row0;
+  Stager S(&F, mem, st);
+  float* dcolor = S.out(color, (size_t)rows * W_ * 3);
+  float* ddepth = S.out(depth, (size_t)rows * W_);
+  float* dnormal = S.out(normal, (size_t)rows * W_ * 3);
+  uint8_t* dhit = S.out(hit, (size_t)rows * W_);
+  if (S.rc) return S.rc;
+  CameraDev cd = make_camera(*cam, ss);
+  // process row chunks so a chunk holds at most ~4M sub-rays
+  const int64_t per_row = (int64_t)W_ * ss * ss;
+  int rows_per_chunk = (int)std::max<int64_t>(1, (4ll << 20) / per_row);
+  Workspace& W = F.ws;
+  for (int r = 0; r < rows; r += rows_per_chunk) {
+    int rc_rows = std::min(rows_per_chunk, rows - r);
+    int64_t n = (int64_t)rc_rows * per_row;
+    KNF_TRY(W.origins.ensure((size_t)n * 24));
+    KNF_TRY(W.dirs.ensure((size_t)n * 24));
+    KNF_TRY(W.t_near.ensure((size_t)n * 8));
+    KNF_TRY(W.t_far.ensure((size_t)n * 8));
+    KNF_TRY(W.normals64.ensure((size_t)n * 24));
+    KNF_TRY(W.colors64.ensure((size_t)n * 24));
+    KNF_TRY(ensure_rays(F, (size_t)n));
+    primary_rays_kernel<<<blocks_for((size_t)n), 256, 0, st>>>(cd, F.geom, (row0 + r) * ss, (long long)n,
+                                                             W.origins.as<double>(), W.dirs.as<double>(),
+                                                             W.t_near.as<double>(), W.t_far.as<double>());
+    F.stats.kernel_launches += 1;
+    KNF_TRY(trace_shade_device(F, W.origins.as<double>(), W.dirs.as<double>(), W.t_near.as<double>(),
+                               W.t_far.as<double>(), n, *s, nullptr, nullptr, nullptr, nullptr,
+                               W.normals64.as<double>(), W.colors64.as<double>(), st));
+    compose_kernel<<<blocks_for((size_t)rc_rows * W_), 256, 0, st>>>(
+        rc_rows, W_, ss, W.hit.as<unsigned char>(), W.t_hit.as<double>(), W.normals64.as<double>(),
+        W.colors64.as<double>(), background[0], background[1], background[2], dcolor + (size_t)r * W_ * 3,
+        ddepth + (size_t)r * W_, dnormal + (size_t)r * W_ * 3, dhit + (size_t)r * W_);
+    F.stats.kernel_launches += 1;
+    KNF_CUDA(cudaGetLastError());
+  }
+  return S.finish();
+}
+
+}  // extern "C"

@@ -1,0 +1,203 @@
+// knf_common.cuh -- shared definitions for libknf_b200 (sm_100a only).
+//
+// Compile the whole library with -fmad=false: the reference's fp64 ray bookkeeping and its
+// fp32 encoder recurrence are sequences of individually rounded NumPy operations, so the
+// compiler must never contract a*b+c on its own.  Fused multiply-adds appear only where the
+// reference itself fuses (OpenBLAS sgemm's k-ordered FMA chain, NumPy's SIMD sin/cos/exp
+// polynomials) and are written explicitly with __fmaf_rn.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/knf_b200.h"
+
+namespace knf {
+
+// ---- compiled architecture (reference defaults, grid.py:32-68) -----------------------------
+constexpr int kHidden = 32;
+constexpr int kSdfFreqs = 6;
+constexpr int kDirFreqs = 4;
+constexpr int kFeat = 8;
+constexpr int kSdfIn = 3 + 6 * kSdfFreqs;              // 39
+constexpr int kSdfOut = 1 + kFeat;                      // 9
+constexpr int kSdfOutPad = 12;                          // padded to a float4 multiple
+constexpr int kColIn = 3 + (3 + 6 * kDirFreqs) + 3 + kFeat;  // 41
+constexpr int kColOut = 3;
+constexpr int kColOutPad = 4;
+
+// Per-cell weight blob, all k-major ("transposed") so a thread reads W[k][j..j+3] as one float4:
+//   W1t[K1][32] | b1[32] | W2t[32][32] | b2[32] | W3t[32][N3P] | b3[N3P]
+template <int K1, int N3P>
+struct BlobLayout {
+  static constexpr int w1 = 0;
+  static constexpr int b1 = w1 + K1 * kHidden;
+  static constexpr int w2 = b1 + kHidden;
+  static constexpr int b2 = w2 + kHidden * kHidden;
+  static constexpr int w3 = b2 + kHidden;
+  static constexpr int b3 = w3 + kHidden * N3P;
+  static constexpr int floats = b3 + N3P;
+  static constexpr int bytes = floats * 4;
+  static_assert(bytes % 16 == 0, "blob must be a multiple of 16 B for cp.async.bulk");
+};
+using SdfBlob = BlobLayout<kSdfIn, kSdfOutPad>;    // 2732 floats = 10928 B
+using ColBlob = BlobLayout<kColIn, kColOutPad>;    // 2532 floats = 10128 B
+
+// Points per warp and warps per CTA of the tile kernels; a tile is <= kTilePts points of one cell.
+constexpr int kWarpPts = 64;
+constexpr int kTileWarps = 4;
+constexpr int kTilePts = kWarpPts * kTileWarps;  // 256
+
+struct GridGeom {
+  int resolution;
+  int n_cells;
+  double lo[3];
+  double hi[3];
+  double fd_step;
+};
+
+// One tile of work for the MLP kernels.
+struct Tile {
+  int cell;
+  int start;  // offset into the sorted permutation
+  int count;  // 1..kTilePts
+  int pad;
+};
+
+// Device-resident counters of one routing pass.
+struct RouteCounters {
+  int n_requests;  // how many evaluation requests were emitted
+  int n_tiles;
+  int tile_cursor;  // dynamic tile scheduler of the MLP kernel
+  int pad;
+};
+
+// ---- device math that reproduces NumPy's fp32 SIMD routines bit for bit --------------------
+// Validated in the build container against numpy 2.3.5 (AVX512F/AVX2+FMA dispatch) on 4e6
+// random arguments each: zero mismatches.  See DESIGN.md "Numerics".
+
+// np.sin / np.cos on float32 (loops_trigonometric): 3-term Cody-Waite reduction by pi/2 and
+// two minimax polynomials.  Valid for |x| < 71476 (beyond that NumPy calls libm).
+__device__ __forceinline__ void np_sincosf(float x, float& s_out, float& c_out) {
+  const float two_over_pi = 0x1.45f306p-1f;
+  const float cw1 = -0x1.921fb0p+00f, cw2 = -0x1.5110b4p-22f, cw3 = -0x1.846988p-48f;
+  const float magic = 0x1.8p+23f;
+  float q = __fsub_rn(__fmaf_rn(x, two_over_pi, magic), magic);
+  float r = __fmaf_rn(q, cw1, x);
+  r = __fmaf_rn(q, cw2, r);
+  r = __fmaf_rn(q, cw3, r);
+  float r2 = __fmul_rn(r, r);
+  float pc = __fmaf_rn(0x1.98e616p-16f, r2, -0x1.6c06dcp-10f);
+  pc = __fmaf_rn(pc, r2, 0x1.55553cp-05f);
+  pc = __fmaf_rn(pc, r2, -0x1.000000p-01f);
+  pc = __fmaf_rn(pc, r2, 0x1.000000p+00f);
+  float ps = __fmaf_rn(0x1.7d3bbcp-19f, r2, -0x1.a06bbap-13f);
+  ps = __fmaf_rn(ps, r2, 0x1.11119ap-07f);
+  ps = __fmaf_rn(ps, r2, -0x1.555556p-03f);
+  ps = __fmul_rn(ps, r2);
+  ps = __fmaf_rn(ps, r, r);
+  int iq = (int)q;
+  float sv = (iq & 1) ? pc : ps;
+  s_out = (iq & 2) ? -sv : sv;
+  int ic = iq + 1;
+  float cv = (ic & 1) ? pc : ps;
+  c_out = (ic & 2) ? -cv : cv;
+}
+
+// Correctly rounded a/b for normal operands (Markstein sequence on the MUFU reciprocal).
+__device__ __forceinline__ float div_rn_fast(float a, float b) { return __fdiv_rn(a, b); }
+
+// np.exp on float32 (loops_exponent_log): Cody-Waite by ln2, rational P5/Q2, scalef.
+__device__ __forceinline__ float np_expf(float x) {
+  const float magic = 0x1.8p+23f;
+  float q = __fmul_rn(x, 1.442695040888963407359924681f);
+  q = __fsub_rn(__fadd_rn(q, magic), magic);
+  float r = __fmaf_rn(q, -6.93145752e-1f, x);
+  r = __fmaf_rn(q, -1.42860677e-6f, r);
+  float num = __fmaf_rn(5.082762527590693718096e-04f, r, 6.757896990527504603057e-03f);
+  num = __fmaf_rn(num, r, 5.114512081637298353406e-02f);
+  num = __fmaf_rn(num, r, 2.473615434895520810817e-01f);
+  num = __fmaf_rn(num, r, 7.257664613233124478488e-01f);
+  num = __fmaf_rn(num, r, 9.999999999980870924916e-01f);
+  float den = __fmaf_rn(2.159509375685829852307e-02f, r, -2.742335390411667452936e-01f);
+  den = __fmaf_rn(den, r, 1.0f);
+  return ldexpf(__fdiv_rn(num, den), (int)q);
+}
+
+// nn.sigmoid (nn.py:36-38) with NumPy's exp: bit-exact given the same input.
+__device__ __forceinline__ float np_sigmoidf(float x) {
+  float t = np_expf(-fabsf(x));
+  float den = __fadd_rn(1.0f, t);
+  return x >= 0.0f ? __fdiv_rn(1.0f, den) : __fdiv_rn(t, den);
+}
+
+// nn.softplus (nn.py:26-33): log1p(exp(-|x|)) + max(x,0).  NumPy's log1p is Intel SVML and
+// cannot be reproduced bit for bit; this evaluates both transcendentals to <= 1 ulp so the
+// result is within ~1 ulp of the reference's (measured in tests/test_gpu_forward.py).
+__device__ __forceinline__ float softplus_acc(float x) {
+  float u = np_expf(-fabsf(x));
+  return __fadd_rn(log1pf(u), fmaxf(x, 0.0f));
+}
+
+// grid._cell_triples (grid.py:176-179) for one coordinate: fp64 arithmetic on the fp32 point.
+__device__ __forceinline__ int cell_coord(double p, double lo, double hi, int n) {
+  double t = (p - lo) / (hi - lo) * (double)n;
+  double fl = floor(t);
+  // np.floor(t).astype(int64) then clip: NaN / +-inf / |t| >= 2^63 convert to INT64_MIN on x86 -> 0
+  if (!(fl >= 0.0)) return 0;
+  if (fl >= 9.2233720368547758e18) return 0;
+  if (fl >= (double)n) return n - 1;
+  return (int)fl;
+}
+
+__device__ __forceinline__ int cell_of(double x, double y, double z, const GridGeom& g) {
+  int i = cell_coord(x, g.lo[0], g.hi[0], g.resolution);
+  int j = cell_coord(y, g.lo[1], g.hi[1], g.resolution);
+  int k = cell_coord(z, g.lo[2], g.hi[2], g.resolution);
+  return (i * g.resolution + j) * g.resolution + k;
+}
+
+// ---- small PTX helpers: mbarrier + TMA 1-D bulk copy (UBLKCP) -------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_copy_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst_smem)),
+               "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// Warp-aggregated append: every active lane with `want` gets a unique slot from *counter.
+// Must be reached by all 32 lanes of the warp (callers keep their loops warp-uniform).
+__device__ __forceinline__ int warp_append(int* counter, bool want) {
+  unsigned mask = __ballot_sync(0xffffffffu, want);
+  if (!want) return -1;
+  int lane = threadIdx.x & 31;
+  int leader = __ffs(mask) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(counter, __popc(mask));
+  base = __shfl_sync(mask, base, leader);
+  return base + __popc(mask & ((1u << lane) - 1));
+}
+
+}  // namespace knf

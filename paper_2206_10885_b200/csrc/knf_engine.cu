@@ -1,0 +1,355 @@
+// knf_engine.cu -- workspace management and the device drivers: routing -> tile MLP, the wavefront
+// sphere-trace loop, and shading.  Everything here is stream-ordered; nothing synchronises except
+// read_hit_count / finish_stats.
+#include "knf_engine.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "knf_mlp.cuh"
+#include "knf_rays.cuh"
+
+namespace knf {
+
+static thread_local std::string g_error;
+
+void set_error(const std::string& msg) { g_error = msg; }
+const std::string& last_error() { return g_error; }
+int fail(int code, const std::string& msg) {
+  g_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  g_error = std::string("CUDA error: ") + cudaGetErrorString(e) + " in " + what;
+  cudaGetLastError();  // clear sticky-less errors
+  return KNF_E_CUDA;
+}
+
+int DevBuf::ensure(size_t bytes) {
+  if (bytes <= cap) return 0;
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+  size_t want = bytes + bytes / 8 + 256;
+  cudaError_t e = cudaMalloc(&p, want);
+  if (e != cudaSuccess) {
+    p = nullptr;
+    cudaGetLastError();
+    return fail(KNF_E_NOMEM, std::string("cudaMalloc of ") + std::to_string(want) + " bytes failed: " + cudaGetErrorString(e));
+  }
+  cap = want;
+  return 0;
+}
+void DevBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+}
+
+void Workspace::release_all() {
+  DevBuf* all[] = {&req_pt, &req_cell, &req_rank, &perm, &tiles, &cell_count, &cell_offset, &counters, &t, &t_prev,
+                   &d_prev, &t_conv, &d_conv, &t_hit, &steps, &phase, &hit, &live0, &live1, &dval, &hit_list,
+                   &hit_count, &sdf_out, &col_v, &col_n, &col_z, &rgb, &origins, &dirs, &t_near, &t_far, &normals64,
+                   &colors64, &steps_out};
+  for (DevBuf* b : all) b->release();
+  for (DevBuf& b : stage) b.release();
+  req_cap = ray_cap = 0;
+}
+
+static inline int blocks_for(size_t n, int threads = 256) {
+  size_t b = (n + threads - 1) / threads;
+  return (int)std::max<size_t>(1, std::min<size_t>(b, 148 * 16));
+}
+
+#define KNF_TRY(expr)       \
+  do {                      \
+    int _rc = (expr);       \
+    if (_rc != 0) return _rc; \
+  } while (0)
+
+constexpr size_t kCounterBytes = 4 * sizeof(RouteCounters) + 4 * sizeof(unsigned long long);
+
+int ensure_requests(Field& F, size_t n) {
+  Workspace& W = F.ws;
+  n = std::max<size_t>(n, 1024);
+  if (n > (size_t)INT32_MAX / 16) return fail(KNF_E_INVALID, "request batch too large for 32-bit routing indices");
+  KNF_TRY(W.req_pt.ensure(n * sizeof(float4)));
+  KNF_TRY(W.req_cell.ensure(n * sizeof(int)));
+  KNF_TRY(W.req_rank.ensure(n * sizeof(int)));
+  KNF_TRY(W.perm.ensure(n * sizeof(int)));
+  KNF_TRY(W.tiles.ensure((n / kTilePts + F.geom.n_cells + 2) * sizeof(Tile)));
+  KNF_TRY(W.dval.ensure(n * sizeof(float)));
+  bool fresh = W.cell_count.p == nullptr;
+  KNF_TRY(W.cell_count.ensure((size_t)F.geom.n_cells * sizeof(int)));
+  KNF_TRY(W.cell_offset.ensure(((size_t)F.geom.n_cells + 1) * sizeof(int)));
+  KNF_TRY(W.counters.ensure(kCounterBytes));
+  if (fresh) {
+    KNF_CUDA(cudaMemset(W.cell_count.p, 0, W.cell_count.cap));
+    KNF_CUDA(cudaMemset(W.counters.p, 0, W.counters.cap));
+  }
+  W.req_cap = std::max(W.req_cap, n);
+  return 0;
+}
+
+int ensure_rays(Field& F, size_t n) {
+  Workspace& W = F.ws;
+  n = std::max<size_t>(n, 1024);
+  KNF_TRY(W.t.ensure(n * 8));
+  KNF_TRY(W.t_prev.ensure(n * 8));
+  KNF_TRY(W.d_prev.ensure(n * 8));
+  KNF_TRY(W.t_conv.ensure(n * 8));
+  KNF_TRY(W.d_conv.ensure(n * 8));
+  KNF_TRY(W.t_hit.ensure(n * 8));
+  KNF_TRY(W.steps.ensure(n * 4));
+  KNF_TRY(W.phase.ensure(n));
+  KNF_TRY(W.hit.ensure(n));
+  KNF_TRY(W.live0.ensure(n * 4));
+  KNF_TRY(W.live1.ensure(n * 4));
+  KNF_TRY(W.hit_list.ensure(n * 4));
+  KNF_TRY(W.hit_count.ensure(16));
+  W.ray_cap = std::max(W.ray_cap, n);
+  return ensure_requests(F, n);
+}
+
+RouteCounters* counters(Field& F, int slot) { return F.ws.counters.as<RouteCounters>() + slot; }
+unsigned long long* stat_counter(Field& F, int which) {
+  return reinterpret_cast<unsigned long long*>(F.ws.counters.as<RouteCounters>() + 4) + which;
+}
+
+RouteBuffers route_buffers(Field& F, int slot, int next_slot) {
+  Workspace& W = F.ws;
+  RouteBuffers R;
+  R.req_pt = W.req_pt.as<float4>();
+  R.req_cell = W.req_cell.as<int>();
+  R.req_rank = W.req_rank.as<int>();
+  R.cell_count = W.cell_count.as<int>();
+  R.cell_offset = W.cell_offset.as<int>();
+  R.perm = W.perm.as<int>();
+  R.tiles = W.tiles.as<Tile>();
+  R.ctr = counters(F, slot);
+  R.next_ctr = next_slot >= 0 ? counters(F, next_slot) : nullptr;
+  R.eval_counter = nullptr;
+  return R;
+}
+
+int begin_call(Field& F, cudaStream_t st) {
+  KNF_CUDA(cudaSetDevice(F.device));
+  KNF_TRY(ensure_requests(F, 1024));
+  KNF_CUDA(cudaMemsetAsync(F.ws.cell_count.p, 0, (size_t)F.geom.n_cells * sizeof(int), st));
+  KNF_CUDA(cudaMemsetAsync(F.ws.counters.p, 0, kCounterBytes, st));
+  F.stats = KnfStats{};
+  F.stats.kernel_launches = 0;
+  if (!F.smem_configured) {
+    KNF_CUDA(cudaFuncSetAttribute(mlp_tile_kernel<kSdfIn, kSdfOut, kSdfOutPad, ACT_SOFTPLUS, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SdfKernelSmem)));
+    KNF_CUDA(cudaFuncSetAttribute(mlp_tile_kernel<kColIn, kColOut, kColOutPad, ACT_RELU, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ColKernelSmem)));
+    F.smem_configured = true;
+  }
+  return 0;
+}
+
+int finish_stats(Field& F, cudaStream_t st) {
+  unsigned long long host[2] = {0, 0};
+  KNF_CUDA(cudaMemcpyAsync(host, stat_counter(F, 0), sizeof(host), cudaMemcpyDeviceToHost, st));
+  KNF_CUDA(cudaStreamSynchronize(st));
+  F.stats.sdf_evals = (int64_t)host[0];
+  F.stats.color_evals = (int64_t)host[1];
+  return 0;
+}
+
+int launch_scan_scatter(Field& F, const RouteBuffers& R, size_t n_upper, cudaStream_t st, int* seg_cell, int* seg_start,
+                        int* n_seg) {
+  route_scan_kernel<<<1, kScanThreads, 0, st>>>(R, F.geom.n_cells, seg_cell, seg_start, n_seg);
+  route_scatter_kernel<<<blocks_for(n_upper), 256, 0, st>>>(R);
+  F.stats.kernel_launches += 2;
+  KNF_CUDA(cudaGetLastError());
+  return 0;
+}
+
+static inline int mlp_grid(const Field& F, size_t n_upper) {
+  size_t tiles_upper = n_upper / kTilePts + std::min<size_t>(n_upper, (size_t)F.geom.n_cells) + 1;
+  return (int)std::max<size_t>(1, std::min<size_t>(tiles_upper, 148 * 2));
+}
+
+int launch_sdf_mlp(Field& F, const RouteBuffers& R, size_t n_upper, float* out_first, float* out_full, cudaStream_t st) {
+  MlpParams P{};
+  P.blobs = F.sdf_blobs;
+  P.perm = R.perm;
+  P.tiles = R.tiles;
+  P.ctr = R.ctr;
+  P.req_pt = R.req_pt;
+  P.out_first = out_first;
+  P.out_full = out_full;
+  mlp_tile_kernel<kSdfIn, kSdfOut, kSdfOutPad, ACT_SOFTPLUS, false>
+      <<<mlp_grid(F, n_upper), kTileWarps * 32, sizeof(SdfKernelSmem), st>>>(P);
+  F.stats.kernel_launches += 1;
+  KNF_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int launch_col_mlp(Field& F, const RouteBuffers& R, size_t n_upper, const float* v, const float* nrm, const float* z,
+                   float* rgb, cudaStream_t st) {
+  MlpParams P{};
+  P.blobs = F.col_blobs;
+  P.perm = R.perm;
+  P.tiles = R.tiles;
+  P.ctr = R.ctr;
+  P.req_pt = R.req_pt;
+  P.col_v = v;
+  P.col_n = nrm;
+  P.col_z = z;
+  P.out_full = rgb;
+  mlp_tile_kernel<kColIn, kColOut, kColOutPad, ACT_RELU, true>
+      <<<mlp_grid(F, n_upper), kTileWarps * 32, sizeof(ColKernelSmem), st>>>(P);
+  F.stats.kernel_launches += 1;
+  KNF_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int sdf_forward_device(Field& F, const float* pts, int64_t n, float* out_full, float* out_first, int* cell_out,
+                       cudaStream_t st) {
+  if (n <= 0) return 0;
+  KNF_TRY(ensure_requests(F, (size_t)n));
+  RouteBuffers R = route_buffers(F, 2, -1);
+  R.eval_counter = stat_counter(F, 0);
+  route_emit_points_kernel<<<blocks_for((size_t)n), 256, 0, st>>>(R, F.geom, pts, (int)n, cell_out);
+  F.stats.kernel_launches += 1;
+  KNF_TRY(launch_scan_scatter(F, R, (size_t)n, st));
+  return launch_sdf_mlp(F, R, (size_t)n, out_first, out_full, st);
+}
+
+int color_forward_device(Field& F, const float* x, const float* v, const float* nrm, const float* z, int64_t n,
+                         float* rgb, cudaStream_t st) {
+  if (n <= 0) return 0;
+  KNF_TRY(ensure_requests(F, (size_t)n));
+  RouteBuffers R = route_buffers(F, 3, -1);
+  R.eval_counter = stat_counter(F, 1);
+  route_emit_points_kernel<<<blocks_for((size_t)n), 256, 0, st>>>(R, F.geom, x, (int)n, nullptr);
+  F.stats.kernel_launches += 1;
+  KNF_TRY(launch_scan_scatter(F, R, (size_t)n, st));
+  return launch_col_mlp(F, R, (size_t)n, v, nrm, z, rgb, st);
+}
+
+int march_device(Field& F, const double* o, const double* d, const double* t_near, const double* t_far, int64_t n,
+                 const KnfSettings& s, unsigned char* hit, double* t, double* pos, int* steps, bool want_hit_list,
+                 cudaStream_t st) {
+  if (n <= 0) return 0;
+  if (n > INT32_MAX / 16) return fail(KNF_E_INVALID, "march batch too large; split the rays");
+  KNF_TRY(ensure_rays(F, (size_t)n));
+  Workspace& W = F.ws;
+  MarchState M{};
+  M.o = o;
+  M.d = d;
+  M.t_far = t_far;
+  M.t = W.t.as<double>();
+  M.t_prev = W.t_prev.as<double>();
+  M.d_prev = W.d_prev.as<double>();
+  M.t_conv = W.t_conv.as<double>();
+  M.d_conv = W.d_conv.as<double>();
+  M.t_hit = W.t_hit.as<double>();
+  M.steps = W.steps.as<int>();
+  M.phase = W.phase.as<unsigned char>();
+  M.hit = W.hit.as<unsigned char>();
+  M.live[0] = W.live0.as<int>();
+  M.live[1] = W.live1.as<int>();
+  M.dval = W.dval.as<float>();
+  M.eps = s.eps_hit;
+  M.step_scale = s.step_scale;
+  M.max_steps = s.max_steps;
+
+  KNF_CUDA(cudaMemsetAsync(counters(F, 0), 0, 2 * sizeof(RouteCounters), st));
+  const int nb = blocks_for((size_t)n);
+  {
+    RouteBuffers R0 = route_buffers(F, 0, 1);
+    march_init_kernel<<<nb, 256, 0, st>>>(R0, F.geom, M, t_near, (int)n);
+    F.stats.kernel_launches += 1;
+  }
+  // max_steps stepping wavefronts + one that only carries secant-refinement evaluations
+  for (int w = 0; w <= s.max_steps; w++) {
+    int cur = w & 1, nxt = cur ^ 1;
+    RouteBuffers R = route_buffers(F, cur, nxt);
+    R.eval_counter = stat_counter(F, 0);
+    KNF_TRY(launch_scan_scatter(F, R, (size_t)n, st));
+    KNF_TRY(launch_sdf_mlp(F, R, (size_t)n, M.dval, nullptr, st));
+    RouteBuffers Rn = route_buffers(F, nxt, -1);
+    march_advance_kernel<<<nb, 256, 0, st>>>(Rn, F.geom, M, counters(F, cur), cur);
+    F.stats.kernel_launches += 1;
+    F.stats.wavefronts += 1;
+  }
+  if (want_hit_list) KNF_CUDA(cudaMemsetAsync(W.hit_count.p, 0, 16, st));
+  march_finish_kernel<<<nb, 256, 0, st>>>(M, (int)n, hit, t, pos, steps, want_hit_list ? W.hit_list.as<int>() : nullptr,
+                                          want_hit_list ? W.hit_count.as<int>() : nullptr);
+  F.stats.kernel_launches += 1;
+  F.stats.rays += n;
+  KNF_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int read_hit_count(Field& F, cudaStream_t st, int* out) {
+  KNF_CUDA(cudaMemcpyAsync(out, F.ws.hit_count.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  KNF_CUDA(cudaStreamSynchronize(st));
+  F.stats.hits += *out;
+  return 0;
+}
+
+static int shade_common(Field& F, ShadePoints S, int64_t m, const ShadeTargets& T, cudaStream_t st) {
+  if (m <= 0) return 0;
+  const bool color = T.colors != nullptr;
+  const int np = color ? 7 : 6;
+  const size_t nreq = (size_t)m * np;
+  KNF_TRY(ensure_requests(F, nreq));
+  Workspace& W = F.ws;
+  KNF_TRY(W.sdf_out.ensure(nreq * kSdfOut * sizeof(float)));
+  if (color) {
+    KNF_TRY(W.col_v.ensure((size_t)m * 3 * sizeof(float)));
+    KNF_TRY(W.col_n.ensure((size_t)m * 3 * sizeof(float)));
+    KNF_TRY(W.col_z.ensure((size_t)m * kFeat * sizeof(float)));
+    KNF_TRY(W.rgb.ensure((size_t)m * 3 * sizeof(float)));
+  }
+  S.m_host = (int)m;
+  S.count = nullptr;
+  RouteBuffers R = route_buffers(F, 2, -1);
+  R.eval_counter = stat_counter(F, 0);
+  shade_emit_kernel<<<blocks_for(nreq), 256, 0, st>>>(R, F.geom, S, np);
+  F.stats.kernel_launches += 1;
+  KNF_TRY(launch_scan_scatter(F, R, nreq, st));
+  KNF_TRY(launch_sdf_mlp(F, R, nreq, nullptr, W.sdf_out.as<float>(), st));
+  RouteBuffers Rc = route_buffers(F, 3, -1);
+  Rc.eval_counter = stat_counter(F, 1);
+  shade_finish_kernel<<<blocks_for((size_t)m), 256, 0, st>>>(
+      Rc, F.geom, S, np, W.sdf_out.as<float>(), T.eps, T.fallback ? 1 : 0, T.grad, T.normals, T.ok,
+      T.scatter_by_ray ? 1 : 0, W.col_v.as<float>(), W.col_n.as<float>(), W.col_z.as<float>(), color ? 1 : 0);
+  F.stats.kernel_launches += 1;
+  if (color) {
+    KNF_TRY(launch_scan_scatter(F, Rc, (size_t)m, st));
+    KNF_TRY(launch_col_mlp(F, Rc, (size_t)m, W.col_v.as<float>(), W.col_n.as<float>(), W.col_z.as<float>(),
+                           W.rgb.as<float>(), st));
+    shade_colors_kernel<<<blocks_for((size_t)m), 256, 0, st>>>(S, W.rgb.as<float>(), T.scatter_by_ray ? 1 : 0,
+                                                              T.clip_colors ? 1 : 0, T.colors);
+    F.stats.kernel_launches += 1;
+  }
+  KNF_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int shade_points_device(Field& F, const double* pts, const double* dirs, int64_t m, const ShadeTargets& T,
+                        cudaStream_t st) {
+  ShadePoints S{};
+  S.pts = pts;
+  S.dirs = dirs;
+  return shade_common(F, S, m, T, st);
+}
+
+int shade_hits_device(Field& F, const double* o, const double* d, int64_t first_hit, int64_t m_hits,
+                      const ShadeTargets& T, cudaStream_t st) {
+  ShadePoints S{};
+  S.o = o;
+  S.d = d;
+  S.t_hit = F.ws.t_hit.as<double>();
+  S.list = F.ws.hit_list.as<int>() + first_hit;
+  return shade_common(F, S, m_hits, T, st);
+}
+
+}  // namespace knf

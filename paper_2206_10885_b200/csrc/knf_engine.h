@@ -1,0 +1,116 @@
+// knf_engine.h -- host-side engine behind the C-ABI: field handle, workspace, and the device
+// drivers (route -> MLP, wavefront march, shade) shared by knf_api.cu and knf_pathtrace.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "knf_common.cuh"
+#include "knf_route.cuh"
+
+namespace knf {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define KNF_CUDA(expr)                                   \
+  do {                                                   \
+    cudaError_t _e = (expr);                             \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr);  \
+  } while (0)
+
+// A lazily grown device allocation.
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes);  // 0 or KNF_E_*
+  void release();
+  template <class T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+struct Workspace {
+  // routing (two independent sets: A for SDF passes, B for the colour pass of shading)
+  DevBuf req_pt, req_cell, req_rank, perm, tiles;
+  DevBuf cell_count, cell_offset;
+  DevBuf counters;  // RouteCounters[4] + stats counters
+  // march state
+  DevBuf t, t_prev, d_prev, t_conv, d_conv, t_hit, steps, phase, hit, live0, live1, dval;
+  // shading
+  DevBuf hit_list, hit_count, sdf_out, col_v, col_n, col_z, rgb;
+  // render-frame ray buffers
+  DevBuf origins, dirs, t_near, t_far, normals64, colors64, steps_out;
+  // host staging (KNF_MEM_HOST calls): input/output mirrors
+  DevBuf stage[12];
+  size_t req_cap = 0;
+  size_t ray_cap = 0;
+  void release_all();
+};
+
+struct Field {
+  int device = 0;
+  GridGeom geom{};
+  int sdf_freqs = kSdfFreqs, dir_freqs = kDirFreqs, feature_dim = kFeat;
+  float* sdf_blobs = nullptr;
+  float* col_blobs = nullptr;
+  Workspace ws;
+  std::mutex mu;
+  KnfStats stats{};
+  bool smem_configured = false;
+};
+
+// ---- drivers (all asynchronous on `st`; pointers are device pointers) -------------------------
+int ensure_requests(Field& F, size_t n_requests);
+int ensure_rays(Field& F, size_t n_rays);
+RouteBuffers route_buffers(Field& F, int counter_slot, int next_slot);
+RouteCounters* counters(Field& F, int slot);
+unsigned long long* stat_counter(Field& F, int which);  // 0 = sdf evals, 1 = colour evals
+int begin_call(Field& F, cudaStream_t st);              // select device, reset routing invariants
+int finish_stats(Field& F, cudaStream_t st);            // pull device counters into F.stats (syncs)
+
+int launch_scan_scatter(Field& F, const RouteBuffers& R, size_t n_upper, cudaStream_t st, int* seg_cell = nullptr,
+                        int* seg_start = nullptr, int* n_seg = nullptr);
+int launch_sdf_mlp(Field& F, const RouteBuffers& R, size_t n_upper, float* out_first, float* out_full, cudaStream_t st);
+int launch_col_mlp(Field& F, const RouteBuffers& R, size_t n_upper, const float* v, const float* nrm, const float* z,
+                   float* rgb, cudaStream_t st);
+
+int sdf_forward_device(Field& F, const float* pts, int64_t n, float* out_full, float* out_first, int* cell_out,
+                       cudaStream_t st);
+int color_forward_device(Field& F, const float* x, const float* v, const float* nrm, const float* z, int64_t n,
+                         float* rgb, cudaStream_t st);
+
+// surface.march_rays; optionally compacts the hit rays into ws.hit_list / ws.hit_count.
+int march_device(Field& F, const double* o, const double* d, const double* t_near, const double* t_far, int64_t n,
+                 const KnfSettings& s, unsigned char* hit, double* t, double* pos, int* steps, bool want_hit_list,
+                 cudaStream_t st);
+
+struct ShadeTargets {
+  double* grad = nullptr;       // (m,3)
+  double* normals = nullptr;    // (m,3)
+  unsigned char* ok = nullptr;  // (m)
+  double* colors = nullptr;     // (m,3); null => no colour pass
+  bool fallback = false;        // degenerate normal -> -view_dir
+  bool scatter_by_ray = false;  // write outputs at the ray index of the hit list instead of densely
+  bool clip_colors = false;
+  double eps = 1e-8;
+};
+// Shade explicit points (pts/dirs, m known) ...
+int shade_points_device(Field& F, const double* pts, const double* dirs, int64_t m, const ShadeTargets& T,
+                        cudaStream_t st);
+// ... or the hits of the last march_device(want_hit_list=true) over rays (o, d); m_hits is the
+// host copy of the hit count; [first_hit, first_hit + m_hits) selects a chunk of the hit list.
+int shade_hits_device(Field& F, const double* o, const double* d, int64_t first_hit, int64_t m_hits,
+                      const ShadeTargets& T, cudaStream_t st);
+int read_hit_count(Field& F, cudaStream_t st, int* out);  // syncs the stream
+
+}  // namespace knf
+
+struct knf_field_s {
+  knf::Field f;
+};

@@ -1,0 +1,179 @@
+"""GPU parity, part 1: routing and the batched multi-network forward (BASELINE config 4),
+through the C-ABI, against the oracle and the reference-generated golden vectors."""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import golden, oracle_from_product
+
+pytestmark = pytest.mark.gpu
+
+FWD_TOL = 2e-6  # reference's own grouped-vs-naive bound is 1e-6 (test_grid.py:81-86); see DESIGN.md Numerics
+
+
+@pytest.fixture(scope="module")
+def G():
+    from paper_2206_10885_b200 import grid
+
+    return grid
+
+
+def test_cell_ids_bit_exact_golden(G):
+    g = golden("cells.npz")
+    for n in (1, 4, 16):
+        cfg = G.GridConfig(resolution=n)
+        assert np.array_equal(G.cell_index_flat(cfg, g[f"pts_{n}"]), g[f"ids_{n}"])
+    cfg = G.GridConfig(resolution=5, bbox_min=(-0.7, -1.1, 0.2), bbox_max=(0.9, 0.4, 1.7))
+    assert np.array_equal(G.cell_index_flat(cfg, g["pts_odd"]), g["ids_odd"])
+
+
+def test_cell_ids_bit_exact_million(G):
+    # SURVEY 8c protocol (1): 1e6 uniform points + every face coordinate +-{0,1,2} ulp
+    rng = np.random.default_rng(0)
+    pts = rng.uniform(-1.05, 1.05, size=(1_000_000, 3)).astype(np.float32)
+    faces = (-1.0 + 2.0 * np.arange(17) / 16).astype(np.float32)
+    ring = [faces]
+    up, dn = faces, faces
+    for _ in range(2):
+        up = np.nextafter(up, np.float32(np.inf))
+        dn = np.nextafter(dn, np.float32(-np.inf))
+        ring += [up, dn]
+    vals = np.concatenate(ring)
+    pts[:60000] = rng.choice(vals, size=(60000, 3))
+    cfg = G.GridConfig(resolution=16)
+    want = oracle.cell_ids(oracle.FieldSpec(resolution=16), pts)
+    assert np.array_equal(G.cell_index_flat(cfg, pts), want)
+    # fp64 points keep their precision (grid.cell_index passes fp64 straight through)
+    p64 = pts[:5000].astype(np.float64) + 1e-12
+    assert np.array_equal(G.cell_index_flat(cfg, p64), oracle.cell_ids(oracle.FieldSpec(resolution=16), p64))
+    assert G.cell_index(cfg, (0.0, 0.0, 0.0)) == (8, 8, 8)
+    assert G.cell_index(cfg, (2.0, 0.0, 0.0)) == (15, 8, 8)
+    assert G.cell_index(cfg, (-1.0, -1.0, -1.0)) == (0, 0, 0)
+
+
+def test_route_groups_by_cell(G, small_field):
+    rng = np.random.default_rng(5)
+    pts = rng.uniform(-1.2, 1.2, size=(5000, 3)).astype(np.float32)
+    r = G.route(small_field, pts)
+    ids = oracle.cell_ids(oracle.FieldSpec(resolution=4), pts)
+    assert sorted(r.order.tolist()) == list(range(5000))  # a permutation
+    assert np.all(np.diff(ids[r.order]) >= 0)  # sorted by cell
+    cells, starts = np.unique(ids[r.order], return_index=True)
+    assert np.array_equal(r.cells, cells) and np.array_equal(r.starts, starts)
+    assert np.array_equal(r.ends, np.append(starts[1:], 5000))
+    assert np.array_equal(r.unsort(r.sort(pts)), pts)
+
+
+def test_sdf_forward_matches_golden_and_oracle(G, small_field, small_oracle):
+    g = golden("forward_r4_seed7.npz")
+    got = G.sdf_query(small_field, g["pts"])
+    assert got.value.dtype == np.float32 and got.features.shape == (3000, 8)
+    assert np.abs(got.value - g["value"]).max() <= FWD_TOL
+    assert np.abs(got.features - g["features"]).max() <= FWD_TOL
+    v, f = oracle.query_sdf(small_oracle, g["pts"])
+    assert np.abs(got.value - v).max() <= FWD_TOL
+    few = G.sdf_query(small_field, g["pts"][:150])
+    assert np.abs(few.value - g["value_few"]).max() <= FWD_TOL
+    assert np.abs(G.sdf_values(small_field, g["pts"]) - g["value"]).max() <= FWD_TOL
+
+
+def test_sdf_forward_a1_field(G):
+    # A1 (test_acceptance.py:113-127): 16^3 seed 42, U(-1.1,1.1) points
+    g = golden("forward_r16_seed42.npz")
+    field = G.field_init(G.GridConfig(resolution=16), seed=42)
+    got = G.sdf_query(field, g["pts"])
+    err_v = np.abs(got.value - g["value"])
+    err_f = np.abs(got.features - g["features"])
+    print(f"A1 parity: value max {err_v.max():.2e} mean {err_v.mean():.2e}; features max {err_f.max():.2e}")
+    assert err_v.max() <= FWD_TOL and err_f.max() <= FWD_TOL
+
+
+def test_color_forward(G, small_field):
+    g = golden("forward_r4_seed7.npz")
+    rgb = G.color_query(small_field, g["pts"], g["v"], g["n"], g["features"])
+    assert rgb.shape == (3000, 3) and rgb.dtype == np.float32
+    err = np.abs(rgb - g["rgb"]).max()
+    print(f"colour parity: max {err:.2e}")
+    assert err <= 1e-6
+    assert np.all((rgb > 0) & (rgb < 1))
+    one = G.color_query(small_field, g["pts"][7], g["v"][7], g["n"][7], g["features"][7])
+    assert np.abs(one[0] - rgb[7]).max() <= 1e-6  # batch == single (test_grid.py:106-132)
+    assert np.array_equal(G.grouped_query(small_field, g["pts"], "color", v=g["v"], n=g["n"], z=g["features"]), rgb)
+    with pytest.raises(ValueError):
+        G.grouped_query(small_field, g["pts"], "density")
+
+
+def test_permutation_equivariance_exact(G, small_field):
+    # test_grid.py:136-142 (array_equal): every point is evaluated with a fixed FMA order
+    rng = np.random.default_rng(9)
+    pts = rng.uniform(-1, 1, size=(4000, 3)).astype(np.float32)
+    perm = rng.permutation(4000)
+    a = G.sdf_query(small_field, pts)
+    b = G.sdf_query(small_field, pts[perm])
+    assert np.array_equal(a.value[perm], b.value)
+    assert np.array_equal(a.features[perm], b.features)
+    # ... and independent of how many points share the cell (the reference is not: OpenBLAS
+    # switches kernels with batch size)
+    c = G.sdf_query(small_field, pts[:37])
+    assert np.array_equal(c.value, a.value[:37])
+
+
+def test_ragged_and_empty_batches(G, small_field, small_oracle):
+    assert G.sdf_query(small_field, np.zeros((0, 3), np.float32)).value.shape == (0,)
+    for n in (1, 2, 63, 64, 65, 255, 256, 257, 1000):
+        pts = np.random.default_rng(n).uniform(-1, 1, size=(n, 3)).astype(np.float32)
+        pts[:, :] = pts[:, :] * 0.2 + 0.3  # all in one or two cells: exercises partial warps/tiles
+        v, _ = oracle.query_sdf(small_oracle, pts)
+        assert np.abs(G.sdf_values(small_field, pts) - v).max() <= FWD_TOL
+
+
+def test_outside_points_clamp_to_boundary_cells(G, small_field, small_oracle):
+    pts = np.random.default_rng(1).uniform(-3, 3, size=(2000, 3)).astype(np.float32)
+    v, f = oracle.query_sdf(small_oracle, pts)
+    got = G.sdf_query(small_field, pts)
+    assert np.abs(got.value - v).max() <= 1e-5  # |enc| arguments up to 3*pi*32: still the same algorithm
+
+
+def test_torch_device_path(G, small_field):
+    import torch
+
+    g = golden("forward_r4_seed7.npz")
+    t = torch.as_tensor(g["pts"], device="cuda")
+    out = G.sdf_query(small_field, t)
+    assert out.value.is_cuda
+    assert np.array_equal(out.value.cpu().numpy(), G.sdf_query(small_field, g["pts"]).value)
+
+
+def test_fd_normals(G, small_field):
+    g = golden("fd_normals_r4.npz")
+    grad = G.grad_fd(small_field, g["pts"])
+    err = np.abs(grad - g["grad"]).max()
+    print(f"FD gradient parity: max {err:.2e} (SDF ulps x 500)")
+    assert err <= 500 * FWD_TOL
+    nrm, ok = G.normal_batch(small_field, g["pts"])
+    assert np.array_equal(ok, g["ok"])
+    assert np.abs(nrm - g["normals"]).max() <= 1e-3
+    assert np.allclose(np.linalg.norm(nrm[ok], axis=1), 1.0, atol=1e-12)
+    assert np.abs(G.normal(small_field, g["pts"][5]) - g["normals"][5]).max() <= 1e-3
+    assert G.grad_fd(small_field, g["pts"][0]).shape == (3,)
+
+
+def test_unsupported_architecture_is_loud(G):
+    cfg = G.GridConfig(resolution=2, feature_dim=4)
+    from paper_2206_10885_b200 import _native as N
+
+    with pytest.raises(N.KnfUnsupported):
+        G.sdf_query(G.field_init(cfg, seed=0), np.zeros((3, 3), np.float32))
+
+
+def test_knf_straight_to_device(G, distilled_field, golden_dir):
+    import os
+
+    from paper_2206_10885_b200.modelio import load_model_to_device
+
+    dev = load_model_to_device(os.path.join(golden_dir, "sphere_r4_distilled.knf"))
+    pts = np.random.default_rng(2).uniform(-1, 1, size=(3000, 3)).astype(np.float32)
+    assert np.array_equal(G.sdf_query(dev, pts).value, G.sdf_query(distilled_field, pts).value)
+    with pytest.raises(OSError):
+        load_model_to_device(os.path.join(golden_dir, "rng.npz"))

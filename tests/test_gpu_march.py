@@ -1,0 +1,220 @@
+"""GPU parity, part 2: ray generation, slabs, the wavefront sphere trace, shading and frames
+(BASELINE configs 1-3 in miniature), through the C-ABI."""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import golden, oracle_from_product
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2206_10885_b200 import surface
+
+    return surface
+
+
+@pytest.fixture(scope="module")
+def cams():
+    from paper_2206_10885_b200 import cameras
+
+    return cameras
+
+
+def test_pixel_rays_bit_exact(cams):
+    for (w, h, pos) in [(64, 48, (1.2, 0.9, 2.0)), (7, 5, (0, 0, 2.5)), (33, 65, (-2, 0.3, 0.4))]:
+        pose = cams.look_at_pose(pos, (0, 0, 0), (0, 1, 0), np.deg2rad(35), w, h)
+        ocam = oracle.camera_look_at(pos, (0, 0, 0), (0, 1, 0), np.deg2rad(35), w, h)
+        assert np.array_equal(pose.rotation, ocam.rotation)
+        o, d = cams.pixel_rays(pose)
+        oo, od = oracle.camera_rays(ocam)
+        assert np.array_equal(o, oo) and np.array_equal(d, od)
+    rng = np.random.default_rng(0)
+    pix = np.stack([rng.integers(0, 33, 500), rng.integers(0, 65, 500)], axis=1)
+    jit = rng.uniform(size=(500, 2))
+    o, d = cams.pixel_rays(pose, pix, jit)
+    oo, od = oracle.camera_rays(ocam, pix, jit)
+    assert np.array_equal(d, od)
+
+
+def test_ray_aabb(S):
+    rng = np.random.default_rng(1)
+    o = rng.uniform(-3, 3, size=(20000, 3))
+    d = rng.normal(size=(20000, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    d[:500, 0] = 0.0  # axis-parallel rays
+    d[200:700, 1] = 0.0
+    o[:100, 0] = 1.0  # on the slab boundary
+    tn, tf, hit = S.ray_aabb_batch(o, d, (-1, -1, -1), (1, 1, 1))
+    otn, otf, ohit = oracle.slab_intersect(o, d, (-1, -1, -1), (1, 1, 1))
+    assert np.array_equal(hit, ohit)
+    assert np.array_equal(tn, otn) and np.array_equal(tf, otf)
+    assert S.ray_aabb(S.Ray((0, 0, -2), (0, 0, 1)), (-1, -1, -1), (1, 1, 1)) == (1.0, 3.0)
+    assert S.ray_aabb(S.Ray((0, 3, -2), (0, 0, 1)), (-1, -1, -1), (1, 1, 1)) is None
+
+
+def _rays(w, h, pos=(0, 0, 2.5), fov=40):
+    cam = oracle.camera_look_at(pos, (0, 0, 0), (0, 1, 0), np.deg2rad(fov), w, h)
+    o, d = oracle.camera_rays(cam)
+    tn, tf, inside = oracle.slab_intersect(o, d, (-1, -1, -1), (1, 1, 1))
+    return o, d, np.where(inside, tn, 1.0), np.where(inside, tf, 0.0)
+
+
+def test_lockstep_march_random_init(S):
+    """SURVEY 8c protocol (3): the reference's own march loop (oracle.march) driven by GPU SDF
+    evaluations, compared round by round with the pure-CPU march.  While both marches hold the
+    same ray set the per-round distances must agree to forward tolerance; this proves the
+    kernels independent of the chaos that a random-init SDF adds to end-to-end frames."""
+    from paper_2206_10885_b200 import grid
+
+    field = grid.field_init(grid.GridConfig(resolution=16), seed=0)
+    ofield = oracle_from_product(field)
+    o, d, tn, tf = _rays(40, 40)
+    log_cpu, log_gpu = [], []
+    cfg = oracle.MarchSettings(max_steps=24)
+    oracle.march(oracle.FieldTraceable(ofield), o, d, tn, tf, cfg, trace_log=log_cpu)
+    oracle.march(S.FieldSurface(field), o, d, tn, tf, cfg, trace_log=log_gpu)
+    # round 0 is identical input by construction; later rounds agree until the first decision flip
+    compared = 0
+    worst = 0.0
+    for (ra, ta, da), (rb, tb, db) in zip(log_cpu, log_gpu):
+        if len(ra) != len(rb) or not np.array_equal(ra, rb):
+            break
+        same_t = ta == tb
+        worst = max(worst, float(np.abs(da[same_t] - db[same_t]).max()))
+        compared += int(same_t.sum())
+    print(f"lock-step: {compared} evaluations compared at identical t, worst |d_gpu - d_cpu| = {worst:.2e}")
+    assert compared >= 1600
+    assert worst <= 5e-6
+
+
+def test_march_distilled_matches_oracle(S, distilled_field, distilled_oracle):
+    o, d, tn, tf = _rays(96, 96)
+    res = S.march_rays(S.FieldSurface(distilled_field), o, d, tn, tf, S.RenderSettings())
+    ref = oracle.march(oracle.FieldTraceable(distilled_oracle), o, d, tn, tf, oracle.MarchSettings())
+    agree = (res.hit == ref.hit).mean()
+    both = res.hit & ref.hit
+    drel = np.abs(res.t[both] - ref.t[both]) / ref.t[both]
+    print(f"march distilled: hit agreement {agree:.4%}, depth rel max {drel.max():.2e}, steps equal {(res.steps == ref.steps).mean():.4%}")
+    assert agree >= 0.999
+    assert drel.max() <= 1e-4
+    assert (res.steps == ref.steps).mean() >= 0.995
+    assert np.abs(res.position[both] - ref.position[both]).max() <= 1e-4
+    assert np.all(res.steps <= 128)
+    # misses keep t = 0 and position = origin, like the reference
+    assert np.all(res.t[~res.hit] == 0) and np.array_equal(res.position[~res.hit], o[~res.hit])
+
+
+def test_frame_distilled_vs_golden(S, cams, distilled_field):
+    """End-to-end FrameBuffers vs the reference's render of the same field + camera
+    (north_star bar: hit >= 99.9 %, depth <= 1e-4 rel, normal & RGB <= 1e-3)."""
+    g = golden("frame_distilled_96.npz")
+    pose = cams.look_at_pose((0, 0, 2.5), (0, 0, 0), (0, 1, 0), np.deg2rad(40), 96, 96)
+    fb = S.render_frame(S.FieldSurface(distilled_field), pose, S.RenderSettings())
+    assert fb.color.dtype == np.float32 and fb.color.shape == (96, 96, 3)
+    assert fb.depth.dtype == np.float32 and fb.hit.dtype == bool
+    agree = (fb.hit == g["hit"]).mean()
+    both = fb.hit & g["hit"]
+    drel = (np.abs(fb.depth[both] - g["depth"][both]) / g["depth"][both]).max()
+    nerr = np.abs(fb.normal - g["normal"])[both]
+    cerr = np.abs(fb.color - g["color"])[both]
+    print(f"frame distilled 96^2: hit {agree:.4%}, depth rel {drel:.2e}, normal max {nerr.max():.2e} "
+          f"(>1e-3 on {(nerr.max(axis=1) > 1e-3).mean():.3%}), rgb max {cerr.max():.2e}")
+    assert agree >= 0.999
+    assert drel <= 1e-4
+    assert cerr.max() <= 1e-3
+    # FD normals amplify SDF ulps by 500/|g|: the reference disagrees with ITSELF by 1.0e-3 between
+    # tile_rows=32 and 128 on this field (DESIGN.md Numerics), so the bound is 2e-3 max, 1e-3 for 99.9 %
+    assert nerr.max() <= 2e-3 and (nerr.max(axis=1) <= 1e-3).mean() >= 0.999
+    assert np.all(np.isinf(fb.depth[~fb.hit])) and np.all(fb.normal[~fb.hit] == 0)
+    assert np.all(fb.color[~fb.hit] == 1.0)
+    nn = np.linalg.norm(fb.normal[fb.hit], axis=1)
+    assert np.allclose(nn, 1.0, atol=1e-6)
+
+
+def test_frame_supersampled_vs_golden(S, cams, distilled_field):
+    g = golden("frame_distilled_ss2.npz")
+    pose = cams.look_at_pose((1.2, 0.9, 2.0), (0, 0, 0), (0, 1, 0), np.deg2rad(35), 40, 30)
+    fb = S.render_frame(S.FieldSurface(distilled_field), pose, S.RenderSettings(), background=(0.2, 0.4, 0.6), supersample=2)
+    agree = (fb.hit == g["hit"]).mean()
+    both = fb.hit & g["hit"]
+    print(f"frame ss2: hit {agree:.4%}, rgb max {np.abs(fb.color - g['color'])[both].max():.2e}")
+    assert agree >= 0.995
+    assert (np.abs(fb.depth[both] - g["depth"][both]) / g["depth"][both]).max() <= 1e-4
+    assert np.abs(fb.color - g["color"])[both].max() <= 2e-3
+    bgpix = ~fb.hit & ~g["hit"]
+    assert np.abs(fb.color[bgpix] - g["color"][bgpix]).max() <= 1e-6
+
+
+def test_frame_banding_and_abort(S, cams, distilled_field):
+    pose = cams.look_at_pose((0, 0, 2.5), (0, 0, 0), (0, 1, 0), np.deg2rad(40), 50, 37)
+    fs = S.FieldSurface(distilled_field)
+    whole = S.render_frame(fs, pose)
+    polls = []
+    banded = S.render_frame(fs, pose, tile_rows=8, abort_check=lambda: polls.append(1) and False)
+    assert len(polls) == 5
+    for k in ("color", "depth", "normal", "hit"):
+        assert np.array_equal(getattr(whole, k), getattr(banded, k)), k  # banding-invariant, like thread count in the reference
+    with pytest.raises(S.RenderAborted):
+        S.render_frame(fs, pose, tile_rows=8, abort_check=lambda: True)
+    with pytest.raises(ValueError):
+        S.render_frame(fs, pose, supersample=0)
+    img = S.pass_image(whole, "normal")
+    assert img.shape == (37, 50, 3) and np.all(img[~whole.hit] == 0)
+    with pytest.raises(ValueError):
+        S.pass_image(whole, "albedo")
+
+
+def test_frame_random_init_reported(S, cams):
+    """BASELINE config 1 in miniature (64^2).  A random-init SDF makes t <- t + 0.8 d an expanding map, so
+    1-ulp SDF differences flip hit decisions (the reference flips against itself, DESIGN.md
+    Numerics).  Parity here is statistical; the strict bar is carried by the distilled field and
+    by the lock-step test above."""
+    from paper_2206_10885_b200 import grid
+
+    g = golden("frame_random16_64.npz")
+    field = grid.field_init(grid.GridConfig(resolution=16), seed=0)
+    pose = cams.look_at_pose((0, 0, 2.5), (0, 0, 0), (0, 1, 0), np.deg2rad(40), 64, 64)
+    fb = S.render_frame(S.FieldSurface(field), pose)
+    agree = (fb.hit == g["hit"]).mean()
+    both = fb.hit & g["hit"]
+    print(f"frame random-init 64^2: hit agreement {agree:.4%}; hits gpu {fb.hit.sum()} ref {g['hit'].sum()}; both {both.sum()}")
+    assert agree >= 0.985
+    assert abs(int(fb.hit.sum()) - int(g["hit"].sum())) <= 0.25 * int(g["hit"].sum()) + 5
+
+
+def test_shade_matches_oracle(S, distilled_field, distilled_oracle):
+    o, d, tn, tf = _rays(64, 64)
+    ref = oracle.march(oracle.FieldTraceable(distilled_oracle), o, d, tn, tf, oracle.MarchSettings())
+    pts, dirs = ref.position[ref.hit], d[ref.hit]
+    col, nrm = S.FieldSurface(distilled_field).shade(pts, dirs)
+    ocol, onrm = oracle.FieldTraceable(distilled_oracle).shade(pts, dirs)
+    print(f"shade: normal max {np.abs(nrm - onrm).max():.2e}, rgb max {np.abs(col - ocol).max():.2e} on {len(pts)} hits")
+    assert np.abs(col - ocol).max() <= 1e-3
+    assert (np.abs(nrm - onrm).max(axis=1) <= 1e-3).mean() >= 0.999
+
+
+def test_sphere_trace_single_ray(S, distilled_field):
+    fs = S.FieldSurface(distilled_field)
+    hit = S.sphere_trace(fs, S.Ray((0, 0, -2.0), (0, 0, 1.0)), 1.0, 3.0, S.RenderSettings())
+    assert hit is not None and abs(hit.t - 1.5) <= 3e-2 and hit.steps_taken <= 128
+    assert abs(np.linalg.norm(hit.normal) - 1) <= 1e-9 and hit.normal[2] < -0.9
+    assert S.sphere_trace(fs, S.Ray((0.95, 0.95, -2.0), (0, 0, 1.0)), 1.0, 3.0, S.RenderSettings()) is None
+    with pytest.raises(ValueError):
+        S.sphere_trace(fs, S.Ray((0, 0, -2.0), (0, 0, 1.0)), 3.0, 1.0, S.RenderSettings())
+    with pytest.raises(TypeError):
+        S.march_rays(object(), np.zeros((1, 3)), np.zeros((1, 3)), np.zeros(1), np.ones(1), S.RenderSettings())
+
+
+def test_reference_tracer_accepts_gpu_surface(S, distilled_field, distilled_oracle):
+    """The drop-in boundary is the traceable-surface protocol (surface.py:1-7): the reference-style
+    CPU loop (here: the oracle's) must run unmodified on our FieldSurface."""
+    o, d, tn, tf = _rays(32, 32)
+    a = oracle.trace_shade(S.FieldSurface(distilled_field), o, d, oracle.MarchSettings())
+    b = oracle.trace_shade(oracle.FieldTraceable(distilled_oracle), o, d, oracle.MarchSettings())
+    assert (a.hit == b.hit).mean() >= 0.999
+    both = a.hit & b.hit
+    assert np.abs(a.t[both] - b.t[both]).max() <= 1e-4
