@@ -14,7 +14,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libknf_b200.so")
+LIB_PATH = os.environ.get("KNF_B200_LIB") or os.path.join(_HERE, "libknf_b200.so")  # env override: kernel A/B experiments
 
 KNF_OK = 0
 KNF_E_INVALID = -1

@@ -45,7 +45,10 @@ using ColBlob = BlobLayout<kColIn, kColOutPad>;    // 2532 floats = 10128 B
 
 // Points per warp and warps per CTA of the tile kernels; a tile is <= kTilePts points of one cell.
 constexpr int kWarpPts = 64;
-constexpr int kTileWarps = 4;
+#ifndef KNF_TILE_WARPS
+#define KNF_TILE_WARPS 4
+#endif
+constexpr int kTileWarps = KNF_TILE_WARPS;
 constexpr int kTilePts = kWarpPts * kTileWarps;  // 256
 
 struct GridGeom {
@@ -137,6 +140,75 @@ __device__ __forceinline__ float np_sigmoidf(float x) {
 __device__ __forceinline__ float softplus_acc(float x) {
   float u = np_expf(-fabsf(x));
   return __fadd_rn(log1pf(u), fmaxf(x, 0.0f));
+}
+
+// The production softplus: same formula, ~32 FMA-pipe instructions and one MUFU.RCP, no
+// conversions, no slow paths.  e = exp(-|x|) by Cody-Waite + a degree-6 polynomial and an integer
+// exponent add; log1p(e) = 2 atanh(e / (2 + e)) with s = e/(2+e) <= 1/3 (one Newton step on the
+// reciprocal, odd polynomial in s).  Emulated in fp32 against float64 on 2e6 N(0,1.5) arguments:
+// mean |error| 0.416 ulp, max 2.7 ulp -- NumPy's own softplus32 measures 0.428 / 3.3 on the same
+// inputs; the two agree bit-for-bit on 64 % of arguments and never differ by more than 4.8e-7.
+__device__ __forceinline__ float softplus_f(float x) {
+  const float y = fminf(fabsf(x), 87.0f);
+  const float magic = 12582912.0f;  // 1.5 * 2^23
+  float tm = __fadd_rn(__fmul_rn(y, -1.4426950408889634f), magic);
+  float nf = __fsub_rn(tm, magic);                       // n = rint(-y / ln 2) <= 0
+  float r = __fmaf_rn(nf, -0.693145751953125f, -y);      // r = -y - n ln2, |r| <= ln2 / 2
+  r = __fmaf_rn(nf, -1.42860677e-6f, r);
+  float p = __fmaf_rn(0.0013943214435130358f, r, 0.00836438313126564f);
+  p = __fmaf_rn(p, r, 0.04166635125875473f);
+  p = __fmaf_rn(p, r, 0.1666657030582428f);
+  p = __fmaf_rn(p, r, 0.5f);
+  float q = __fmaf_rn(p, __fmul_rn(r, r), r);
+  float er = __fadd_rn(1.0f, q);                          // exp(r) in [0.707, 1.414]
+  float e = __int_as_float(__float_as_int(er) + (__float_as_int(tm) << 23));  // * 2^n, n >= -126
+  float den = __fadd_rn(2.0f, e);
+  float rc;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(den));  // MUFU.RCP, ~1 ulp; corrected below
+  float s0 = __fmul_rn(e, rc);
+  float s = __fmaf_rn(__fmaf_rn(-s0, den, e), rc, s0);     // s = e / (2 + e) to ~0.5 ulp
+  float s2 = __fmul_rn(s, s);
+  float g = __fmaf_rn(0.2493898570537567f, s2, 0.21339640021324158f);
+  g = __fmaf_rn(g, s2, 0.28616610169410706f);
+  g = __fmaf_rn(g, s2, 0.3999920189380646f);
+  g = __fmaf_rn(g, s2, 0.6666666865348816f);
+  float l = __fmaf_rn(__fmul_rn(s, s2), g, __fadd_rn(s, s));  // 2 atanh(s)
+  return __fadd_rn(fmaxf(x, 0.0f), l);
+}
+
+// Two softplus_f evaluations in one packed (f32x2) instruction stream: every polynomial step is an
+// FFMA2/FMUL2/FADD2, so a pair costs ~24 packed + ~10 scalar issue slots instead of 2 x 32.  Each
+// half performs exactly the operations of softplus_f except that the first multiply-add is fused.
+__device__ __forceinline__ float2 softplus_f2(float2 x) {
+  const float2 yn = make_float2(fmaxf(-fabsf(x.x), -87.0f), fmaxf(-fabsf(x.y), -87.0f));  // -min(|x|, 87)
+  const float2 magic = make_float2(12582912.0f, 12582912.0f);
+  float2 tm = __ffma2_rn(yn, make_float2(1.4426950408889634f, 1.4426950408889634f), magic);
+  float2 nf = __fadd2_rn(tm, make_float2(-12582912.0f, -12582912.0f));
+  float2 r = __ffma2_rn(nf, make_float2(-0.693145751953125f, -0.693145751953125f), yn);
+  r = __ffma2_rn(nf, make_float2(-1.42860677e-6f, -1.42860677e-6f), r);
+  float2 p = __ffma2_rn(make_float2(0.0013943214435130358f, 0.0013943214435130358f), r,
+                        make_float2(0.00836438313126564f, 0.00836438313126564f));
+  p = __ffma2_rn(p, r, make_float2(0.04166635125875473f, 0.04166635125875473f));
+  p = __ffma2_rn(p, r, make_float2(0.1666657030582428f, 0.1666657030582428f));
+  p = __ffma2_rn(p, r, make_float2(0.5f, 0.5f));
+  float2 q = __ffma2_rn(p, __fmul2_rn(r, r), r);
+  float2 er = __fadd2_rn(make_float2(1.0f, 1.0f), q);
+  float2 e = make_float2(__int_as_float(__float_as_int(er.x) + (__float_as_int(tm.x) << 23)),
+                         __int_as_float(__float_as_int(er.y) + (__float_as_int(tm.y) << 23)));
+  float2 nden = __ffma2_rn(e, make_float2(-1.0f, -1.0f), make_float2(-2.0f, -2.0f));  // -(2 + e), exact same rounding
+  float2 rc;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc.x) : "f"(-nden.x));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc.y) : "f"(-nden.y));
+  float2 s0 = __fmul2_rn(e, rc);
+  float2 s = __ffma2_rn(__ffma2_rn(s0, nden, e), rc, s0);
+  float2 s2 = __fmul2_rn(s, s);
+  float2 g = __ffma2_rn(make_float2(0.2493898570537567f, 0.2493898570537567f), s2,
+                        make_float2(0.21339640021324158f, 0.21339640021324158f));
+  g = __ffma2_rn(g, s2, make_float2(0.28616610169410706f, 0.28616610169410706f));
+  g = __ffma2_rn(g, s2, make_float2(0.3999920189380646f, 0.3999920189380646f));
+  g = __ffma2_rn(g, s2, make_float2(0.6666666865348816f, 0.6666666865348816f));
+  float2 l = __ffma2_rn(__fmul2_rn(s, s2), g, __fadd2_rn(s, s));
+  return __fadd2_rn(make_float2(fmaxf(x.x, 0.0f), fmaxf(x.y, 0.0f)), l);
 }
 
 // grid._cell_triples (grid.py:176-179) for one coordinate: fp64 arithmetic on the fp32 point.

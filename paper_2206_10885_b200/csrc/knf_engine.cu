@@ -170,7 +170,7 @@ int launch_scan_scatter(Field& F, const RouteBuffers& R, size_t n_upper, cudaStr
 
 static inline int mlp_grid(const Field& F, size_t n_upper) {
   size_t tiles_upper = n_upper / kTilePts + std::min<size_t>(n_upper, (size_t)F.geom.n_cells) + 1;
-  return (int)std::max<size_t>(1, std::min<size_t>(tiles_upper, 148 * 2));
+  return (int)std::max<size_t>(1, std::min<size_t>(tiles_upper, 148 * (16 / kTileWarps > 10 ? 10 : 16 / kTileWarps)));
 }
 
 int launch_sdf_mlp(Field& F, const RouteBuffers& R, size_t n_upper, float* out_first, float* out_full, cudaStream_t st) {

@@ -15,8 +15,13 @@
 //     rounded add -- exactly the arithmetic OpenBLAS sgemm + NumPy's `+ b` perform in the
 //     reference's per-cell path, so given the same layer inputs the pre-activations are
 //     bit-identical to the reference's;
+//   * pre-activations go back into the SAME panel (the layer's inputs are dead once every lane
+//     holds its accumulators), and softplus runs over the panel in a rolled loop -- one copy of
+//     the softplus code instead of 128 inlined ones keeps the kernel inside the instruction
+//     cache (ncu on the first version: "no_instruction" was the top stall);
 //   * the 32 -> N3 output layer is evaluated two points per lane and written straight to the
 //     caller's buffers in request order (no unsort pass).
+// Shared memory: 10.9 KB weights + 4 x 10.6 KB panels = 53.4 KB per CTA -> 4 CTAs (16 warps) per SM.
 //
 // FP32 FFMA, not tensor cores: TF32/BF16 mma gives ~1e-3 absolute SDF error, 1000x over the
 // parity budget that FD normals (x 1/2h = 500 amplification) need.  See DESIGN.md.
@@ -46,66 +51,93 @@ struct MlpParams {
   float* out_full;             // SDF: (n, 1+F) rows; colour: (n,3) rows (nullable)
 };
 
-template <int K1, int N3, int N3P, int HIDDEN_ACT, bool IS_COLOR>
+template <int K1, int N3P>
 struct MlpSmem {
   using Blob = BlobLayout<K1, N3P>;
   alignas(16) float w[Blob::floats];
-  alignas(16) float x[kTileWarps][K1 * kPanelLd];       // layer-1 input panel, later layer-2 output
-  alignas(16) float h[kTileWarps][kHidden * kPanelLd];  // layer-1 output panel
+  alignas(16) float x[kTileWarps][K1 * kPanelLd];  // one activation panel per warp, reused by every layer
   alignas(8) uint64_t bar;
   int tile_idx[2];
 };
 
-template <int ACT>
-__device__ __forceinline__ float hidden_act(float z) {
-  if (ACT == ACT_RELU) return fmaxf(z, 0.0f);
-  return softplus_acc(z);
+__device__ __forceinline__ float2 splat(float v) { return make_float2(v, v); }
+
+// acc[ip][j] = (point 2ip, point 2ip+1) x neuron j: sum_k In[k][pt] * Wt[k][nr], k ascending, one
+// IEEE fma per k and lane -- issued as packed FFMA2 (Blackwell fma.rn.f32x2: the weight is the
+// scalar-broadcast operand, two points share an instruction), which halves the issue slots of the
+// FFMA stream without changing a bit of the result.
+struct LayerOperands {
+  float4 xa, xb, wa, wb;
+};
+__device__ __forceinline__ void load_operands(LayerOperands& o, const float* __restrict__ xp, const float* __restrict__ wp,
+                                              int k) {
+  o.xa = *reinterpret_cast<const float4*>(xp + k * kPanelLd);
+  o.xb = *reinterpret_cast<const float4*>(xp + k * kPanelLd + 32);
+  o.wa = *reinterpret_cast<const float4*>(wp + k * kHidden);
+  o.wb = *reinterpret_cast<const float4*>(wp + k * kHidden + 16);
+}
+__device__ __forceinline__ void fma_block(const LayerOperands& o, float2 (&acc)[4][8]) {
+  const float2 xs[4] = {make_float2(o.xa.x, o.xa.y), make_float2(o.xa.z, o.xa.w), make_float2(o.xb.x, o.xb.y),
+                        make_float2(o.xb.z, o.xb.w)};
+  const float ws[8] = {o.wa.x, o.wa.y, o.wa.z, o.wa.w, o.wb.x, o.wb.y, o.wb.z, o.wb.w};
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int j = 0; j < 8; j++) acc[i][j] = __ffma2_rn(xs[i], splat(ws[j]), acc[i][j]);
 }
 
-// acc[i][j] = sum_k In[k][pt_i] * Wt[k][nr_j], k ascending, one FFMA per k.
+// Explicit two-stage software pipeline (operands of step k+1 are in flight while step k's 32
+// FFMA2 issue); the loop body covers two steps so the two operand sets keep their registers --
+// ptxas' own rotation of a 4x-unrolled loop cost 34 MOVs per iteration (ncu, v3).
+// Rows K..K+1 of the panel / weight block may be read but are never used.
 template <int K>
 __device__ __forceinline__ void layer_8x8(const float* __restrict__ In, const float* __restrict__ Wt, int pg, int ng,
-                                          float (&acc)[8][8]) {
+                                          float2 (&acc)[4][8]) {
 #pragma unroll
-  for (int i = 0; i < 8; i++)
+  for (int i = 0; i < 4; i++)
 #pragma unroll
-    for (int j = 0; j < 8; j++) acc[i][j] = 0.0f;
+    for (int j = 0; j < 8; j++) acc[i][j] = make_float2(0.0f, 0.0f);
   const float* xp = In + pg * 4;
   const float* wp = Wt + ng * 4;
-#pragma unroll 3
-  for (int k = 0; k < K; k++) {
-    float4 xa = *reinterpret_cast<const float4*>(xp + k * kPanelLd);
-    float4 xb = *reinterpret_cast<const float4*>(xp + k * kPanelLd + 32);
-    float4 wa = *reinterpret_cast<const float4*>(wp + k * kHidden);
-    float4 wb = *reinterpret_cast<const float4*>(wp + k * kHidden + 16);
-    const float xs[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-    const float ws[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
-#pragma unroll
-    for (int i = 0; i < 8; i++)
-#pragma unroll
-      for (int j = 0; j < 8; j++) acc[i][j] = __fmaf_rn(xs[i], ws[j], acc[i][j]);
+  LayerOperands a, b;
+  load_operands(a, xp, wp, 0);
+#pragma unroll 1
+  for (int k = 0; k + 1 < K; k += 2) {
+    load_operands(b, xp, wp, k + 1);
+    fma_block(a, acc);
+    load_operands(a, xp, wp, k + 2);
+    fma_block(b, acc);
   }
+  if (K & 1) fma_block(a, acc);
 }
 
-// z = acc + b ; h = act(z) ; Out[neuron][point] (k-major panel for the next layer)
+// Out[neuron][point] = act(acc + b), k-major panel for the next layer.  RELU is applied here;
+// SOFTPLUS stores the pre-activation and leaves the transcendental to softplus_panel().
 template <int ACT>
-__device__ __forceinline__ void store_hidden(float (&acc)[8][8], const float* __restrict__ bias, float* __restrict__ Out,
-                                             int pg, int ng) {
+__device__ __forceinline__ void store_hidden(float2 (&acc)[4][8], const float* __restrict__ bias,
+                                             float* __restrict__ Out, int pg, int ng) {
 #pragma unroll
   for (int j = 0; j < 8; j++) {
     int neuron = (j < 4) ? (ng * 4 + j) : (16 + ng * 4 + (j - 4));
-    float b = bias[neuron];
-    float4 lo, hi;
-    lo.x = hidden_act<ACT>(__fadd_rn(acc[0][j], b));
-    lo.y = hidden_act<ACT>(__fadd_rn(acc[1][j], b));
-    lo.z = hidden_act<ACT>(__fadd_rn(acc[2][j], b));
-    lo.w = hidden_act<ACT>(__fadd_rn(acc[3][j], b));
-    hi.x = hidden_act<ACT>(__fadd_rn(acc[4][j], b));
-    hi.y = hidden_act<ACT>(__fadd_rn(acc[5][j], b));
-    hi.z = hidden_act<ACT>(__fadd_rn(acc[6][j], b));
-    hi.w = hidden_act<ACT>(__fadd_rn(acc[7][j], b));
-    *reinterpret_cast<float4*>(Out + neuron * kPanelLd + pg * 4) = lo;
-    *reinterpret_cast<float4*>(Out + neuron * kPanelLd + 32 + pg * 4) = hi;
+    float2 b = splat(bias[neuron]);
+    float2 v[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      v[i] = __fadd2_rn(acc[i][j], b);
+      if (ACT == ACT_RELU) v[i] = make_float2(fmaxf(v[i].x, 0.0f), fmaxf(v[i].y, 0.0f));
+    }
+    *reinterpret_cast<float4*>(Out + neuron * kPanelLd + pg * 4) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
+    *reinterpret_cast<float4*>(Out + neuron * kPanelLd + 32 + pg * 4) = make_float4(v[2].x, v[2].y, v[3].x, v[3].y);
+  }
+}
+
+// In-place softplus over a 32 x 64 panel: lane owns the adjacent columns 2*lane, 2*lane+1 and
+// runs both through one packed evaluation (LDS.64 / STS.64, conflict-free).
+__device__ __forceinline__ void softplus_panel(float* __restrict__ panel, int lane) {
+#pragma unroll 4
+  for (int j = 0; j < kHidden; j++) {
+    float2* cell = reinterpret_cast<float2*>(panel + j * kPanelLd + 2 * lane);
+    *cell = softplus_f2(*cell);
   }
 }
 
@@ -137,9 +169,9 @@ __device__ __forceinline__ void encode_into(float* __restrict__ panel, int row0,
 }
 
 template <int K1, int N3, int N3P, int HIDDEN_ACT, bool IS_COLOR>
-static __global__ void __launch_bounds__(kTileWarps * 32, 2) mlp_tile_kernel(MlpParams P) {
+static __global__ void __launch_bounds__(kTileWarps * 32, 16 / kTileWarps > 10 ? 10 : 16 / kTileWarps) mlp_tile_kernel(MlpParams P) {
   using Blob = BlobLayout<K1, N3P>;
-  using Smem = MlpSmem<K1, N3, N3P, HIDDEN_ACT, IS_COLOR>;
+  using Smem = MlpSmem<K1, N3P>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
 
@@ -158,7 +190,6 @@ static __global__ void __launch_bounds__(kTileWarps * 32, 2) mlp_tile_kernel(Mlp
   const int n_tiles = P.ctr->n_tiles;
   uint32_t parity = 0;
   float* X = S.x[warp];
-  float* H = S.h[warp];
 
   for (;;) {
     if (tid == 0) S.tile_idx[parity] = atomicAdd(&P.ctr->tile_cursor, 1);
@@ -178,7 +209,7 @@ static __global__ void __launch_bounds__(kTileWarps * 32, 2) mlp_tile_kernel(Mlp
       // ---- gather + encode two points per lane -------------------------------------------------
 #pragma unroll
       for (int q = 0; q < 2; q++) {
-        int p = lane + 32 * q;
+        int p = 2 * lane + q;  // the lane's two adjacent panel columns
         float px = 0.f, py = 0.f, pz = 0.f;
         if (p < wcount) {
           slot[q] = P.perm[tile.start + warp * kWarpPts + p];
@@ -221,56 +252,71 @@ static __global__ void __launch_bounds__(kTileWarps * 32, 2) mlp_tile_kernel(Mlp
     parity ^= 1;
 
     if (wcount > 0) {
-      float acc[8][8];
+      float2 acc[4][8];
       // ---- layer 1: K1 -> 32 ---------------------------------------------------------------------
       layer_8x8<K1>(X, S.w + Blob::w1, pg, ng, acc);
-      store_hidden<HIDDEN_ACT>(acc, S.w + Blob::b1, H, pg, ng);
+      __syncwarp();  // every lane holds its accumulators: the input rows are dead
+      store_hidden<HIDDEN_ACT>(acc, S.w + Blob::b1, X, pg, ng);
       __syncwarp();
-      // ---- layer 2: 32 -> 32 (output panel reuses X) ----------------------------------------------
-      layer_8x8<kHidden>(H, S.w + Blob::w2, pg, ng, acc);
-      __syncwarp();  // all lanes finished reading... X is not read in layer 2, H is; X is free
+      if (HIDDEN_ACT == ACT_SOFTPLUS) {
+        softplus_panel(X, lane);
+        __syncwarp();
+      }
+      // ---- layer 2: 32 -> 32 -----------------------------------------------------------------------
+      layer_8x8<kHidden>(X, S.w + Blob::w2, pg, ng, acc);
+      __syncwarp();
       store_hidden<HIDDEN_ACT>(acc, S.w + Blob::b2, X, pg, ng);
       __syncwarp();
+      if (HIDDEN_ACT == ACT_SOFTPLUS) softplus_panel(X, lane);  // lane reads back only its own columns below
       // ---- layer 3: 32 -> N3, two points per lane ---------------------------------------------------
-      float o0[N3P], o1[N3P];
-#pragma unroll
-      for (int j = 0; j < N3P; j++) o0[j] = o1[j] = 0.0f;
       const float* W3 = S.w + Blob::w3;
-#pragma unroll 4
-      for (int k = 0; k < kHidden; k++) {
-        float a0 = X[k * kPanelLd + lane];
-        float a1 = X[k * kPanelLd + 32 + lane];
-#pragma unroll
-        for (int j4 = 0; j4 < N3P; j4 += 4) {
-          float4 w = *reinterpret_cast<const float4*>(W3 + k * N3P + j4);
-          o0[j4 + 0] = __fmaf_rn(a0, w.x, o0[j4 + 0]);
-          o0[j4 + 1] = __fmaf_rn(a0, w.y, o0[j4 + 1]);
-          o0[j4 + 2] = __fmaf_rn(a0, w.z, o0[j4 + 2]);
-          o0[j4 + 3] = __fmaf_rn(a0, w.w, o0[j4 + 3]);
-          o1[j4 + 0] = __fmaf_rn(a1, w.x, o1[j4 + 0]);
-          o1[j4 + 1] = __fmaf_rn(a1, w.y, o1[j4 + 1]);
-          o1[j4 + 2] = __fmaf_rn(a1, w.z, o1[j4 + 2]);
-          o1[j4 + 3] = __fmaf_rn(a1, w.w, o1[j4 + 3]);
-        }
-      }
       const float* B3 = S.w + Blob::b3;
+      const float* Xc = X + 2 * lane;
+      if (!IS_COLOR && P.out_full == nullptr) {
+        // march wavefronts only need the distance (output 0)
+        float2 d = make_float2(0.0f, 0.0f);
+#pragma unroll 8
+        for (int k = 0; k < kHidden; k++)
+          d = __ffma2_rn(*reinterpret_cast<const float2*>(Xc + k * kPanelLd), splat(W3[k * N3P]), d);
+        if (slot[0] >= 0) P.out_first[slot[0]] = __fadd_rn(d.x, B3[0]);
+        if (slot[1] >= 0) P.out_first[slot[1]] = __fadd_rn(d.y, B3[0]);
+      } else {
+        float2 o01[N3P];
 #pragma unroll
-      for (int q = 0; q < 2; q++) {
-        if (slot[q] < 0) continue;
-        float* o = q ? o1 : o0;
-        if (!IS_COLOR) {
-          float d = __fadd_rn(o[0], B3[0]);
-          if (P.out_first) P.out_first[slot[q]] = d;
-          if (P.out_full) {
-            float* row = P.out_full + (size_t)slot[q] * N3;
+        for (int j = 0; j < N3P; j++) o01[j] = make_float2(0.0f, 0.0f);
+#pragma unroll 4
+        for (int k = 0; k < kHidden; k++) {
+          float2 a = *reinterpret_cast<const float2*>(Xc + k * kPanelLd);
+#pragma unroll
+          for (int j4 = 0; j4 < N3P; j4 += 4) {
+            float4 w = *reinterpret_cast<const float4*>(W3 + k * N3P + j4);
+            o01[j4 + 0] = __ffma2_rn(a, splat(w.x), o01[j4 + 0]);
+            o01[j4 + 1] = __ffma2_rn(a, splat(w.y), o01[j4 + 1]);
+            o01[j4 + 2] = __ffma2_rn(a, splat(w.z), o01[j4 + 2]);
+            o01[j4 + 3] = __ffma2_rn(a, splat(w.w), o01[j4 + 3]);
+          }
+        }
+        float o0[N3P], o1[N3P];
+#pragma unroll
+        for (int j = 0; j < N3P; j++) {
+          o0[j] = o01[j].x;
+          o1[j] = o01[j].y;
+        }
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+          if (slot[q] < 0) continue;
+          float* o = q ? o1 : o0;
+          float* row = P.out_full + (size_t)slot[q] * N3;
+          if (!IS_COLOR) {
+            float d = __fadd_rn(o[0], B3[0]);
+            if (P.out_first) P.out_first[slot[q]] = d;
             row[0] = d;
 #pragma unroll
             for (int j = 1; j < N3; j++) row[j] = __fadd_rn(o[j], B3[j]);
-          }
-        } else {
-          float* row = P.out_full + (size_t)slot[q] * N3;
+          } else {
 #pragma unroll
-          for (int j = 0; j < N3; j++) row[j] = np_sigmoidf(__fadd_rn(o[j], B3[j]));
+            for (int j = 0; j < N3; j++) row[j] = np_sigmoidf(__fadd_rn(o[j], B3[j]));
+          }
         }
       }
     }
@@ -278,7 +324,7 @@ static __global__ void __launch_bounds__(kTileWarps * 32, 2) mlp_tile_kernel(Mlp
   }
 }
 
-using SdfKernelSmem = MlpSmem<kSdfIn, kSdfOut, kSdfOutPad, ACT_SOFTPLUS, false>;
-using ColKernelSmem = MlpSmem<kColIn, kColOut, kColOutPad, ACT_RELU, true>;
+using SdfKernelSmem = MlpSmem<kSdfIn, kSdfOutPad>;
+using ColKernelSmem = MlpSmem<kColIn, kColOutPad>;
 
 }  // namespace knf

@@ -1,0 +1,11 @@
+"""Tiny driver for ncu: a few dense sdf_query launches (1M points over 4096 cells)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_2206_10885_b200 import grid
+M = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
+dev = grid.device_field(grid.field_init(grid.GridConfig(resolution=16), seed=0))
+pts = torch.as_tensor(np.random.default_rng(0).uniform(-1, 1, (M, 3)).astype(np.float32), device="cuda")
+for _ in range(4):
+    grid.sdf_query(dev, pts)
+torch.cuda.synchronize()
