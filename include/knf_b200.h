@@ -87,6 +87,14 @@ typedef struct {
   int64_t hits;
   int64_t wavefronts;   /* march iterations executed */
   int64_t kernel_launches;
+  /* filled only while profiling is enabled (knf_field_set_profiling): CUDA-event time of the
+   * SDF tile-MLP launches and of the routing launches (emit/advance + scan + scatter) */
+  int64_t sdf_mlp_launches;
+  int64_t route_launches;
+  double sdf_mlp_ms;
+  double route_ms;
+  double color_mlp_ms;
+  double other_ms;
 } KnfStats;
 
 int knf_abi_version(void);
@@ -104,7 +112,11 @@ int knf_field_create_from_knf(const char* path, int device, knf_field_t* out);
 int knf_field_destroy(knf_field_t f);
 /* fills the GridConfig part of `desc` (pointers are set to NULL) */
 int knf_field_describe(knf_field_t f, KnfFieldDesc* desc);
+/* Statistics accumulate over calls until reset.  knf_field_stats synchronises the device. */
 int knf_field_stats(knf_field_t f, KnfStats* out);
+int knf_field_stats_reset(knf_field_t f);
+/* Bracket every kernel launch with CUDA events on the call's stream (adds ~1 us of host work per launch). */
+int knf_field_set_profiling(knf_field_t f, int enable);
 
 /* ---- routing: grid.py:176-213 ------------------------------------------------------------ */
 /* grid.cell_index_flat (grid.py:182-185) on fp32 points (fp64 arithmetic, bit-exact). */

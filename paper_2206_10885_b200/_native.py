@@ -80,6 +80,12 @@ class KnfStats(C.Structure):
         ("hits", C.c_int64),
         ("wavefronts", C.c_int64),
         ("kernel_launches", C.c_int64),
+        ("sdf_mlp_launches", C.c_int64),
+        ("route_launches", C.c_int64),
+        ("sdf_mlp_ms", C.c_double),
+        ("route_ms", C.c_double),
+        ("color_mlp_ms", C.c_double),
+        ("other_ms", C.c_double),
     ]
 
 
@@ -111,6 +117,8 @@ _SIGNATURES = {
     "knf_field_destroy": [_P],
     "knf_field_describe": [_P, C.POINTER(KnfFieldDesc)],
     "knf_field_stats": [_P, C.POINTER(KnfStats)],
+    "knf_field_stats_reset": [_P],
+    "knf_field_set_profiling": [_P, _I32],
     "knf_cell_index": [_P, _P, _I64, _P, _I32, _P],
     "knf_cell_index_f64": [_P, _P, _I64, _P, _I32, _P],
     "knf_route": [_P, _P, _I64, _P, _P, _P, _P, _P, _I32, _P],

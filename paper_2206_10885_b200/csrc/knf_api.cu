@@ -1,6 +1,7 @@
 // knf_api.cu -- the extern "C" surface declared in include/knf_b200.h.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -174,6 +175,7 @@ int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
     F.geom.hi[a] = d->bbox_max[a];
   }
   F.geom.fd_step = d->fd_step;
+  if (const char* env = std::getenv("KNF_MARCH_MAX_INNER")) F.march_max_inner = std::max(1, std::atoi(env));  // tuning knob
   std::vector<float> packed;
   pack_family<kSdfIn, kSdfOut, kSdfOutPad>(F.geom.n_cells, d->sdf_w, d->sdf_b, packed);
   KNF_CUDA(cudaMalloc(&F.sdf_blobs, packed.size() * sizeof(float)));
@@ -325,6 +327,8 @@ int knf_field_destroy(knf_field_t f) {
   {
     std::lock_guard<std::mutex> lk(f->f.mu);
     f->f.ws.release_all();
+    for (cudaEvent_t e : f->f.events) cudaEventDestroy(e);
+    if (f->f.host_poll) cudaFreeHost(f->f.host_poll);
     if (f->f.sdf_blobs) cudaFree(f->f.sdf_blobs);
     if (f->f.col_blobs) cudaFree(f->f.col_blobs);
   }
@@ -355,7 +359,26 @@ int knf_field_stats(knf_field_t f, KnfStats* out) {
   KNF_CUDA(cudaSetDevice(f->f.device));
   KNF_CUDA(cudaDeviceSynchronize());
   if (f->f.ws.counters.p) KNF_TRY(finish_stats(f->f, 0));
+  KNF_TRY(collect_profile(f->f));
   *out = f->f.stats;
+  return 0;
+}
+
+int knf_field_stats_reset(knf_field_t f) {
+  KNF_TRY(check_field(f));
+  std::lock_guard<std::mutex> lk(f->f.mu);
+  KNF_CUDA(cudaSetDevice(f->f.device));
+  KNF_CUDA(cudaDeviceSynchronize());
+  KNF_TRY(collect_profile(f->f));
+  f->f.stats = KnfStats{};
+  if (f->f.ws.counters.p) KNF_CUDA(cudaMemset(stat_counter(f->f, 0), 0, 4 * sizeof(unsigned long long)));
+  return 0;
+}
+
+int knf_field_set_profiling(knf_field_t f, int enable) {
+  KNF_TRY(check_field(f));
+  std::lock_guard<std::mutex> lk(f->f.mu);
+  f->f.profiling = enable != 0;
   return 0;
 }
 

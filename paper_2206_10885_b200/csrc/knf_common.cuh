@@ -43,13 +43,10 @@ struct BlobLayout {
 using SdfBlob = BlobLayout<kSdfIn, kSdfOutPad>;    // 2732 floats = 10928 B
 using ColBlob = BlobLayout<kColIn, kColOutPad>;    // 2532 floats = 10128 B
 
-// Points per warp and warps per CTA of the tile kernels; a tile is <= kTilePts points of one cell.
+// A tile is <= kTilePts requests of one cell and is processed by one warp (one-warp CTAs).
 constexpr int kWarpPts = 64;
-#ifndef KNF_TILE_WARPS
-#define KNF_TILE_WARPS 4
-#endif
-constexpr int kTileWarps = KNF_TILE_WARPS;
-constexpr int kTilePts = kWarpPts * kTileWarps;  // 256
+constexpr int kTilePts = kWarpPts;
+constexpr int kWarpCtasPerSm = 10;  // 21.5 KB of shared memory each
 
 struct GridGeom {
   int resolution;

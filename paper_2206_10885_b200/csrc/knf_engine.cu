@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstring>
 
+#include "knf_march.cuh"
 #include "knf_mlp.cuh"
 #include "knf_rays.cuh"
 
@@ -48,7 +49,7 @@ void DevBuf::release() {
 }
 
 void Workspace::release_all() {
-  DevBuf* all[] = {&req_pt, &req_cell, &req_rank, &perm, &tiles, &cell_count, &cell_offset, &counters, &t, &t_prev,
+  DevBuf* all[] = {&req_pt1, &req_cell1, &req_rank1, &req_pt, &req_cell, &req_rank, &perm, &tiles, &cell_count, &cell_offset, &counters, &t, &t_prev,
                    &d_prev, &t_conv, &d_conv, &t_hit, &steps, &phase, &hit, &live0, &live1, &dval, &hit_list,
                    &hit_count, &sdf_out, &col_v, &col_n, &col_z, &rgb, &origins, &dirs, &t_near, &t_far, &normals64,
                    &colors64, &steps_out};
@@ -106,6 +107,9 @@ int ensure_rays(Field& F, size_t n) {
   KNF_TRY(W.hit.ensure(n));
   KNF_TRY(W.live0.ensure(n * 4));
   KNF_TRY(W.live1.ensure(n * 4));
+  KNF_TRY(W.req_pt1.ensure(n * sizeof(float4)));
+  KNF_TRY(W.req_cell1.ensure(n * sizeof(int)));
+  KNF_TRY(W.req_rank1.ensure(n * sizeof(int)));
   KNF_TRY(W.hit_list.ensure(n * 4));
   KNF_TRY(W.hit_count.ensure(16));
   W.ray_cap = std::max(W.ray_cap, n);
@@ -117,12 +121,12 @@ unsigned long long* stat_counter(Field& F, int which) {
   return reinterpret_cast<unsigned long long*>(F.ws.counters.as<RouteCounters>() + 4) + which;
 }
 
-RouteBuffers route_buffers(Field& F, int slot, int next_slot) {
+RouteBuffers route_buffers(Field& F, int slot, int next_slot, int list) {
   Workspace& W = F.ws;
   RouteBuffers R;
-  R.req_pt = W.req_pt.as<float4>();
-  R.req_cell = W.req_cell.as<int>();
-  R.req_rank = W.req_rank.as<int>();
+  R.req_pt = (list ? W.req_pt1 : W.req_pt).as<float4>();
+  R.req_cell = (list ? W.req_cell1 : W.req_cell).as<int>();
+  R.req_rank = (list ? W.req_rank1 : W.req_rank).as<int>();
   R.cell_count = W.cell_count.as<int>();
   R.cell_offset = W.cell_offset.as<int>();
   R.perm = W.perm.as<int>();
@@ -137,16 +141,56 @@ int begin_call(Field& F, cudaStream_t st) {
   KNF_CUDA(cudaSetDevice(F.device));
   KNF_TRY(ensure_requests(F, 1024));
   KNF_CUDA(cudaMemsetAsync(F.ws.cell_count.p, 0, (size_t)F.geom.n_cells * sizeof(int), st));
-  KNF_CUDA(cudaMemsetAsync(F.ws.counters.p, 0, kCounterBytes, st));
-  F.stats = KnfStats{};
-  F.stats.kernel_launches = 0;
+  KNF_CUDA(cudaMemsetAsync(F.ws.counters.p, 0, 4 * sizeof(RouteCounters), st));  // stat counters persist
   if (!F.smem_configured) {
-    KNF_CUDA(cudaFuncSetAttribute(mlp_tile_kernel<kSdfIn, kSdfOut, kSdfOutPad, ACT_SOFTPLUS, false>,
+    KNF_CUDA(cudaFuncSetAttribute(mlp_warp_kernel<kSdfIn, kSdfOut, kSdfOutPad, ACT_SOFTPLUS, false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SdfKernelSmem)));
-    KNF_CUDA(cudaFuncSetAttribute(mlp_tile_kernel<kColIn, kColOut, kColOutPad, ACT_RELU, true>,
+    KNF_CUDA(cudaFuncSetAttribute(mlp_warp_kernel<kColIn, kColOut, kColOutPad, ACT_RELU, true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ColKernelSmem)));
+    KNF_CUDA(cudaFuncSetAttribute(march_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(SdfKernelSmem)));
+    if (!F.host_poll) KNF_CUDA(cudaMallocHost(&F.host_poll, 64));
     F.smem_configured = true;
   }
+  return 0;
+}
+
+static cudaEvent_t next_event(Field& F) {
+  if (F.events_used == F.events.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    F.events.push_back(e);
+  }
+  return F.events[F.events_used++];
+}
+ProfScope::ProfScope(Field& f, cudaStream_t s, int k) : F(f), st(s), kind(k), on(f.profiling) {
+  if (!on) return;
+  e0 = F.events_used;
+  cudaEventRecord(next_event(F), st);
+}
+ProfScope::~ProfScope() {
+  if (!on) return;
+  size_t e1 = F.events_used;
+  cudaEventRecord(next_event(F), st);
+  F.spans.push_back({kind, e0, e1});
+}
+int collect_profile(Field& F) {
+  KNF_CUDA(cudaDeviceSynchronize());
+  for (const Field::Span& sp : F.spans) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, F.events[sp.e0], F.events[sp.e1]) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    switch (sp.kind) {
+      case SPAN_SDF_MLP: F.stats.sdf_mlp_ms += ms; F.stats.sdf_mlp_launches += 1; break;
+      case SPAN_ROUTE: F.stats.route_ms += ms; F.stats.route_launches += 1; break;
+      case SPAN_COLOR_MLP: F.stats.color_mlp_ms += ms; break;
+      default: F.stats.other_ms += ms; break;
+    }
+  }
+  F.spans.clear();
+  F.events_used = 0;
   return 0;
 }
 
@@ -161,6 +205,7 @@ int finish_stats(Field& F, cudaStream_t st) {
 
 int launch_scan_scatter(Field& F, const RouteBuffers& R, size_t n_upper, cudaStream_t st, int* seg_cell, int* seg_start,
                         int* n_seg) {
+  ProfScope prof(F, st, SPAN_ROUTE);
   route_scan_kernel<<<1, kScanThreads, 0, st>>>(R, F.geom.n_cells, seg_cell, seg_start, n_seg);
   route_scatter_kernel<<<blocks_for(n_upper), 256, 0, st>>>(R);
   F.stats.kernel_launches += 2;
@@ -170,7 +215,7 @@ int launch_scan_scatter(Field& F, const RouteBuffers& R, size_t n_upper, cudaStr
 
 static inline int mlp_grid(const Field& F, size_t n_upper) {
   size_t tiles_upper = n_upper / kTilePts + std::min<size_t>(n_upper, (size_t)F.geom.n_cells) + 1;
-  return (int)std::max<size_t>(1, std::min<size_t>(tiles_upper, 148 * (16 / kTileWarps > 10 ? 10 : 16 / kTileWarps)));
+  return (int)std::max<size_t>(1, std::min<size_t>(tiles_upper, 148 * kWarpCtasPerSm));
 }
 
 int launch_sdf_mlp(Field& F, const RouteBuffers& R, size_t n_upper, float* out_first, float* out_full, cudaStream_t st) {
@@ -182,8 +227,9 @@ int launch_sdf_mlp(Field& F, const RouteBuffers& R, size_t n_upper, float* out_f
   P.req_pt = R.req_pt;
   P.out_first = out_first;
   P.out_full = out_full;
-  mlp_tile_kernel<kSdfIn, kSdfOut, kSdfOutPad, ACT_SOFTPLUS, false>
-      <<<mlp_grid(F, n_upper), kTileWarps * 32, sizeof(SdfKernelSmem), st>>>(P);
+  ProfScope prof(F, st, SPAN_SDF_MLP);
+  mlp_warp_kernel<kSdfIn, kSdfOut, kSdfOutPad, ACT_SOFTPLUS, false>
+      <<<mlp_grid(F, n_upper), 32, sizeof(SdfKernelSmem), st>>>(P);
   F.stats.kernel_launches += 1;
   KNF_CUDA(cudaGetLastError());
   return 0;
@@ -201,8 +247,9 @@ int launch_col_mlp(Field& F, const RouteBuffers& R, size_t n_upper, const float*
   P.col_n = nrm;
   P.col_z = z;
   P.out_full = rgb;
-  mlp_tile_kernel<kColIn, kColOut, kColOutPad, ACT_RELU, true>
-      <<<mlp_grid(F, n_upper), kTileWarps * 32, sizeof(ColKernelSmem), st>>>(P);
+  ProfScope prof(F, st, SPAN_COLOR_MLP);
+  mlp_warp_kernel<kColIn, kColOut, kColOutPad, ACT_RELU, true>
+      <<<mlp_grid(F, n_upper), 32, sizeof(ColKernelSmem), st>>>(P);
   F.stats.kernel_launches += 1;
   KNF_CUDA(cudaGetLastError());
   return 0;
@@ -254,7 +301,6 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
   M.hit = W.hit.as<unsigned char>();
   M.live[0] = W.live0.as<int>();
   M.live[1] = W.live1.as<int>();
-  M.dval = W.dval.as<float>();
   M.eps = s.eps_hit;
   M.step_scale = s.step_scale;
   M.max_steps = s.max_steps;
@@ -262,21 +308,43 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
   KNF_CUDA(cudaMemsetAsync(counters(F, 0), 0, 2 * sizeof(RouteCounters), st));
   const int nb = blocks_for((size_t)n);
   {
-    RouteBuffers R0 = route_buffers(F, 0, 1);
+    ProfScope prof(F, st, SPAN_ROUTE);
+    RouteBuffers R0 = route_buffers(F, 0, 1, 0);
     march_init_kernel<<<nb, 256, 0, st>>>(R0, F.geom, M, t_near, (int)n);
     F.stats.kernel_launches += 1;
   }
-  // max_steps stepping wavefronts + one that only carries secant-refinement evaluations
+  // Global wavefronts.  A ray is evaluated at least once per wavefront it takes part in, so
+  // max_steps stepping evaluations + one secant evaluation bound the count by max_steps + 1; tile
+  // residency usually finishes in far fewer, which the host learns by polling the request count.
   for (int w = 0; w <= s.max_steps; w++) {
-    int cur = w & 1, nxt = cur ^ 1;
-    RouteBuffers R = route_buffers(F, cur, nxt);
-    R.eval_counter = stat_counter(F, 0);
+    const int cur = w & 1, nxt = cur ^ 1;
+    RouteBuffers R = route_buffers(F, cur, nxt, cur);
     KNF_TRY(launch_scan_scatter(F, R, (size_t)n, st));
-    KNF_TRY(launch_sdf_mlp(F, R, (size_t)n, M.dval, nullptr, st));
-    RouteBuffers Rn = route_buffers(F, nxt, -1);
-    march_advance_kernel<<<nb, 256, 0, st>>>(Rn, F.geom, M, counters(F, cur), cur);
+    MarchTileArgs A{};
+    A.P.blobs = F.sdf_blobs;
+    A.P.perm = R.perm;
+    A.P.tiles = R.tiles;
+    A.P.ctr = R.ctr;
+    A.P.req_pt = R.req_pt;
+    A.next = route_buffers(F, nxt, -1, nxt);
+    A.G = F.geom;
+    A.M = M;
+    A.live_in = M.live[cur];
+    A.live_out = M.live[nxt];
+    A.eval_counter = stat_counter(F, 0);
+    A.max_inner = F.march_max_inner;
+    {
+      ProfScope prof(F, st, SPAN_SDF_MLP);
+      march_warp_kernel<<<mlp_grid(F, (size_t)n), 32, sizeof(SdfKernelSmem), st>>>(A);
+    }
     F.stats.kernel_launches += 1;
     F.stats.wavefronts += 1;
+    const bool poll = (w == 1) || (w == 3) || (w % 8 == 7);
+    if (poll && w < s.max_steps) {
+      KNF_CUDA(cudaMemcpyAsync(F.host_poll, &counters(F, nxt)->n_requests, sizeof(int), cudaMemcpyDeviceToHost, st));
+      KNF_CUDA(cudaStreamSynchronize(st));
+      if (*F.host_poll == 0) break;
+    }
   }
   if (want_hit_list) KNF_CUDA(cudaMemsetAsync(W.hit_count.p, 0, 16, st));
   march_finish_kernel<<<nb, 256, 0, st>>>(M, (int)n, hit, t, pos, steps, want_hit_list ? W.hit_list.as<int>() : nullptr,

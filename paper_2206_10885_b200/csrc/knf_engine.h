@@ -38,6 +38,7 @@ struct DevBuf {
 struct Workspace {
   // routing (two independent sets: A for SDF passes, B for the colour pass of shading)
   DevBuf req_pt, req_cell, req_rank, perm, tiles;
+  DevBuf req_pt1, req_cell1, req_rank1;  // second request list: the fused march kernel reads one list while filling the other
   DevBuf cell_count, cell_offset;
   DevBuf counters;  // RouteCounters[4] + stats counters
   // march state
@@ -63,12 +64,36 @@ struct Field {
   std::mutex mu;
   KnfStats stats{};
   bool smem_configured = false;
+  // optional per-launch event timing
+  bool profiling = false;
+  std::vector<cudaEvent_t> events;
+  struct Span {
+    int kind;
+    size_t e0, e1;
+  };
+  std::vector<Span> spans;
+  size_t events_used = 0;
+  int* host_poll = nullptr;  // pinned; early-out polling of the march loop
+  int march_max_inner = 8;    // tile-residency cap (steps in place per tile visit)
 };
+
+enum { SPAN_SDF_MLP = 0, SPAN_ROUTE = 1, SPAN_COLOR_MLP = 2, SPAN_OTHER = 3 };
+// RAII: records an event pair around the launches issued in its scope when F.profiling is set.
+struct ProfScope {
+  Field& F;
+  cudaStream_t st;
+  int kind;
+  size_t e0 = 0;
+  bool on;
+  ProfScope(Field& f, cudaStream_t s, int k);
+  ~ProfScope();
+};
+int collect_profile(Field& F);  // syncs; folds finished spans into F.stats
 
 // ---- drivers (all asynchronous on `st`; pointers are device pointers) -------------------------
 int ensure_requests(Field& F, size_t n_requests);
 int ensure_rays(Field& F, size_t n_rays);
-RouteBuffers route_buffers(Field& F, int counter_slot, int next_slot);
+RouteBuffers route_buffers(Field& F, int counter_slot, int next_slot, int list = 0);
 RouteCounters* counters(Field& F, int slot);
 unsigned long long* stat_counter(Field& F, int which);  // 0 = sdf evals, 1 = colour evals
 int begin_call(Field& F, cudaStream_t st);              // select device, reset routing invariants

@@ -1,0 +1,126 @@
+// knf_march.cuh -- the fused sphere-trace kernel (north_star subsystems 2 + 3; SURVEY K3 + K5).
+//
+// march_warp_kernel = the SDF tile MLP of knf_mlp.cuh with the march step of surface.march_rays
+// (surface.py:180-223) as its epilogue, plus *tile residency*: after a step, every ray whose next
+// sample still falls in the tile's cell is evaluated again right away by the same warp -- the
+// cell's weights are already in shared memory and the ray is already in a lane -- and only rays
+// that changed cell (or tiles that thinned out below half their size) go back through the global
+// routing pass.  Rays inside a random-init or a real field crawl through a cell for many steps
+// (step 0.8 * max(d, eps/2) against a cell edge of 0.125), so the number of global wavefronts
+// drops from max_steps + 1 to a few dozen, and the per-step ray-state traffic is overlapped with
+// other warps' FFMA work instead of being a separate HBM-bound kernel.
+// Every ray still sees exactly the reference's sequence of evaluations; only their order across
+// rays changes, and no result depends on that order.
+#pragma once
+
+#include "knf_mlp.cuh"
+#include "knf_rays.cuh"
+
+namespace knf {
+
+struct MarchTileArgs {
+  MlpParams P;         // current wavefront: blobs, perm, tiles, counters, request points
+  RouteBuffers next;   // where rays that leave their tile are queued for the next wavefront
+  GridGeom G;
+  MarchState M;
+  const int* live_in;  // request slot -> ray id (current wavefront)
+  int* live_out;       // same for the next wavefront
+  unsigned long long* eval_counter;  // statistics: SDF evaluations performed
+  int max_inner;       // cap on consecutive in-place steps of one tile
+};
+
+static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(MarchTileArgs A) {
+  using Blob = SdfBlob;
+  using Smem = MlpSmem<kSdfIn, kSdfOutPad>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+  const int lane = threadIdx.x;
+  if (lane == 0) {
+    mbar_init(&S.bar, 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  const MlpParams& P = A.P;
+  const int n_tiles = P.ctr->n_tiles;
+  uint32_t parity = 0;
+  float* X = S.x;
+  unsigned long long evals = 0;
+
+  for (;;) {
+    const int t = next_tile(P.ctr, lane);
+    if (t >= n_tiles) break;
+    const Tile tile = P.tiles[t];
+    fetch_weights<Blob>(S.w, P.blobs, tile.cell, &S.bar, lane);
+
+    bool active[2];
+    int ray[2] = {0, 0};
+    float px[2], py[2], pz[2];
+#pragma unroll
+    for (int q = 0; q < 2; q++) {
+      int p = 2 * lane + q;
+      active[q] = p < tile.count;
+      px[q] = py[q] = pz[q] = 0.f;
+      if (active[q]) {
+        int slot = P.perm[tile.start + p];
+        ray[q] = A.live_in[slot];
+        float4 pt = P.req_pt[slot];
+        px[q] = pt.x; py[q] = pt.y; pz[q] = pt.z;
+      }
+    }
+    int n_active = tile.count;
+
+    for (int inner = 0;; inner++) {
+      encode_into<kSdfFreqs>(X, 0, 2 * lane + 0, px[0], py[0], pz[0]);
+      encode_into<kSdfFreqs>(X, 0, 2 * lane + 1, px[1], py[1], pz[1]);
+      __syncwarp();
+      if (inner == 0) {
+        mbar_wait(&S.bar, parity);  // weights have landed
+        parity ^= 1;
+      }
+      hidden_layers<kSdfIn, kSdfOutPad, ACT_SOFTPLUS>(X, S.w, lane);
+      const float2 dist = output_distance<kSdfOutPad>(X, S.w + Blob::w3, S.w + Blob::b3, lane);
+      evals += (lane == 0) ? (unsigned long long)n_active : 0ull;
+
+      // ---- the march step for the lane's two rays -----------------------------------------------------
+      bool want[2], stay[2];
+      int cell[2];
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        want[q] = false;
+        cell[q] = -1;
+        if (active[q]) {
+          double t_next = 0.0;
+          want[q] = march_step(A.M, ray[q], q ? dist.y : dist.x, t_next);
+          if (want[q]) {
+            // pts = origins + t * dirs in fp64 (surface.py:184), then the fp32 cast of grid.py:375
+            const size_t r3 = 3 * (size_t)ray[q];
+            px[q] = __double2float_rn(A.M.o[r3 + 0] + t_next * A.M.d[r3 + 0]);
+            py[q] = __double2float_rn(A.M.o[r3 + 1] + t_next * A.M.d[r3 + 1]);
+            pz[q] = __double2float_rn(A.M.o[r3 + 2] + t_next * A.M.d[r3 + 2]);
+            cell[q] = cell_of(px[q], py[q], pz[q], A.G);
+          }
+        }
+        stay[q] = want[q] && cell[q] == tile.cell;
+      }
+      const int n_stay = __popc(__ballot_sync(0xffffffffu, stay[0])) + __popc(__ballot_sync(0xffffffffu, stay[1]));
+      // keep stepping in place while at least half of the tile's rays are still here
+      const bool cont = n_stay > 0 && 2 * n_stay >= tile.count && inner + 1 < A.max_inner;
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        const bool emit = want[q] && !(cont && stay[q]);
+        const int slot = warp_append(&A.next.ctr->n_requests, emit);
+        if (emit) A.live_out[slot] = ray[q];
+        route_emit_cell(A.next, emit, slot, px[q], py[q], pz[q], cell[q]);
+        active[q] = cont && stay[q];
+        if (!active[q]) px[q] = py[q] = pz[q] = 0.f;
+      }
+      if (!cont) break;
+      n_active = n_stay;
+      __syncwarp();
+    }
+    __syncwarp();  // every lane is done reading S.w and the panel before the next tile overwrites them
+  }
+  if (lane == 0 && evals && A.eval_counter) atomicAdd(A.eval_counter, evals);
+}
+
+}  // namespace knf

@@ -3,12 +3,14 @@
 // Replaces nn.fourier_encode (nn.py:66-93) + grid.grid_forward (grid.py:241-294) + the
 // activations (nn.py:26-50) for one family of per-cell MLPs.
 //
-// Work unit: a *tile* = up to 256 evaluation requests that fall in the same grid cell
-// (produced by the routing pass, knf_route.cuh).  One CTA of 4 warps owns a tile:
-//   * thread 0 pulls the cell's 10.9 KB weight blob into shared memory with ONE TMA bulk copy
+// Work unit: a *tile* = up to 64 evaluation requests that fall in the same grid cell (produced by
+// the routing pass, knf_route.cuh).  ONE WARP owns a tile (one-warp CTAs, 10 per SM): no block
+// barriers, so a warp never waits for a slower sibling (the 4-warp version spent 21 % of its
+// samples at the per-tile __syncthreads, ncu v3):
+//   * lane 0 pulls the cell's 10.9 KB weight blob into shared memory with ONE TMA bulk copy
 //     (cp.async.bulk -> UBLKCP) signalled on an mbarrier; the copy overlaps the encode;
-//   * each warp owns 64 of the tile's points.  It encodes them (NumPy-exact sin/cos + the fp32
-//     double-angle recurrence) into a k-major shared-memory panel X[k][64];
+//   * the warp encodes its 64 points (NumPy-exact sin/cos + the fp32 double-angle recurrence)
+//     into a k-major shared-memory panel X[k][64];
 //   * hidden layers are register-tiled SGEMMs: every lane accumulates an 8 point x 8 neuron
 //     block, reading 8 activations + 8 weights (4 LDS.128) per k for 64 FFMAs.  The k loop is
 //     sequential from k = 0 with one FFMA per step and the bias is added afterwards as its own
@@ -21,7 +23,7 @@
 //     cache (ncu on the first version: "no_instruction" was the top stall);
 //   * the 32 -> N3 output layer is evaluated two points per lane and written straight to the
 //     caller's buffers in request order (no unsort pass).
-// Shared memory: 10.9 KB weights + 4 x 10.6 KB panels = 53.4 KB per CTA -> 4 CTAs (16 warps) per SM.
+// Shared memory: 10.9 KB weights + 10.6 KB panel = 21.5 KB per one-warp CTA -> 10 CTAs per SM.
 //
 // FP32 FFMA, not tensor cores: TF32/BF16 mma gives ~1e-3 absolute SDF error, 1000x over the
 // parity budget that FD normals (x 1/2h = 500 amplification) need.  See DESIGN.md.
@@ -55,9 +57,8 @@ template <int K1, int N3P>
 struct MlpSmem {
   using Blob = BlobLayout<K1, N3P>;
   alignas(16) float w[Blob::floats];
-  alignas(16) float x[kTileWarps][K1 * kPanelLd];  // one activation panel per warp, reused by every layer
+  alignas(16) float x[K1 * kPanelLd];  // the warp's activation panel, reused by every layer
   alignas(8) uint64_t bar;
-  int tile_idx[2];
 };
 
 __device__ __forceinline__ float2 splat(float v) { return make_float2(v, v); }
@@ -168,159 +169,163 @@ __device__ __forceinline__ void encode_into(float* __restrict__ panel, int row0,
   }
 }
 
+// Layers 1 and 2 (+ activations) of one 64-point warp tile; leaves h2 in the panel.
+template <int K1, int N3P, int HIDDEN_ACT>
+__device__ __forceinline__ void hidden_layers(float* __restrict__ X, const float* __restrict__ W, int lane) {
+  using Blob = BlobLayout<K1, N3P>;
+  const int pg = lane >> 2;  // 8 point groups of 4(+4) points
+  const int ng = lane & 3;   // 4 neuron groups of 4(+4) neurons
+  float2 acc[4][8];
+  layer_8x8<K1>(X, W + Blob::w1, pg, ng, acc);
+  __syncwarp();  // every lane holds its accumulators: the input rows are dead
+  store_hidden<HIDDEN_ACT>(acc, W + Blob::b1, X, pg, ng);
+  __syncwarp();
+  if (HIDDEN_ACT == ACT_SOFTPLUS) {
+    softplus_panel(X, lane);
+    __syncwarp();
+  }
+  layer_8x8<kHidden>(X, W + Blob::w2, pg, ng, acc);
+  __syncwarp();
+  store_hidden<HIDDEN_ACT>(acc, W + Blob::b2, X, pg, ng);
+  __syncwarp();
+  if (HIDDEN_ACT == ACT_SOFTPLUS) softplus_panel(X, lane);  // the output layer reads back only the lane's own columns
+}
+
+// Output 0 (the distance) of the 32 -> N3 layer for the lane's two columns.
+template <int N3P>
+__device__ __forceinline__ float2 output_distance(const float* __restrict__ X, const float* __restrict__ W3,
+                                                  const float* __restrict__ B3, int lane) {
+  const float* Xc = X + 2 * lane;
+  float2 d = make_float2(0.0f, 0.0f);
+#pragma unroll 8
+  for (int k = 0; k < kHidden; k++)
+    d = __ffma2_rn(*reinterpret_cast<const float2*>(Xc + k * kPanelLd), splat(W3[k * N3P]), d);
+  return __fadd2_rn(d, splat(B3[0]));
+}
+
+// Weight fetch for one tile: one elected lane arms the mbarrier and issues the TMA bulk copy.
+template <class Blob>
+__device__ __forceinline__ void fetch_weights(float* smem_w, const float* __restrict__ blobs, int cell, uint64_t* bar,
+                                              int lane) {
+  if (lane == 0) {
+    fence_proxy_async();
+    mbar_expect_tx(bar, Blob::bytes);
+    bulk_copy_g2s(smem_w, blobs + (size_t)cell * Blob::floats, Blob::bytes, bar);
+  }
+}
+
+__device__ __forceinline__ int next_tile(RouteCounters* ctr, int lane) {
+  int t = 0;
+  if (lane == 0) t = atomicAdd(&ctr->tile_cursor, 1);
+  return __shfl_sync(0xffffffffu, t, 0);
+}
+
+// Batched-forward kernel (grid.sdf_query / color_query, shading probes): ONE WARP per CTA, each
+// warp a persistent worker that pulls 64-request tiles from the routing pass's tile list.
 template <int K1, int N3, int N3P, int HIDDEN_ACT, bool IS_COLOR>
-static __global__ void __launch_bounds__(kTileWarps * 32, 16 / kTileWarps > 10 ? 10 : 16 / kTileWarps) mlp_tile_kernel(MlpParams P) {
+static __global__ void __launch_bounds__(32, kWarpCtasPerSm) mlp_warp_kernel(MlpParams P) {
   using Blob = BlobLayout<K1, N3P>;
   using Smem = MlpSmem<K1, N3P>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
-
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5;
-  const int lane = tid & 31;
-  const int pg = lane >> 2;  // 8 point groups of 4(+4) points
-  const int ng = lane & 3;   // 4 neuron groups of 4(+4) neurons
-
-  if (tid == 0) {
+  const int lane = threadIdx.x;
+  if (lane == 0) {
     mbar_init(&S.bar, 1);
     fence_barrier_init();
   }
-  __syncthreads();
-
+  __syncwarp();
   const int n_tiles = P.ctr->n_tiles;
   uint32_t parity = 0;
-  float* X = S.x[warp];
+  float* X = S.x;
 
   for (;;) {
-    if (tid == 0) S.tile_idx[parity] = atomicAdd(&P.ctr->tile_cursor, 1);
-    __syncthreads();  // also: every warp is done reading S.w of the previous tile
-    const int t = S.tile_idx[parity];
+    const int t = next_tile(P.ctr, lane);
     if (t >= n_tiles) break;
     const Tile tile = P.tiles[t];
-    if (tid == 0) {
-      fence_proxy_async();
-      mbar_expect_tx(&S.bar, Blob::bytes);
-      bulk_copy_g2s(S.w, P.blobs + (size_t)tile.cell * Blob::floats, Blob::bytes, &S.bar);
-    }
+    fetch_weights<Blob>(S.w, P.blobs, tile.cell, &S.bar, lane);
 
-    const int wcount = min(kWarpPts, tile.count - warp * kWarpPts);  // points of this warp (may be <= 0)
     int slot[2] = {-1, -1};
-    if (wcount > 0) {
-      // ---- gather + encode two points per lane -------------------------------------------------
 #pragma unroll
-      for (int q = 0; q < 2; q++) {
-        int p = 2 * lane + q;  // the lane's two adjacent panel columns
-        float px = 0.f, py = 0.f, pz = 0.f;
-        if (p < wcount) {
-          slot[q] = P.perm[tile.start + warp * kWarpPts + p];
-          float4 pt = P.req_pt[slot[q]];
-          px = pt.x; py = pt.y; pz = pt.z;
-        }
-        if (!IS_COLOR) {
-          encode_into<kSdfFreqs>(X, 0, p, px, py, pz);
-        } else {
-          // grid.color_query (grid.py:397): [x | enc_L4(v) | n | z]
-          float vx = 0.f, vy = 0.f, vz = 0.f, nx = 0.f, ny = 0.f, nz = 0.f;
-          float zf[kFeat];
-#pragma unroll
-          for (int f = 0; f < kFeat; f++) zf[f] = 0.f;
-          if (p < wcount) {
-            const float* v = P.col_v + (size_t)slot[q] * 3;
-            const float* nn = P.col_n + (size_t)slot[q] * 3;
-            const float* zz = P.col_z + (size_t)slot[q] * kFeat;
-            vx = v[0]; vy = v[1]; vz = v[2];
-            nx = nn[0]; ny = nn[1]; nz = nn[2];
-#pragma unroll
-            for (int f = 0; f < kFeat; f++) zf[f] = zz[f];
-          }
-          X[0 * kPanelLd + p] = px;
-          X[1 * kPanelLd + p] = py;
-          X[2 * kPanelLd + p] = pz;
-          encode_into<kDirFreqs>(X, 3, p, vx, vy, vz);
-          constexpr int r = 3 + 3 + 6 * kDirFreqs;
-          X[(r + 0) * kPanelLd + p] = nx;
-          X[(r + 1) * kPanelLd + p] = ny;
-          X[(r + 2) * kPanelLd + p] = nz;
-#pragma unroll
-          for (int f = 0; f < kFeat; f++) X[(r + 3 + f) * kPanelLd + p] = zf[f];
-        }
+    for (int q = 0; q < 2; q++) {
+      int p = 2 * lane + q;  // the lane's two adjacent panel columns
+      float px = 0.f, py = 0.f, pz = 0.f;
+      if (p < tile.count) {
+        slot[q] = P.perm[tile.start + p];
+        float4 pt = P.req_pt[slot[q]];
+        px = pt.x; py = pt.y; pz = pt.z;
       }
-      __syncwarp();
+      if (!IS_COLOR) {
+        encode_into<kSdfFreqs>(X, 0, p, px, py, pz);
+      } else {
+        // grid.color_query (grid.py:397): [x | enc_L4(v) | n | z]
+        float vx = 0.f, vy = 0.f, vz = 0.f, nx = 0.f, ny = 0.f, nz = 0.f;
+        float zf[kFeat];
+#pragma unroll
+        for (int f = 0; f < kFeat; f++) zf[f] = 0.f;
+        if (p < tile.count) {
+          const float* v = P.col_v + (size_t)slot[q] * 3;
+          const float* nn = P.col_n + (size_t)slot[q] * 3;
+          const float* zz = P.col_z + (size_t)slot[q] * kFeat;
+          vx = v[0]; vy = v[1]; vz = v[2];
+          nx = nn[0]; ny = nn[1]; nz = nn[2];
+#pragma unroll
+          for (int f = 0; f < kFeat; f++) zf[f] = zz[f];
+        }
+        X[0 * kPanelLd + p] = px;
+        X[1 * kPanelLd + p] = py;
+        X[2 * kPanelLd + p] = pz;
+        encode_into<kDirFreqs>(X, 3, p, vx, vy, vz);
+        constexpr int r = 3 + 3 + 6 * kDirFreqs;
+        X[(r + 0) * kPanelLd + p] = nx;
+        X[(r + 1) * kPanelLd + p] = ny;
+        X[(r + 2) * kPanelLd + p] = nz;
+#pragma unroll
+        for (int f = 0; f < kFeat; f++) X[(r + 3 + f) * kPanelLd + p] = zf[f];
+      }
     }
-
-    mbar_wait(&S.bar, parity);  // weights have landed (all threads observe the phase)
+    __syncwarp();
+    mbar_wait(&S.bar, parity);  // weights have landed
     parity ^= 1;
 
-    if (wcount > 0) {
-      float2 acc[4][8];
-      // ---- layer 1: K1 -> 32 ---------------------------------------------------------------------
-      layer_8x8<K1>(X, S.w + Blob::w1, pg, ng, acc);
-      __syncwarp();  // every lane holds its accumulators: the input rows are dead
-      store_hidden<HIDDEN_ACT>(acc, S.w + Blob::b1, X, pg, ng);
-      __syncwarp();
-      if (HIDDEN_ACT == ACT_SOFTPLUS) {
-        softplus_panel(X, lane);
-        __syncwarp();
-      }
-      // ---- layer 2: 32 -> 32 -----------------------------------------------------------------------
-      layer_8x8<kHidden>(X, S.w + Blob::w2, pg, ng, acc);
-      __syncwarp();
-      store_hidden<HIDDEN_ACT>(acc, S.w + Blob::b2, X, pg, ng);
-      __syncwarp();
-      if (HIDDEN_ACT == ACT_SOFTPLUS) softplus_panel(X, lane);  // lane reads back only its own columns below
-      // ---- layer 3: 32 -> N3, two points per lane ---------------------------------------------------
-      const float* W3 = S.w + Blob::w3;
-      const float* B3 = S.w + Blob::b3;
+    hidden_layers<K1, N3P, HIDDEN_ACT>(X, S.w, lane);
+
+    const float* W3 = S.w + Blob::w3;
+    const float* B3 = S.w + Blob::b3;
+    if (!IS_COLOR && P.out_full == nullptr) {
+      float2 d = output_distance<N3P>(X, W3, B3, lane);
+      if (slot[0] >= 0) P.out_first[slot[0]] = d.x;
+      if (slot[1] >= 0) P.out_first[slot[1]] = d.y;
+    } else {
       const float* Xc = X + 2 * lane;
-      if (!IS_COLOR && P.out_full == nullptr) {
-        // march wavefronts only need the distance (output 0)
-        float2 d = make_float2(0.0f, 0.0f);
-#pragma unroll 8
-        for (int k = 0; k < kHidden; k++)
-          d = __ffma2_rn(*reinterpret_cast<const float2*>(Xc + k * kPanelLd), splat(W3[k * N3P]), d);
-        if (slot[0] >= 0) P.out_first[slot[0]] = __fadd_rn(d.x, B3[0]);
-        if (slot[1] >= 0) P.out_first[slot[1]] = __fadd_rn(d.y, B3[0]);
-      } else {
-        float2 o01[N3P];
+      float2 o01[N3P];
 #pragma unroll
-        for (int j = 0; j < N3P; j++) o01[j] = make_float2(0.0f, 0.0f);
+      for (int j = 0; j < N3P; j++) o01[j] = make_float2(0.0f, 0.0f);
 #pragma unroll 4
-        for (int k = 0; k < kHidden; k++) {
-          float2 a = *reinterpret_cast<const float2*>(Xc + k * kPanelLd);
+      for (int k = 0; k < kHidden; k++) {
+        float2 a = *reinterpret_cast<const float2*>(Xc + k * kPanelLd);
 #pragma unroll
-          for (int j4 = 0; j4 < N3P; j4 += 4) {
-            float4 w = *reinterpret_cast<const float4*>(W3 + k * N3P + j4);
-            o01[j4 + 0] = __ffma2_rn(a, splat(w.x), o01[j4 + 0]);
-            o01[j4 + 1] = __ffma2_rn(a, splat(w.y), o01[j4 + 1]);
-            o01[j4 + 2] = __ffma2_rn(a, splat(w.z), o01[j4 + 2]);
-            o01[j4 + 3] = __ffma2_rn(a, splat(w.w), o01[j4 + 3]);
-          }
+        for (int j4 = 0; j4 < N3P; j4 += 4) {
+          float4 w = *reinterpret_cast<const float4*>(W3 + k * N3P + j4);
+          o01[j4 + 0] = __ffma2_rn(a, splat(w.x), o01[j4 + 0]);
+          o01[j4 + 1] = __ffma2_rn(a, splat(w.y), o01[j4 + 1]);
+          o01[j4 + 2] = __ffma2_rn(a, splat(w.z), o01[j4 + 2]);
+          o01[j4 + 3] = __ffma2_rn(a, splat(w.w), o01[j4 + 3]);
         }
-        float o0[N3P], o1[N3P];
+      }
 #pragma unroll
-        for (int j = 0; j < N3P; j++) {
-          o0[j] = o01[j].x;
-          o1[j] = o01[j].y;
-        }
+      for (int q = 0; q < 2; q++) {
+        if (slot[q] < 0) continue;
+        float* row = P.out_full + (size_t)slot[q] * N3;
 #pragma unroll
-        for (int q = 0; q < 2; q++) {
-          if (slot[q] < 0) continue;
-          float* o = q ? o1 : o0;
-          float* row = P.out_full + (size_t)slot[q] * N3;
-          if (!IS_COLOR) {
-            float d = __fadd_rn(o[0], B3[0]);
-            if (P.out_first) P.out_first[slot[q]] = d;
-            row[0] = d;
-#pragma unroll
-            for (int j = 1; j < N3; j++) row[j] = __fadd_rn(o[j], B3[j]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < N3; j++) row[j] = np_sigmoidf(__fadd_rn(o[j], B3[j]));
-          }
+        for (int j = 0; j < N3; j++) {
+          float v = __fadd_rn(q ? o01[j].y : o01[j].x, B3[j]);
+          if (IS_COLOR) v = np_sigmoidf(v);
+          row[j] = v;
+          if (!IS_COLOR && j == 0 && P.out_first) P.out_first[slot[q]] = v;
         }
       }
     }
-    // loop: the __syncthreads at the top orders these reads of S.w before the next bulk copy
+    __syncwarp();  // every lane is done reading S.w and the panel before the next tile overwrites them
   }
 }
 

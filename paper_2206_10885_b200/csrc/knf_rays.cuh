@@ -156,7 +156,6 @@ struct MarchState {
   unsigned char* phase;
   unsigned char* hit;
   int* live[2];      // request slot -> ray id, double buffered by wavefront parity
-  float* dval;       // request slot -> distance from the MLP kernel
   double eps;
   double step_scale;
   int max_steps;
@@ -197,65 +196,50 @@ static __global__ void march_init_kernel(RouteBuffers R, GridGeom G, MarchState 
   }
 }
 
-// Consume wavefront `w`'s distances, advance every live ray, emit wavefront w+1's requests.
-static __global__ void march_advance_kernel(RouteBuffers Rnext, GridGeom G, MarchState M, const RouteCounters* __restrict__ cur,
-                                     int parity) {
-  const int n = cur->n_requests;
-  const int* live_in = M.live[parity];
-  int* live_out = M.live[parity ^ 1];
-  int stride = gridDim.x * blockDim.x;
-  int n_round = (n + 31) & ~31;
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n_round; s += stride) {
-    bool want = false;
-    int ray = 0;
-    double t_next = 0.0;
-    if (s < n) {
-      ray = live_in[s];
-      double dv = (double)M.dval[s];
-      double t = M.t[ray];
-      if (M.phase[ray] == PH_REFINE) {
-        // surface.py:203-206: keep the secant point unless it is farther from the surface
-        double tc = M.t_conv[ray];
-        M.t_hit[ray] = (fabs(dv) > fabs(M.d_conv[ray])) ? tc : t;
-        M.hit[ray] = 1;
-        M.phase[ray] = PH_DONE;
-      } else {
-        int st = M.steps[ray] + 1;
-        M.steps[ray] = st;
-        if (fabs(dv) <= M.eps) {
-          double tp = M.t_prev[ray], dp = M.d_prev[ray];
-          bool usable = isfinite(tp) && (fabs(dv - dp) > 1e-12);
-          if (usable) {
-            double root = t - dv * (t - tp) / (dv - dp);
-            double a = fmin(t, tp), b = fmax(t, tp);
-            root = fmin(fmax(root, a), b + (b - a));  // np.clip(root, a, b + (b - a))
-            M.t_conv[ray] = t;
-            M.d_conv[ray] = dv;
-            M.t[ray] = root;
-            M.phase[ray] = PH_REFINE;
-            want = true;
-            t_next = root;
-          } else {
-            M.t_hit[ray] = t;
-            M.hit[ray] = 1;
-            M.phase[ray] = PH_DONE;
-          }
-        } else {
-          M.t_prev[ray] = t;
-          M.d_prev[ray] = dv;
-          double tn = t + M.step_scale * fmax(dv, M.eps / 2);
-          M.t[ray] = tn;
-          if (tn > M.t_far[ray] || st >= M.max_steps) {
-            M.phase[ray] = PH_DONE;  // left the box, or the step budget is spent: a miss
-          } else {
-            want = true;
-            t_next = tn;
-          }
-        }
-      }
-    }
-    emit_at(Rnext, G, M, live_out, want, ray, t_next);
+// One sphere-trace step of one ray (the body of the reference loop, surface.py:185-223) given the
+// fp32 distance `dval` the MLP just produced at the ray's current parameter.  Updates the ray's
+// state and returns true when the ray needs another evaluation, at parameter t_next (either the
+// next march position or the secant candidate).
+__device__ __forceinline__ bool march_step(const MarchState& M, int ray, float dval, double& t_next) {
+  const double dv = (double)dval;
+  const double t = M.t[ray];
+  if (M.phase[ray] == PH_REFINE) {
+    // surface.py:203-206: keep the secant point unless it is farther from the surface
+    M.t_hit[ray] = (fabs(dv) > fabs(M.d_conv[ray])) ? M.t_conv[ray] : t;
+    M.hit[ray] = 1;
+    M.phase[ray] = PH_DONE;
+    return false;
   }
+  const int st = M.steps[ray] + 1;
+  M.steps[ray] = st;
+  if (fabs(dv) <= M.eps) {
+    const double tp = M.t_prev[ray], dp = M.d_prev[ray];
+    if (isfinite(tp) && (fabs(dv - dp) > 1e-12)) {
+      double root = t - dv * (t - tp) / (dv - dp);
+      const double a = fmin(t, tp), b = fmax(t, tp);
+      root = fmin(fmax(root, a), b + (b - a));  // np.clip(root, a, b + (b - a))
+      M.t_conv[ray] = t;
+      M.d_conv[ray] = dv;
+      M.t[ray] = root;
+      M.phase[ray] = PH_REFINE;
+      t_next = root;
+      return true;
+    }
+    M.t_hit[ray] = t;
+    M.hit[ray] = 1;
+    M.phase[ray] = PH_DONE;
+    return false;
+  }
+  M.t_prev[ray] = t;
+  M.d_prev[ray] = dv;
+  const double tn = t + M.step_scale * fmax(dv, M.eps / 2);
+  M.t[ray] = tn;
+  if (tn > M.t_far[ray] || st >= M.max_steps) {
+    M.phase[ray] = PH_DONE;  // left the box, or the step budget is spent: a miss
+    return false;
+  }
+  t_next = tn;
+  return true;
 }
 
 // Write the TraceResult arrays (surface.py:225-226) and, optionally, compact the hit rays.

@@ -32,11 +32,11 @@ struct RouteBuffers {
   unsigned long long* eval_counter;  // += n_requests per pass (nullable); statistics only
 };
 
-// Record request `slot` at fp32 point (x,y,z).  Must be called by converged lanes with
-// `active` false for lanes that have nothing to emit.
-__device__ __forceinline__ void route_emit(const RouteBuffers& R, const GridGeom& G, bool active, int slot, float x,
-                                           float y, float z) {
-  int cell = active ? cell_of(x, y, z, G) : -1;
+// Record request `slot` at fp32 point (x,y,z) whose cell is already known.  Must be reached by
+// all 32 lanes; `active` is false for lanes that have nothing to emit.
+__device__ __forceinline__ void route_emit_cell(const RouteBuffers& R, bool active, int slot, float x, float y, float z,
+                                                int cell) {
+  if (!active) cell = -1;
   unsigned peers = __match_any_sync(0xffffffffu, cell);  // all 32 lanes reach this (warp-uniform loops)
   if (active) {
     int lane = threadIdx.x & 31;
@@ -49,6 +49,11 @@ __device__ __forceinline__ void route_emit(const RouteBuffers& R, const GridGeom
     R.req_cell[slot] = cell;
     R.req_rank[slot] = rank;
   }
+}
+
+__device__ __forceinline__ void route_emit(const RouteBuffers& R, const GridGeom& G, bool active, int slot, float x,
+                                           float y, float z) {
+  route_emit_cell(R, active, slot, x, y, z, active ? cell_of(x, y, z, G) : -1);
 }
 
 // grid.cell_index_flat on caller points + emit, slot = row index (the batched-forward entry).

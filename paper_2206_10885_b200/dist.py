@@ -1,0 +1,90 @@
+"""Multi-GPU sharding of the render path: one process per GPU, the field replicated,
+rays partitioned with NO data-path collective -- frames shard by view (weak scaling) or by
+contiguous row band (strong scaling) -- and one final gather of the finished buffers over
+NVLink (torch.distributed, NCCL on GPUs; the same code runs on gloo/CPU tensors in the tests).
+
+The reference has no distributed code at all (its only parallelism is a thread pool over row
+bands, surface.py:326-333); row bands are the unit it already proves result-invariant.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def shard_views(n_views: int, rank: int, world: int) -> list[int]:
+    """Round-robin views -> ranks (view v goes to rank v % world)."""
+    if not (0 <= rank < world):
+        raise ValueError("rank out of range")
+    return list(range(rank, n_views, world))
+
+
+def shard_rows(height: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced row band [row0, row1) of rank `rank`; bands tile [0, height) in rank order.
+    Ranks beyond the row count get an empty band."""
+    if not (0 <= rank < world):
+        raise ValueError("rank out of range")
+    base, extra = divmod(height, world)
+    row0 = rank * base + min(rank, extra)
+    return row0, row0 + base + (1 if rank < extra else 0)
+
+
+def gather_row_bands(local, height: int, group=None):
+    """All-gather row bands (first dim = rows of this rank's band) into the full (height, ...) tensor.
+
+    Bands are padded to the largest band so one all_gather_into_tensor moves everything; every
+    rank returns the assembled frame.  Works for CUDA tensors over NCCL and CPU tensors over gloo.
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    bands = [shard_rows(height, r, world) for r in range(world)]
+    if local.shape[0] != bands[rank][1] - bands[rank][0]:
+        raise ValueError("local band has the wrong number of rows")
+    tallest = max(b[1] - b[0] for b in bands)
+    padded = torch.zeros((tallest,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    padded[: local.shape[0]] = local
+    out = torch.empty((world * tallest,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, padded.contiguous(), group=group)
+    pieces = [out[r * tallest : r * tallest + (b[1] - b[0])] for r, b in enumerate(bands)]
+    return torch.cat(pieces, dim=0)
+
+
+def gather_views(local, group=None):
+    """All-gather one finished per-rank buffer (e.g. a colour frame) -> (world, ...) on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    out = torch.empty((world,) + tuple(local.shape), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out.view(world * local.shape[0], *local.shape[1:]) if local.dim() > 0 else out,
+                                local.contiguous(), group=group)
+    return out
+
+
+def render_frame_sharded(surface, pose, settings=None, background=(1.0, 1.0, 1.0), supersample: int = 1, group=None,
+                         render_rows=None):
+    """One frame split into row bands across the ranks of `group`, assembled on every rank.
+
+    Returns (color (H,W,3) f32, depth (H,W) f32, normal (H,W,3) f32, hit (H,W) u8) torch tensors on
+    the rank's device.  `render_rows` is injectable so the host logic can be tested without a GPU.
+    """
+    import torch.distributed as dist
+
+    from . import surface as S
+
+    settings = settings or S.RenderSettings()
+    render_rows = render_rows or (lambda r0, r1: S.render_rows(surface, pose, settings, background, supersample, r0, r1,
+                                                                device_out=True))
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    H = int(pose.height)
+    r0, r1 = shard_rows(H, rank, world)
+    if r1 > r0:
+        bands = render_rows(r0, r1)
+    else:
+        bands = render_rows(0, 1)
+        bands = tuple(b[:0] for b in bands)
+    return tuple(gather_row_bands(b, H, group) for b in bands)

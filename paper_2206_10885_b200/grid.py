@@ -210,7 +210,13 @@ class DeviceField:
     def stats(self) -> dict:
         st = N.KnfStats()
         N.check(N.load().knf_field_stats(self.handle, C.byref(st)))
-        return {k: int(getattr(st, k)) for k, _ in N.KnfStats._fields_}
+        return {k: getattr(st, k) for k, _ in N.KnfStats._fields_}
+
+    def reset_stats(self):
+        N.check(N.load().knf_field_stats_reset(self.handle))
+
+    def set_profiling(self, enable: bool):
+        N.check(N.load().knf_field_set_profiling(self.handle, int(bool(enable))))
 
 
 def _default_device() -> int:

