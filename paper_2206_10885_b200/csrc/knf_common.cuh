@@ -28,10 +28,15 @@ constexpr int kColOutPad = 4;
 
 // Per-cell weight blob, all k-major ("transposed") so a thread reads W[k][j..j+3] as one float4:
 //   W1t[K1][32] | b1[32] | W2t[32][32] | b2[32] | W3t[32][N3P] | b3[N3P]
+// The first layer's K is padded to a multiple of 8 with zero rows (39 -> 40, 41 -> 48) so the k loop
+// runs in fully unrolled chunks of 8; a zero row adds fma(0, 0, acc) = acc, which changes no bit.
+__host__ __device__ constexpr int pad_k(int k) { return (k + 7) / 8 * 8; }
+
 template <int K1, int N3P>
 struct BlobLayout {
+  static constexpr int rows1 = pad_k(K1);
   static constexpr int w1 = 0;
-  static constexpr int b1 = w1 + K1 * kHidden;
+  static constexpr int b1 = w1 + rows1 * kHidden;
   static constexpr int w2 = b1 + kHidden;
   static constexpr int b2 = w2 + kHidden * kHidden;
   static constexpr int w3 = b2 + kHidden;
@@ -40,8 +45,8 @@ struct BlobLayout {
   static constexpr int bytes = floats * 4;
   static_assert(bytes % 16 == 0, "blob must be a multiple of 16 B for cp.async.bulk");
 };
-using SdfBlob = BlobLayout<kSdfIn, kSdfOutPad>;    // 2732 floats = 10928 B
-using ColBlob = BlobLayout<kColIn, kColOutPad>;    // 2532 floats = 10128 B
+using SdfBlob = BlobLayout<kSdfIn, kSdfOutPad>;    // 2764 floats = 11056 B
+using ColBlob = BlobLayout<kColIn, kColOutPad>;    // 2756 floats = 11024 B
 
 // A tile is <= kTilePts requests of one cell and is processed by one warp (one-warp CTAs).
 constexpr int kWarpPts = 64;

@@ -55,6 +55,7 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(M
     bool active[2];
     int ray[2] = {0, 0};
     float px[2], py[2], pz[2];
+    RayRegs rr[2];  // the lane's two rays live in registers for the whole tile visit
 #pragma unroll
     for (int q = 0; q < 2; q++) {
       int p = 2 * lane + q;
@@ -65,8 +66,10 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(M
         ray[q] = A.live_in[slot];
         float4 pt = P.req_pt[slot];
         px[q] = pt.x; py[q] = pt.y; pz[q] = pt.z;
+        ray_load(rr[q], A.M, ray[q]);  // in flight during the first MLP pass
       }
     }
+    zero_pad_rows<kSdfIn>(X, lane);
     int n_active = tile.count;
 
     for (int inner = 0;; inner++) {
@@ -90,13 +93,12 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(M
         cell[q] = -1;
         if (active[q]) {
           double t_next = 0.0;
-          want[q] = march_step(A.M, ray[q], q ? dist.y : dist.x, t_next);
+          want[q] = ray_step(rr[q], A.M, ray[q], q ? dist.y : dist.x, t_next);
           if (want[q]) {
             // pts = origins + t * dirs in fp64 (surface.py:184), then the fp32 cast of grid.py:375
-            const size_t r3 = 3 * (size_t)ray[q];
-            px[q] = __double2float_rn(A.M.o[r3 + 0] + t_next * A.M.d[r3 + 0]);
-            py[q] = __double2float_rn(A.M.o[r3 + 1] + t_next * A.M.d[r3 + 1]);
-            pz[q] = __double2float_rn(A.M.o[r3 + 2] + t_next * A.M.d[r3 + 2]);
+            px[q] = __double2float_rn(rr[q].o[0] + t_next * rr[q].d[0]);
+            py[q] = __double2float_rn(rr[q].o[1] + t_next * rr[q].d[1]);
+            pz[q] = __double2float_rn(rr[q].o[2] + t_next * rr[q].d[2]);
             cell[q] = cell_of(px[q], py[q], pz[q], A.G);
           }
         }
@@ -109,7 +111,10 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(M
       for (int q = 0; q < 2; q++) {
         const bool emit = want[q] && !(cont && stay[q]);
         const int slot = warp_append(&A.next.ctr->n_requests, emit);
-        if (emit) A.live_out[slot] = ray[q];
+        if (emit) {
+          A.live_out[slot] = ray[q];
+          ray_store(rr[q], A.M, ray[q]);
+        }
         route_emit_cell(A.next, emit, slot, px[q], py[q], pz[q], cell[q]);
         active[q] = cont && stay[q];
         if (!active[q]) px[q] = py[q] = pz[q] = 0.f;

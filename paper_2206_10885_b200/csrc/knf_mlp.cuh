@@ -57,7 +57,7 @@ template <int K1, int N3P>
 struct MlpSmem {
   using Blob = BlobLayout<K1, N3P>;
   alignas(16) float w[Blob::floats];
-  alignas(16) float x[K1 * kPanelLd];  // the warp's activation panel, reused by every layer
+  alignas(16) float x[pad_k(K1) * kPanelLd];  // the warp's activation panel, reused by every layer
   alignas(8) uint64_t bar;
 };
 
@@ -87,29 +87,28 @@ __device__ __forceinline__ void fma_block(const LayerOperands& o, float2 (&acc)[
     for (int j = 0; j < 8; j++) acc[i][j] = __ffma2_rn(xs[i], splat(ws[j]), acc[i][j]);
 }
 
-// Explicit two-stage software pipeline (operands of step k+1 are in flight while step k's 32
-// FFMA2 issue); the loop body covers two steps so the two operand sets keep their registers --
-// ptxas' own rotation of a 4x-unrolled loop cost 34 MOVs per iteration (ncu, v3).
-// Rows K..K+1 of the panel / weight block may be read but are never used.
+// K is a multiple of 8: the k loop runs as fully unrolled chunks of 8 steps (288 instructions,
+// ptxas pipelines the LDS inside the chunk).  Rolled-up variants made ptxas rotate the operand
+// registers with ~30 MOVs per iteration (ncu v3/v4: 9-13 % of all issued instructions).
 template <int K>
 __device__ __forceinline__ void layer_8x8(const float* __restrict__ In, const float* __restrict__ Wt, int pg, int ng,
                                           float2 (&acc)[4][8]) {
+  static_assert(K % 8 == 0, "pad K to a multiple of 8");
 #pragma unroll
   for (int i = 0; i < 4; i++)
 #pragma unroll
     for (int j = 0; j < 8; j++) acc[i][j] = make_float2(0.0f, 0.0f);
   const float* xp = In + pg * 4;
   const float* wp = Wt + ng * 4;
-  LayerOperands a, b;
-  load_operands(a, xp, wp, 0);
 #pragma unroll 1
-  for (int k = 0; k + 1 < K; k += 2) {
-    load_operands(b, xp, wp, k + 1);
-    fma_block(a, acc);
-    load_operands(a, xp, wp, k + 2);
-    fma_block(b, acc);
+  for (int k0 = 0; k0 < K; k0 += 8) {
+#pragma unroll
+    for (int kk = 0; kk < 8; kk++) {
+      LayerOperands o;
+      load_operands(o, xp, wp, k0 + kk);
+      fma_block(o, acc);
+    }
   }
-  if (K & 1) fma_block(a, acc);
 }
 
 // Out[neuron][point] = act(acc + b), k-major panel for the next layer.  RELU is applied here;
@@ -169,6 +168,13 @@ __device__ __forceinline__ void encode_into(float* __restrict__ panel, int row0,
   }
 }
 
+// Rows K1 .. pad_k(K1)-1 of the input panel must be zero for the lane's two columns.
+template <int K1>
+__device__ __forceinline__ void zero_pad_rows(float* __restrict__ X, int lane) {
+#pragma unroll
+  for (int r = K1; r < pad_k(K1); r++) *reinterpret_cast<float2*>(X + r * kPanelLd + 2 * lane) = make_float2(0.f, 0.f);
+}
+
 // Layers 1 and 2 (+ activations) of one 64-point warp tile; leaves h2 in the panel.
 template <int K1, int N3P, int HIDDEN_ACT>
 __device__ __forceinline__ void hidden_layers(float* __restrict__ X, const float* __restrict__ W, int lane) {
@@ -176,7 +182,7 @@ __device__ __forceinline__ void hidden_layers(float* __restrict__ X, const float
   const int pg = lane >> 2;  // 8 point groups of 4(+4) points
   const int ng = lane & 3;   // 4 neuron groups of 4(+4) neurons
   float2 acc[4][8];
-  layer_8x8<K1>(X, W + Blob::w1, pg, ng, acc);
+  layer_8x8<pad_k(K1)>(X, W + Blob::w1, pg, ng, acc);
   __syncwarp();  // every lane holds its accumulators: the input rows are dead
   store_hidden<HIDDEN_ACT>(acc, W + Blob::b1, X, pg, ng);
   __syncwarp();
@@ -283,6 +289,7 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) mlp_warp_kernel(Mlp
         for (int f = 0; f < kFeat; f++) X[(r + 3 + f) * kPanelLd + p] = zf[f];
       }
     }
+    zero_pad_rows<K1>(X, lane);
     __syncwarp();
     mbar_wait(&S.bar, parity);  // weights have landed
     parity ^= 1;

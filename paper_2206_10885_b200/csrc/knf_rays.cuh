@@ -196,46 +196,78 @@ static __global__ void march_init_kernel(RouteBuffers R, GridGeom G, MarchState 
   }
 }
 
+// A ray's marching state held in registers while it is resident in a tile.
+struct RayRegs {
+  double o[3], d[3];
+  double t, t_far, t_prev, d_prev;
+  int steps;
+  int phase;
+};
+__device__ __forceinline__ void ray_load(RayRegs& R, const MarchState& M, int ray) {
+  const size_t r3 = 3 * (size_t)ray;
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    R.o[a] = M.o[r3 + a];
+    R.d[a] = M.d[r3 + a];
+  }
+  R.t = M.t[ray];
+  R.t_far = M.t_far[ray];
+  R.t_prev = M.t_prev[ray];
+  R.d_prev = M.d_prev[ray];
+  R.steps = M.steps[ray];
+  R.phase = M.phase[ray];
+}
+// Write back what a later tile visit (or the finish kernel) needs.
+__device__ __forceinline__ void ray_store(const RayRegs& R, const MarchState& M, int ray) {
+  M.t[ray] = R.t;
+  M.t_prev[ray] = R.t_prev;
+  M.d_prev[ray] = R.d_prev;
+  M.steps[ray] = R.steps;
+  M.phase[ray] = (unsigned char)R.phase;
+}
+
 // One sphere-trace step of one ray (the body of the reference loop, surface.py:185-223) given the
-// fp32 distance `dval` the MLP just produced at the ray's current parameter.  Updates the ray's
-// state and returns true when the ray needs another evaluation, at parameter t_next (either the
-// next march position or the secant candidate).
-__device__ __forceinline__ bool march_step(const MarchState& M, int ray, float dval, double& t_next) {
+// fp32 distance `dval` the MLP just produced at the ray's current parameter.  Returns true when
+// the ray needs another evaluation, at parameter t_next (the next march position or the secant
+// candidate); on false the ray is finished and its result has been written to global memory.
+__device__ __forceinline__ bool ray_step(RayRegs& R, const MarchState& M, int ray, float dval, double& t_next) {
   const double dv = (double)dval;
-  const double t = M.t[ray];
-  if (M.phase[ray] == PH_REFINE) {
+  const double t = R.t;
+  if (R.phase == PH_REFINE) {
     // surface.py:203-206: keep the secant point unless it is farther from the surface
     M.t_hit[ray] = (fabs(dv) > fabs(M.d_conv[ray])) ? M.t_conv[ray] : t;
     M.hit[ray] = 1;
     M.phase[ray] = PH_DONE;
+    M.steps[ray] = R.steps;
     return false;
   }
-  const int st = M.steps[ray] + 1;
-  M.steps[ray] = st;
+  R.steps += 1;
   if (fabs(dv) <= M.eps) {
-    const double tp = M.t_prev[ray], dp = M.d_prev[ray];
+    const double tp = R.t_prev, dp = R.d_prev;
     if (isfinite(tp) && (fabs(dv - dp) > 1e-12)) {
       double root = t - dv * (t - tp) / (dv - dp);
       const double a = fmin(t, tp), b = fmax(t, tp);
       root = fmin(fmax(root, a), b + (b - a));  // np.clip(root, a, b + (b - a))
       M.t_conv[ray] = t;
       M.d_conv[ray] = dv;
-      M.t[ray] = root;
-      M.phase[ray] = PH_REFINE;
+      R.t = root;
+      R.phase = PH_REFINE;
       t_next = root;
       return true;
     }
     M.t_hit[ray] = t;
     M.hit[ray] = 1;
     M.phase[ray] = PH_DONE;
+    M.steps[ray] = R.steps;
     return false;
   }
-  M.t_prev[ray] = t;
-  M.d_prev[ray] = dv;
+  R.t_prev = t;
+  R.d_prev = dv;
   const double tn = t + M.step_scale * fmax(dv, M.eps / 2);
-  M.t[ray] = tn;
-  if (tn > M.t_far[ray] || st >= M.max_steps) {
+  R.t = tn;
+  if (tn > R.t_far || R.steps >= M.max_steps) {
     M.phase[ray] = PH_DONE;  // left the box, or the step budget is spent: a miss
+    M.steps[ray] = R.steps;
     return false;
   }
   t_next = tn;
