@@ -208,6 +208,13 @@ int knf_scene_destroy(knf_scene_t sc);
 /* pathtrace.Rng.uniform (pathtrace.py:37-49), bit-exact: u[i] = hash(seed, pixel[i], sample[i], slot[i]). */
 int knf_rng_uniform(uint64_t seed, const uint64_t* pixel, const uint64_t* sample, const uint64_t* slot,
                     int64_t n, double* u, int device, int mem, void* stream);
+/* pathtrace.sample_lambertian (pathtrace.py:287-304) with teacher.orthonormal_tangents (teacher.py:302-309):
+ * normals (n,3), u1/u2 (n) -> dirs (n,3), pdf (n, nullable). */
+int knf_sample_lambertian(const double* normals, const double* u1, const double* u2, int64_t n, double* dirs, double* pdf,
+                          int device, int mem, void* stream);
+/* pathtrace.intersect_scene (pathtrace.py:311-330): nearest hit over all objects; t = +inf and obj = -1 on a miss. */
+int knf_intersect_scene(knf_scene_t sc, const double* origins, const double* dirs, int64_t n, double t_max, double* t,
+                        int32_t* obj, int mem, void* stream);
 /* Rows [row0,row1) of pathtrace.render_pathtraced (pathtrace.py:436-471): hdr (rows,W,3) f64 mean
  * radiance over samples sample_offset .. sample_offset+spp-1. */
 int knf_pathtrace(knf_scene_t sc, const KnfCamera* cam, int32_t spp, uint64_t seed, int32_t max_bounces,

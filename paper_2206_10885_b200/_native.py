@@ -137,6 +137,8 @@ _SIGNATURES = {
     "knf_scene_create": [C.POINTER(KnfObject), C.c_int32, C.POINTER(C.c_double * 3), _I32, C.POINTER(_P)],
     "knf_scene_destroy": [_P],
     "knf_rng_uniform": [C.c_uint64, _P, _P, _P, _I64, _P, _I32, _I32, _P],
+    "knf_sample_lambertian": [_P, _P, _P, _I64, _P, _P, _I32, _I32, _P],
+    "knf_intersect_scene": [_P, _P, _P, _I64, C.c_double, _P, _P, _I32, _P],
     "knf_pathtrace": [_P, C.POINTER(KnfCamera), C.c_int32, C.c_uint64, C.c_int32, C.c_int32, _I32, _I32, _P, _I32, _P],
     "knf_trace_paths": [_P, _P, _P, _P, _I64, C.c_uint64, C.c_uint64, C.c_int32, _P, _I32, _P],
 }

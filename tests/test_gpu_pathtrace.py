@@ -1,0 +1,148 @@
+"""GPU parity, part 3: the path tracer (BASELINE config 5 in miniature) through the C-ABI."""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def PT():
+    from paper_2206_10885_b200 import pathtrace
+
+    return pathtrace
+
+
+def _scenes(PT, neural_surface=None):
+    floor = PT.QuadObj((-3, -1.0, -3), (6, 0, 0), (0, 0, 6), PT.Lambertian((0.7, 0.7, 0.7)))
+    lamp = PT.SphereObj((1.5, 1.2, 0.5), 0.4, PT.Emissive((6.0, 5.0, 4.0)))
+    crate = PT.BoxObj((-1.9, -1.0, -0.6), (-1.2, -0.3, 0.1), PT.Lambertian((0.2, 0.6, 0.3)))
+    objs = [floor, lamp, crate]
+    if neural_surface is not None:
+        objs.append(PT.NeuralObject(neural_surface, translation=(0.1, -0.2, 0.0)))
+    return PT.Scene(objs, PT.ConstantEnv((0.6, 0.7, 0.9)))
+
+
+def _oracle_scene(neural=None):
+    floor = oracle.QuadShape((-3, -1.0, -3), (6, 0, 0), (0, 0, 6), oracle.Diffuse((0.7, 0.7, 0.7)))
+    lamp = oracle.SphereShape((1.5, 1.2, 0.5), 0.4, oracle.Emitter((6.0, 5.0, 4.0)))
+    crate = oracle.BoxShape((-1.9, -1.0, -0.6), (-1.2, -0.3, 0.1), oracle.Diffuse((0.2, 0.6, 0.3)))
+    objs = [floor, lamp, crate]
+    if neural is not None:
+        objs.append(oracle.NeuralShape(neural, translation=(0.1, -0.2, 0.0)))
+    return oracle.PathScene(objs, oracle.UniformSky((0.6, 0.7, 0.9)))
+
+
+def _pose():
+    from paper_2206_10885_b200.cameras import look_at_pose
+
+    return look_at_pose((0.5, 0.8, 3.2), (0, -0.2, 0), (0, 1, 0), np.deg2rad(45), 32, 24)
+
+
+def test_rng_bit_exact(PT):
+    g = golden("rng.npz")
+    for seed in (0, 12345, 2**63 + 17):
+        u = PT.Rng(seed).uniform(g["pixel"], g["sample"], g["slot"])
+        assert np.array_equal(u, g[f"u_{seed}"])
+    assert PT.Rng(7).uniform(3, 4, 5) == oracle.hash_uniform(7, 3, 4, 5)
+
+
+def test_sample_lambertian(PT):
+    rng = np.random.default_rng(0)
+    n = rng.normal(size=(5000, 3))
+    n /= np.linalg.norm(n, axis=1, keepdims=True)
+    n[:50] = [0, 0, 1.0]
+    n[50:100] = [0, 0, -1.0]
+    u1, u2 = rng.uniform(size=5000), rng.uniform(size=5000)
+    d, pdf = PT.sample_lambertian(n, (u1, u2))
+    want = oracle.cosine_sample(n, u1, u2)
+    assert np.abs(d - want).max() <= 1e-12  # fp64 sin/cos differ from NumPy's SVML in the last ulp
+    assert np.all(np.sum(d * n, axis=1) >= -1e-12)
+    assert np.allclose(pdf, np.sqrt(np.maximum(0, 1 - u1)) / np.pi)
+    one, p = PT.sample_lambertian(np.array([0.0, 0.0, 1.0]), (0.25, 0.5))
+    assert one.shape == (3,) and isinstance(p, float)
+
+
+def test_intersect_scene_nearest_wins(PT):
+    rng = np.random.default_rng(1)
+    o = np.tile([0.5, 0.8, 3.2], (4000, 1)) + rng.normal(0, 0.05, (4000, 3))
+    d = rng.normal(size=(4000, 3)) + [0, -0.3, -2.0]
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    t, obj, _ = PT.intersect_scene(_scenes(PT), o, d)
+    ot, oobj, _ = oracle.nearest_hit(_oracle_scene(), o, d)
+    assert np.array_equal(obj, oobj)
+    fin = np.isfinite(ot)
+    assert np.array_equal(np.isfinite(t), fin)
+    assert np.abs(t[fin] - ot[fin]).max() <= 1e-12
+
+
+def test_analytic_scene_matches_reference_golden(PT):
+    g = golden("pathtrace_analytic.npz")
+    out = PT.render_pathtraced(_scenes(PT), _pose(), spp=3, seed=11, max_bounces=8, sample_offset=2)
+    err = np.abs(out.hdr - g["hdr"]).max(axis=2)
+    print(f"analytic path trace: max err {err.max():.2e}, pixels within 1e-9: {(err <= 1e-9).mean():.4%}")
+    assert (err <= 1e-9).mean() >= 0.995
+    assert np.abs(out.ldr - np.clip(out.hdr, 0, 1) ** (1 / 2.2)).max() == 0
+
+
+def test_white_furnace_exact(PT):
+    from paper_2206_10885_b200.cameras import look_at_pose
+
+    scene = PT.Scene([PT.SphereObj((0, 0, 0), 0.5, PT.Lambertian((1, 1, 1)))], PT.ConstantEnv((1, 1, 1)))
+    pose = look_at_pose((0, 0, 2.0), (0, 0, 0), (0, 1, 0), np.deg2rad(40), 16, 16)
+    out = PT.render_pathtraced(scene, pose, spp=4, seed=3)
+    ocam = oracle.camera_look_at((0, 0, 2.0), (0, 0, 0), (0, 1, 0), np.deg2rad(40), 16, 16)
+    ohdr, _ = oracle.render_paths(oracle.PathScene([oracle.SphereShape((0, 0, 0), 0.5, oracle.Diffuse((1, 1, 1)))],
+                                                   oracle.UniformSky((1, 1, 1))), ocam, spp=4, seed=3)
+    assert np.abs(out.hdr - ohdr).max() <= 1e-12
+    assert np.allclose(out.hdr[0, 0], 1.0, rtol=1e-12)
+
+
+def test_spp1_equals_trace_path_and_offsets_compose(PT):
+    from paper_2206_10885_b200.surface import Ray
+
+    scene, pose = _scenes(PT), _pose()
+    a = PT.render_pathtraced(scene, pose, spp=1, seed=5, sample_offset=0).hdr
+    b = PT.render_pathtraced(scene, pose, spp=1, seed=5, sample_offset=1).hdr
+    both = PT.render_pathtraced(scene, pose, spp=2, seed=5).hdr
+    assert np.abs(both - (a + b) / 2).max() <= 1e-15
+    # pixel (row 10, col 7): rebuild its jittered ray and trace it alone (test_pathtrace.py:142-154)
+    from paper_2206_10885_b200.cameras import pixel_rays
+
+    pid = 10 * 32 + 7
+    rng = PT.Rng(5)
+    jit = np.array([[rng.uniform(pid, 0, 1 << 20), rng.uniform(pid, 0, (1 << 20) + 1)]])
+    o, d = pixel_rays(pose, np.array([[7, 10]]), jit)
+    single = PT.trace_path(scene, Ray(o[0], d[0]), rng, max_bounces=8, pixel=pid, sample=0)
+    assert np.abs(single - a[10, 7]).max() <= 1e-15
+    with pytest.raises(ValueError):
+        PT.render_pathtraced(scene, pose, spp=0, seed=1)
+
+
+def test_neural_object_scene(PT, distilled_field, distilled_oracle):
+    from paper_2206_10885_b200.surface import FieldSurface
+
+    g = golden("pathtrace_scene.npz")
+    scene = _scenes(PT, FieldSurface(distilled_field))
+    out = PT.render_pathtraced(scene, _pose(), spp=2, seed=7, max_bounces=8)
+    err = np.abs(out.hdr - g["hdr"]).max(axis=2)
+    print(f"neural path trace vs reference golden: pixels within 1e-3: {(err <= 1e-3).mean():.4%}, max {err.max():.2e}")
+    assert (err <= 1e-3).mean() >= 0.97  # secondary bounces off FD normals amplify SDF ulps; see DESIGN.md
+    t, obj, _ = PT.intersect_scene(scene, np.array([[0.5, 0.8, 3.2]]), np.array([[-0.1, -0.25, -1.0]]) / np.linalg.norm([-0.1, -0.25, -1.0]))
+    ot, oobj, _ = oracle.nearest_hit(_oracle_scene(oracle.FieldTraceable(distilled_oracle)), np.array([[0.5, 0.8, 3.2]]),
+                                     np.array([[-0.1, -0.25, -1.0]]) / np.linalg.norm([-0.1, -0.25, -1.0]))
+    assert obj[0] == oobj[0] and abs(t[0] - ot[0]) <= 1e-4
+
+
+def test_scene_validation(PT):
+    with pytest.raises(ValueError):
+        PT.SphereObj((0, 0, 0), -1.0, PT.Lambertian())
+    with pytest.raises(ValueError):
+        PT.Lambertian((1.5, 0, 0))
+    with pytest.raises(ValueError):
+        PT.QuadObj((0, 0, 0), (1, 0, 0), (2, 0, 0), PT.Lambertian())
+    with pytest.raises(TypeError):
+        PT.NeuralObject(object())
