@@ -180,8 +180,10 @@ def main():
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device: there is no CPU fallback for the product path")
     torch.cuda.set_device(local)
-    if world > 1:
+    use_dist = world > 1 or "RANK" in os.environ  # under torchrun even a single rank goes through NCCL
+    if use_dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
 
     W, H = args.width, args.height
@@ -191,15 +193,15 @@ def main():
     dev = torch.device("cuda", local)
     bufs = (torch.empty((H, W, 3), dtype=torch.float32, device=dev), torch.empty((H, W), dtype=torch.float32, device=dev),
             torch.empty((H, W, 3), dtype=torch.float32, device=dev), torch.empty((H, W), dtype=torch.uint8, device=dev))
-    gathered = torch.empty((world, H, W, 3), dtype=torch.float32, device=dev) if world > 1 else None
+    gathered = torch.empty((world, H, W, 3), dtype=torch.float32, device=dev) if use_dist else None
 
     def resident_step(s):
         surface.render_rows(fs, orbit_view(s * world + rank, W, H), settings, (1.0, 1.0, 1.0), 1, 0, H, out=bufs, device_out=True)
-        if world > 1:
+        if use_dist:
             dist.all_gather_into_tensor(gathered.view(world * H, W, 3), bufs[0], async_op=False)
 
     def barrier():
-        if world > 1:
+        if use_dist:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -219,7 +221,7 @@ def main():
         e1.record()
         barrier()
         ms = e0.elapsed_time(e1)
-        if world > 1:
+        if use_dist:
             t = torch.tensor([ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
@@ -243,7 +245,7 @@ def main():
         e2e_step(args.warmup + s)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
-    if world > 1:
+    if use_dist:
         t = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
@@ -295,7 +297,7 @@ def main():
                                     "sample": f"one {w}x{h} frame of the same camera/field ({sec:.1f} s of oracle time), extrapolated per ray to {W}x{H}",
                                     "krays_per_s": rps / 1e3, "host_cpus": os.cpu_count(), "numpy": np.__version__}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
     return 0
 

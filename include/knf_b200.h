@@ -139,6 +139,14 @@ int knf_sdf_values(knf_field_t f, const float* pts, int64_t n, float* dist, int 
 int knf_color_forward(knf_field_t f, const float* x, const float* v, const float* nrm, const float* z,
                       int64_t n, float* rgb, int mem, void* stream);
 
+/* ---- encoder + activations as stand-alone operators: nn.py:26-93 ----------------------------- */
+/* nn.fourier_encode (nn.py:66-93) for 3-vectors: x (n,3) fp32 -> out (n, 3 + 6*L) fp32, 0 <= L <= 8;
+ * bit-exact with NumPy's fp32 sin/cos + double-angle recurrence for |pi*x| < 71476. */
+int knf_fourier_encode(const float* x, int64_t n, int32_t L, float* out, int device, int mem, void* stream);
+/* nn.softplus / nn.sigmoid (nn.py:26-38), elementwise on fp32: the device routines the MLP kernels use. */
+int knf_softplus(const float* x, int64_t n, float* out, int device, int mem, void* stream);
+int knf_sigmoid(const float* x, int64_t n, float* out, int device, int mem, void* stream);
+
 /* ---- FD normals: grid.py:416-461 ---------------------------------------------------------- */
 /* grid.grad_fd (grid.py:440-451): pts (n,3) f64 -> grad (n,3) f64. */
 int knf_fd_gradient(knf_field_t f, const double* pts, int64_t n, double* grad, int mem, void* stream);

@@ -125,6 +125,9 @@ _SIGNATURES = {
     "knf_sdf_forward": [_P, _P, _I64, _P, _I32, _P],
     "knf_sdf_values": [_P, _P, _I64, _P, _I32, _P],
     "knf_color_forward": [_P, _P, _P, _P, _P, _I64, _P, _I32, _P],
+    "knf_fourier_encode": [_P, _I64, C.c_int32, _P, _I32, _I32, _P],
+    "knf_softplus": [_P, _I64, _P, _I32, _I32, _P],
+    "knf_sigmoid": [_P, _I64, _P, _I32, _I32, _P],
     "knf_fd_gradient": [_P, _P, _I64, _P, _I32, _P],
     "knf_fd_normals": [_P, _P, _I64, C.c_double, _P, _P, _I32, _P],
     "knf_pixel_rays": [C.POINTER(KnfCamera), _P, _P, _I64, _P, _P, _I32, _I32, _P],

@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "knf_engine.h"
+#include "knf_mlp.cuh"
 #include "knf_rays.cuh"
 
 using namespace knf;
@@ -204,9 +205,75 @@ uint32_t crc32_bytes(const unsigned char* p, size_t n) {
   return c ^ 0xFFFFFFFFu;
 }
 
+__global__ void fourier_encode_kernel(const float* __restrict__ x, long long n, int L, float* __restrict__ out) {
+  const float pi_f = 3.14159274101257324e+00f;
+  const int width = 3 + 6 * L;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    float* row = out + i * width;
+    float s[3], c[3];
+    for (int a = 0; a < 3; a++) {
+      float v = x[3 * i + a];
+      row[a] = v;
+      if (L > 0) np_sincosf(__fmul_rn(pi_f, v), s[a], c[a]);
+    }
+    for (int o = 0; o < L; o++)
+      for (int a = 0; a < 3; a++) {
+        row[3 + 6 * o + a] = s[a];
+        row[3 + 6 * o + 3 + a] = c[a];
+        float two_s = __fmul_rn(2.0f, s[a]);
+        float ns = __fmul_rn(two_s, c[a]);
+        float nc = __fsub_rn(1.0f, __fmul_rn(two_s, s[a]));
+        s[a] = ns;
+        c[a] = nc;
+      }
+  }
+}
+__global__ void activation_kernel(const float* __restrict__ x, long long n, int which, float* __restrict__ out) {
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = which == 0 ? softplus_f2(make_float2(x[i], x[i])).x : np_sigmoidf(x[i]);
+}
+
+int unary_op(const float* x, int64_t n, int which, float* out, int device, int mem, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !out))) return fail(KNF_E_INVALID, "bad arguments to an activation operator");
+  if (n == 0) return 0;
+  KNF_CUDA(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager S(nullptr, mem, st);
+  const float* dx = S.in(x, (size_t)n);
+  float* dout = S.out(out, (size_t)n);
+  if (S.rc) return S.rc;
+  activation_kernel<<<blocks_for((size_t)n), 256, 0, st>>>(dx, (long long)n, which, dout);
+  KNF_CUDA(cudaGetLastError());
+  return S.finish();
+}
+
 }  // namespace
 
 extern "C" {
+
+int knf_fourier_encode(const float* x, int64_t n, int32_t L, float* out, int device, int mem, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !out))) return fail(KNF_E_INVALID, "bad arguments to knf_fourier_encode");
+  if (L < 0) return fail(KNF_E_INVALID, "L must be >= 0");
+  if (L > 8) return fail(KNF_E_UNSUPPORTED, "L > 8 is not supported");
+  if (n == 0) return 0;
+  KNF_CUDA(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager S(nullptr, mem, st);
+  const float* dx = S.in(x, (size_t)n * 3);
+  float* dout = S.out(out, (size_t)n * (3 + 6 * L));
+  if (S.rc) return S.rc;
+  fourier_encode_kernel<<<blocks_for((size_t)n), 256, 0, st>>>(dx, (long long)n, L, dout);
+  KNF_CUDA(cudaGetLastError());
+  return S.finish();
+}
+int knf_softplus(const float* x, int64_t n, float* out, int device, int mem, void* stream) {
+  return unary_op(x, n, 0, out, device, mem, stream);
+}
+int knf_sigmoid(const float* x, int64_t n, float* out, int device, int mem, void* stream) {
+  return unary_op(x, n, 1, out, device, mem, stream);
+}
 
 int knf_abi_version(void) { return KNF_ABI_VERSION; }
 const char* knf_last_error(void) { return knf::last_error().c_str(); }

@@ -108,6 +108,9 @@ __device__ __forceinline__ void layer_8x8(const float* __restrict__ In, const fl
       load_operands(o, xp, wp, k0 + kk);
       fma_block(o, acc);
     }
+    // keep ptxas from prefetching the next chunk's operands across the back-edge: that rotation cost
+    // ~35 MOVs per chunk (ncu v5); the other resident warps cover the one exposed LDS latency
+    asm volatile("" ::: "memory");
   }
 }
 

@@ -26,6 +26,20 @@ PASSES = (PASS_COLOR, PASS_NORMAL, PASS_DEPTH)
 DEPTH_MISS = np.inf
 
 
+def thread_count() -> int:
+    """surface.thread_count (surface.py:32-39).  Kept for callers that size thread pools from it; the
+    device renderer does not use host threads."""
+    import os
+
+    env = os.environ.get("KNF_THREADS")
+    if env:
+        try:
+            return max(1, int(env))
+        except ValueError:
+            pass
+    return max(1, os.cpu_count() or 1)
+
+
 class RenderAborted(RuntimeError):
     """Frame rendering stopped early by the abort callback (surface.py:28-29)."""
 

@@ -19,6 +19,25 @@ def G():
     return grid
 
 
+def test_device_math_against_reference_golden():
+    """The device routines behind the MLP kernels, probed directly: the encoder (NumPy's SIMD sin/cos
+    + the fp32 double-angle recurrence) and the sigmoid (NumPy's exp + IEEE division) must be
+    BIT-EXACT with the reference; softplus (NumPy's log1p is SVML) within 2 ulp."""
+    from paper_2206_10885_b200 import nn
+
+    g = golden("encode_act.npz")
+    assert np.array_equal(nn.fourier_encode(g["x"], 6), g["enc6"])
+    assert np.array_equal(nn.fourier_encode(g["x"], 4), g["enc4"])
+    assert nn.fourier_encode(g["x"][0], 6).shape == (39,)
+    assert np.array_equal(nn.sigmoid(g["z"]), g["sigmoid"])
+    sp = nn.softplus(g["z"])
+    ulp = np.spacing(np.abs(g["softplus"]))
+    print(f"softplus vs NumPy: identical {np.mean(sp == g['softplus']):.3f}, max {np.abs(sp - g['softplus']).max():.2e}, max ulps {(np.abs(sp - g['softplus']) / ulp).max():.1f}")
+    assert np.abs(sp - g["softplus"]).max() <= 5e-7 and (np.abs(sp - g["softplus"]) / ulp).max() <= 4
+    with pytest.raises(ValueError):
+        nn.fourier_encode(g["x"], -1)
+
+
 def test_cell_ids_bit_exact_golden(G):
     g = golden("cells.npz")
     for n in (1, 4, 16):
