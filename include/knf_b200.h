@@ -189,6 +189,20 @@ int knf_render_frame(knf_field_t f, const KnfCamera* cam, const KnfSettings* s, 
                      int supersample, int row0, int row1, float* color, float* depth, float* normal,
                      uint8_t* hit, int mem, void* stream);
 
+/* ---- next rows: the interactive caller and the mesh-sampling caller ------------------- */
+enum { KNF_PASS_COLOR = 0, KNF_PASS_NORMAL = 1, KNF_PASS_DEPTH = 2 };
+/* 8(f).2 service._render_once (service.py:279-288): render_frame -> surface.pass_image (surface.py:339-350)
+ * -> images.to_uint8 (images.py:15-17) on the device; rgb is (rows,W,3) u8. */
+int knf_render_pass_u8(knf_field_t f, const KnfCamera* cam, const KnfSettings* s, const double background[3],
+                       int supersample, int render_pass, int row0, int row1, uint8_t* rgb, int mem, void* stream);
+/* images.to_uint8 of an fp64 image after clip(img / divisor, 0, 1) and, if gamma22, ** (1/2.2)
+ * (the progressive path-trace display transform, service.py:297-299). */
+int knf_tonemap_u8(const double* img, int64_t n, double divisor, int gamma22, uint8_t* out, int device, int mem, void* stream);
+/* 8(f).4 mesh._sample_volume (mesh.py:43-57): fp32 SDF values on the R^3 np.linspace lattice of
+ * [bbox_min, bbox_max], "ij" order (x slowest); values has R^3 entries. */
+int knf_sample_volume(knf_field_t f, int32_t resolution, const double bbox_min[3], const double bbox_max[3], float* values,
+                      int mem, void* stream);
+
 /* ---- path tracer: pathtrace.py -------------------------------------------------------------- */
 enum { KNF_OBJ_SPHERE = 0, KNF_OBJ_QUAD = 1, KNF_OBJ_BOX = 2, KNF_OBJ_NEURAL = 3 };
 enum { KNF_MAT_LAMBERTIAN = 0, KNF_MAT_EMISSIVE = 1 };

@@ -6,7 +6,7 @@ CUDA kernels behind the C-ABI in ``include/knf_b200.h``.  No CPU fallback.
 """
 
 from . import _native  # noqa: F401
-from . import cameras, grid, modelio, nn, surface  # noqa: F401
+from . import cameras, grid, hooks, modelio, nn, surface  # noqa: F401
 from . import pathtrace  # noqa: F401
 
 __version__ = "0.1.0"

@@ -137,6 +137,9 @@ _SIGNATURES = {
     "knf_trace_and_shade": [_P, _P, _P, _I64, C.POINTER(KnfSettings), _P, _P, _P, _P, _P, _P, _I32, _P],
     "knf_render_frame": [_P, C.POINTER(KnfCamera), C.POINTER(KnfSettings), C.POINTER(C.c_double * 3), _I32, _I32,
                          _I32, _P, _P, _P, _P, _I32, _P],
+    "knf_render_pass_u8": [_P, C.POINTER(KnfCamera), C.POINTER(KnfSettings), C.POINTER(C.c_double * 3), _I32, _I32, _I32, _I32, _P, _I32, _P],
+    "knf_tonemap_u8": [_P, _I64, C.c_double, _I32, _P, _I32, _I32, _P],
+    "knf_sample_volume": [_P, C.c_int32, C.POINTER(C.c_double * 3), C.POINTER(C.c_double * 3), _P, _I32, _P],
     "knf_scene_create": [C.POINTER(KnfObject), C.c_int32, C.POINTER(C.c_double * 3), _I32, C.POINTER(_P)],
     "knf_scene_destroy": [_P],
     "knf_rng_uniform": [C.c_uint64, _P, _P, _P, _I64, _P, _I32, _I32, _P],

@@ -235,6 +235,57 @@ __global__ void activation_kernel(const float* __restrict__ x, long long n, int 
     out[i] = which == 0 ? softplus_f2(make_float2(x[i], x[i])).x : np_sigmoidf(x[i]);
 }
 
+__global__ void pass_u8_kernel(int pass, long long n, const float* __restrict__ color, const float* __restrict__ depth,
+                               const float* __restrict__ normal, const unsigned char* __restrict__ hit,
+                               unsigned char* __restrict__ out) {
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    double v[3];
+    if (pass == KNF_PASS_COLOR) {
+      for (int a = 0; a < 3; a++) v[a] = (double)color[3 * i + a];
+    } else if (pass == KNF_PASS_NORMAL) {
+      for (int a = 0; a < 3; a++) v[a] = hit[i] ? 0.5 * ((double)normal[3 * i + a] + 1.0) : 0.0;
+    } else {
+      float d = depth[i];
+      double g = isfinite(d) ? 1.0 / (1.0 + (double)d) : 0.0;
+      v[0] = v[1] = v[2] = g;
+    }
+    for (int a = 0; a < 3; a++) out[3 * i + a] = (unsigned char)(fmin(fmax(v[a], 0.0), 1.0) * 255.0 + 0.5);
+  }
+}
+__global__ void tonemap_u8_kernel(const double* __restrict__ img, long long n, double divisor, int gamma22,
+                                  unsigned char* __restrict__ out) {
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    double v = fmin(fmax(img[i] / divisor, 0.0), 1.0);
+    if (gamma22) v = pow(v, 1.0 / 2.2);
+    out[i] = (unsigned char)(fmin(fmax(v, 0.0), 1.0) * 255.0 + 0.5);
+  }
+}
+struct LatticeDev {
+  double start[3], stop[3], step[3];
+  int res;
+};
+// np.linspace: arange(num) * step + start with the last sample forced to `stop`; meshgrid(indexing="ij").
+__global__ void lattice_emit_kernel(RouteBuffers R, GridGeom G, LatticeDev L, long long base, int n) {
+  int stride = gridDim.x * blockDim.x;
+  int n_round = (n + 31) & ~31;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n_round; s += stride) {
+    bool act = s < n;
+    float p[3] = {0.f, 0.f, 0.f};
+    if (act) {
+      long long idx = base + s;
+      int ijk[3] = {(int)(idx / ((long long)L.res * L.res)), (int)((idx / L.res) % L.res), (int)(idx % L.res)};
+      for (int a = 0; a < 3; a++) {
+        double c = ijk[a] == L.res - 1 ? L.stop[a] : (double)ijk[a] * L.step[a] + L.start[a];
+        p[a] = __double2float_rn(c);
+      }
+    }
+    route_emit(R, G, act, s, p[0], p[1], p[2]);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) R.ctr->n_requests = n;
+}
+
 int unary_op(const float* x, int64_t n, int which, float* out, int device, int mem, void* stream) {
   if (n < 0 || (n > 0 && (!x || !out))) return fail(KNF_E_INVALID, "bad arguments to an activation operator");
   if (n == 0) return 0;
@@ -766,28 +817,13 @@ int knf_trace_and_shade(knf_field_t f, const double* origins, const double* dirs
   return S.finish();
 }
 
-int knf_render_frame(knf_field_t f, const KnfCamera* cam, const KnfSettings* s, const double background[3],
-                     int supersample, int row0, int row1, float* color, float* depth, float* normal, uint8_t* hit,
-                     int mem, void* stream) {
-  KNF_TRY(check_field(f));
-  KNF_TRY(check_settings(s));
-  if (!cam || !background || !color || !depth || !normal || !hit) return fail(KNF_E_INVALID, "null argument to knf_render_frame");
-  if (supersample < 1) return fail(KNF_E_INVALID, "supersample must be >= 1");
-  if (cam->width <= 0 || cam->height <= 0) return fail(KNF_E_INVALID, "image dimensions must be positive");
-  if (row0 < 0 || row1 > cam->height || row0 >= row1) return fail(KNF_E_INVALID, "row range out of bounds");
-  Field& F = f->f;
-  std::lock_guard<std::mutex> lk(F.mu);
-  cudaStream_t st = (cudaStream_t)stream;
-  KNF_TRY(begin_call(F, st));
-  const int W_ = cam->width, ss = supersample;
+// Rows [row0,row1) of a frame into device buffers (shared by knf_render_frame and knf_render_pass_u8).
+static int render_rows_device(Field& F, const KnfCamera& cam, const KnfSettings& s, const double background[3], int ss,
+                              int row0, int row1, float* dcolor, float* ddepth, float* dnormal, uint8_t* dhit,
+                              cudaStream_t st) {
+  const int W_ = cam.width;
   const int rows = row1 - row0;
-  Stager S(&F, mem, st);
-  float* dcolor = S.out(color, (size_t)rows * W_ * 3);
-  float* ddepth = S.out(depth, (size_t)rows * W_);
-  float* dnormal = S.out(normal, (size_t)rows * W_ * 3);
-  uint8_t* dhit = S.out(hit, (size_t)rows * W_);
-  if (S.rc) return S.rc;
-  CameraDev cd = make_camera(*cam, ss);
+  CameraDev cd = make_camera(cam, ss);
   // process row chunks so a chunk holds at most ~4M sub-rays
   const int64_t per_row = (int64_t)W_ * ss * ss;
   int rows_per_chunk = (int)std::max<int64_t>(1, (4ll << 20) / per_row);
@@ -807,7 +843,7 @@ int knf_render_frame(knf_field_t f, const KnfCamera* cam, const KnfSettings* s, 
                                                              W.t_near.as<double>(), W.t_far.as<double>());
     F.stats.kernel_launches += 1;
     KNF_TRY(trace_shade_device(F, W.origins.as<double>(), W.dirs.as<double>(), W.t_near.as<double>(),
-                               W.t_far.as<double>(), n, *s, nullptr, nullptr, nullptr, nullptr,
+                               W.t_far.as<double>(), n, s, nullptr, nullptr, nullptr, nullptr,
                                W.normals64.as<double>(), W.colors64.as<double>(), st));
     compose_kernel<<<blocks_for((size_t)rc_rows * W_), 256, 0, st>>>(
         rc_rows, W_, ss, W.hit.as<unsigned char>(), W.t_hit.as<double>(), W.normals64.as<double>(),
@@ -815,6 +851,121 @@ int knf_render_frame(knf_field_t f, const KnfCamera* cam, const KnfSettings* s, 
         ddepth + (size_t)r * W_, dnormal + (size_t)r * W_ * 3, dhit + (size_t)r * W_);
     F.stats.kernel_launches += 1;
     KNF_CUDA(cudaGetLastError());
+  }
+  return 0;
+}
+
+static int check_frame_args(const KnfCamera* cam, const double* background, int supersample, int row0, int row1) {
+  if (!cam || !background) return fail(KNF_E_INVALID, "null camera or background");
+  if (supersample < 1) return fail(KNF_E_INVALID, "supersample must be >= 1");
+  if (cam->width <= 0 || cam->height <= 0) return fail(KNF_E_INVALID, "image dimensions must be positive");
+  if (row0 < 0 || row1 > cam->height || row0 >= row1) return fail(KNF_E_INVALID, "row range out of bounds");
+  return 0;
+}
+
+int knf_render_frame(knf_field_t f, const KnfCamera* cam, const KnfSettings* s, const double background[3],
+                     int supersample, int row0, int row1, float* color, float* depth, float* normal, uint8_t* hit,
+                     int mem, void* stream) {
+  KNF_TRY(check_field(f));
+  KNF_TRY(check_settings(s));
+  KNF_TRY(check_frame_args(cam, background, supersample, row0, row1));
+  if (!color || !depth || !normal || !hit) return fail(KNF_E_INVALID, "null argument to knf_render_frame");
+  Field& F = f->f;
+  std::lock_guard<std::mutex> lk(F.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  KNF_TRY(begin_call(F, st));
+  const size_t px = (size_t)(row1 - row0) * cam->width;
+  Stager S(&F, mem, st);
+  float* dcolor = S.out(color, px * 3);
+  float* ddepth = S.out(depth, px);
+  float* dnormal = S.out(normal, px * 3);
+  uint8_t* dhit = S.out(hit, px);
+  if (S.rc) return S.rc;
+  KNF_TRY(render_rows_device(F, *cam, *s, background, supersample, row0, row1, dcolor, ddepth, dnormal, dhit, st));
+  return S.finish();
+}
+
+// SURVEY 8(f).2, the interactive caller (service._render_once, service.py:279-288): render_frame ->
+// surface.pass_image (surface.py:339-350) -> images.to_uint8 (images.py:15-17), all on the device, so
+// only 3 bytes per pixel cross PCIe instead of 29.
+int knf_render_pass_u8(knf_field_t f, const KnfCamera* cam, const KnfSettings* s, const double background[3],
+                       int supersample, int render_pass, int row0, int row1, uint8_t* rgb, int mem, void* stream) {
+  KNF_TRY(check_field(f));
+  KNF_TRY(check_settings(s));
+  KNF_TRY(check_frame_args(cam, background, supersample, row0, row1));
+  if (!rgb) return fail(KNF_E_INVALID, "null output image");
+  if (render_pass < KNF_PASS_COLOR || render_pass > KNF_PASS_DEPTH) return fail(KNF_E_INVALID, "unknown pass");
+  Field& F = f->f;
+  std::lock_guard<std::mutex> lk(F.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  KNF_TRY(begin_call(F, st));
+  const size_t px = (size_t)(row1 - row0) * cam->width;
+  Stager S(&F, mem, st);
+  uint8_t* drgb = S.out(rgb, px * 3);
+  if (S.rc) return S.rc;
+  Workspace& W = F.ws;
+  KNF_TRY(W.frame_color.ensure(px * 12));
+  KNF_TRY(W.frame_depth.ensure(px * 4));
+  KNF_TRY(W.frame_normal.ensure(px * 12));
+  KNF_TRY(W.frame_hit.ensure(px));
+  KNF_TRY(render_rows_device(F, *cam, *s, background, supersample, row0, row1, W.frame_color.as<float>(),
+                             W.frame_depth.as<float>(), W.frame_normal.as<float>(), W.frame_hit.as<uint8_t>(), st));
+  pass_u8_kernel<<<blocks_for(px), 256, 0, st>>>(render_pass, (long long)px, W.frame_color.as<float>(),
+                                                W.frame_depth.as<float>(), W.frame_normal.as<float>(),
+                                                W.frame_hit.as<uint8_t>(), drgb);
+  F.stats.kernel_launches += 1;
+  KNF_CUDA(cudaGetLastError());
+  return S.finish();
+}
+
+// images.to_uint8 of an fp64 image, optionally after the path tracer's display transform
+// clip(hdr / divisor, 0, 1) ** (1 / 2.2) (service.py:297-299, pathtrace.py:470).
+int knf_tonemap_u8(const double* img, int64_t n, double divisor, int gamma22, uint8_t* out, int device, int mem, void* stream) {
+  if (n < 0 || (n > 0 && (!img || !out)) || !(divisor > 0)) return fail(KNF_E_INVALID, "bad arguments to knf_tonemap_u8");
+  if (n == 0) return 0;
+  KNF_CUDA(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)stream;
+  Stager S(nullptr, mem, st);
+  const double* din = S.in(img, (size_t)n);
+  uint8_t* dout = S.out(out, (size_t)n);
+  if (S.rc) return S.rc;
+  tonemap_u8_kernel<<<blocks_for((size_t)n), 256, 0, st>>>(din, (long long)n, divisor, gamma22, dout);
+  KNF_CUDA(cudaGetLastError());
+  return S.finish();
+}
+
+// SURVEY 8(f).4, mesh._sample_volume (mesh.py:43-57): SDF values on an R^3 np.linspace lattice
+// (x-major, "ij" order), lattice points generated on the device.
+int knf_sample_volume(knf_field_t f, int32_t resolution, const double bbox_min[3], const double bbox_max[3], float* values,
+                      int mem, void* stream) {
+  KNF_TRY(check_field(f));
+  if (resolution < 2 || !bbox_min || !bbox_max || !values) return fail(KNF_E_INVALID, "bad arguments to knf_sample_volume");
+  if (resolution > 1024) return fail(KNF_E_UNSUPPORTED, "resolution > 1024 is not supported");
+  Field& F = f->f;
+  std::lock_guard<std::mutex> lk(F.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  KNF_TRY(begin_call(F, st));
+  const int64_t R = resolution, total = R * R * R;
+  Stager S(&F, mem, st);
+  float* dvals = S.out(values, (size_t)total);
+  if (S.rc) return S.rc;
+  LatticeDev L;
+  for (int a = 0; a < 3; a++) {
+    L.start[a] = bbox_min[a];
+    L.stop[a] = bbox_max[a];
+    L.step[a] = (bbox_max[a] - bbox_min[a]) / (double)(resolution - 1);  // np.linspace's step
+  }
+  L.res = resolution;
+  const int64_t chunk = 16ll << 20;
+  for (int64_t base = 0; base < total; base += chunk) {
+    const int64_t n = std::min(chunk, total - base);
+    KNF_TRY(ensure_requests(F, (size_t)n));
+    RouteBuffers Rb = route_buffers(F, 2, -1);
+    Rb.eval_counter = stat_counter(F, 0);
+    lattice_emit_kernel<<<blocks_for((size_t)n), 256, 0, st>>>(Rb, F.geom, L, (long long)base, (int)n);
+    F.stats.kernel_launches += 1;
+    KNF_TRY(launch_scan_scatter(F, Rb, (size_t)n, st));
+    KNF_TRY(launch_sdf_mlp(F, Rb, (size_t)n, dvals + base, nullptr, st));
   }
   return S.finish();
 }

@@ -52,7 +52,7 @@ void Workspace::release_all() {
   DevBuf* all[] = {&req_pt1, &req_cell1, &req_rank1, &req_pt, &req_cell, &req_rank, &perm, &tiles, &cell_count, &cell_offset, &counters, &t, &t_prev,
                    &d_prev, &t_conv, &d_conv, &t_hit, &steps, &phase, &hit, &live0, &live1, &dval, &hit_list,
                    &hit_count, &sdf_out, &col_v, &col_n, &col_z, &rgb, &origins, &dirs, &t_near, &t_far, &normals64,
-                   &colors64, &steps_out};
+                   &colors64, &steps_out, &frame_color, &frame_depth, &frame_normal, &frame_hit};
   for (DevBuf* b : all) b->release();
   for (DevBuf& b : stage) b.release();
   req_cap = ray_cap = 0;

@@ -47,6 +47,7 @@ struct Workspace {
   DevBuf hit_list, hit_count, sdf_out, col_v, col_n, col_z, rgb;
   // render-frame ray buffers
   DevBuf origins, dirs, t_near, t_far, normals64, colors64, steps_out;
+  DevBuf frame_color, frame_depth, frame_normal, frame_hit;  // knf_render_pass_u8 intermediates
   // host staging (KNF_MEM_HOST calls): input/output mirrors
   DevBuf stage[12];
   size_t req_cap = 0;

@@ -100,10 +100,15 @@ __device__ __forceinline__ void layer_8x8(const float* __restrict__ In, const fl
     for (int j = 0; j < 8; j++) acc[i][j] = make_float2(0.0f, 0.0f);
   const float* xp = In + pg * 4;
   const float* wp = Wt + ng * 4;
+#ifndef KNF_LAYER_CHUNK
+#define KNF_LAYER_CHUNK 8
+#endif
+  constexpr int kChunk = KNF_LAYER_CHUNK == 0 ? K : KNF_LAYER_CHUNK;
+  static_assert(K % kChunk == 0, "chunk must divide K");
 #pragma unroll 1
-  for (int k0 = 0; k0 < K; k0 += 8) {
+  for (int k0 = 0; k0 < K; k0 += kChunk) {
 #pragma unroll
-    for (int kk = 0; kk < 8; kk++) {
+    for (int kk = 0; kk < kChunk; kk++) {
       LayerOperands o;
       load_operands(o, xp, wp, k0 + kk);
       fma_block(o, acc);
@@ -136,8 +141,12 @@ __device__ __forceinline__ void store_hidden(float2 (&acc)[4][8], const float* _
 
 // In-place softplus over a 32 x 64 panel: lane owns the adjacent columns 2*lane, 2*lane+1 and
 // runs both through one packed evaluation (LDS.64 / STS.64, conflict-free).
+#ifndef KNF_SP_UNROLL
+#define KNF_SP_UNROLL 4
+#endif
+constexpr int kSoftplusUnroll = KNF_SP_UNROLL;
 __device__ __forceinline__ void softplus_panel(float* __restrict__ panel, int lane) {
-#pragma unroll 4
+#pragma unroll kSoftplusUnroll
   for (int j = 0; j < kHidden; j++) {
     float2* cell = reinterpret_cast<float2*>(panel + j * kPanelLd + 2 * lane);
     *cell = softplus_f2(*cell);

@@ -1,0 +1,62 @@
+"""SURVEY 8(f) "next" rows: the callers on either side of the hot path, kept on the device.
+
+* ``render_pass_u8``  -- what ``service.RenderService._render_once`` does for the sphere-traced
+  renderer (service.py:279-288): ``to_uint8(pass_image(render_frame(...), render_pass))``, fused on the
+  GPU so 3 bytes per pixel cross PCIe instead of 29.
+* ``tonemap_u8``      -- ``to_uint8(clip(hdr / spp, 0, 1) ** (1 / 2.2))`` of the progressive path-trace
+  branch (service.py:297-299), or plain ``images.to_uint8`` (images.py:15-17).
+* ``sample_volume``   -- ``mesh._sample_volume`` (mesh.py:43-57): SDF values on the marching-cubes lattice.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+from .cameras import camera_struct
+from .grid import _default_device, device_field
+from .surface import PASSES, RenderAborted, RenderSettings, _need_field_surface, _settings_struct
+
+
+def render_pass_u8(surface, pose, settings: RenderSettings | None = None, background=(1.0, 1.0, 1.0), supersample: int = 1,
+                   tile_rows: int = 32, abort_check=None) -> np.ndarray:
+    """(H, W, 3) uint8 image of ``settings.render_pass``; ``abort_check`` is polled per band like render_frame."""
+    settings = settings or RenderSettings()
+    fs = _need_field_surface(surface)
+    cam, st, bg = camera_struct(pose), _settings_struct(settings), N.vec3(background)
+    H, W = int(pose.height), int(pose.width)
+    out = np.empty((H, W, 3), dtype=np.uint8)
+    code = PASSES.index(settings.render_pass)
+    bands = [(0, H)] if abort_check is None else [(r, min(r + tile_rows, H)) for r in range(0, H, tile_rows)]
+    for r0, r1 in bands:
+        if abort_check is not None and abort_check():
+            raise RenderAborted("camera or settings changed")
+        N.check(N.load().knf_render_pass_u8(fs.dev.handle, C.byref(cam), C.byref(st), C.byref(bg), int(supersample), code, r0, r1,
+                                            N.ptr(out[r0:r1]), N.MEM_HOST, N.current_stream(fs.dev.device)))
+    return out
+
+
+def tonemap_u8(img, divisor: float = 1.0, gamma22: bool = False, device: int | None = None) -> np.ndarray:
+    a = np.ascontiguousarray(img, dtype=np.float64)
+    out = np.empty(a.shape, dtype=np.uint8)
+    device = _default_device() if device is None else device
+    N.check(N.load().knf_tonemap_u8(N.ptr(a), a.size, float(divisor), int(bool(gamma22)), N.ptr(out), device, N.MEM_HOST,
+                                    N.current_stream(device)))
+    return out
+
+
+def to_uint8(img) -> np.ndarray:
+    """images.to_uint8 (images.py:15-17)."""
+    return tonemap_u8(img)
+
+
+def sample_volume(field, resolution: int, bbox_min=(-1.0, -1.0, -1.0), bbox_max=(1.0, 1.0, 1.0)) -> np.ndarray:
+    """mesh._sample_volume for a KiloField -> (R, R, R) float64 SDF lattice."""
+    dev = device_field(field)
+    vals = np.empty(int(resolution) ** 3, dtype=np.float32)
+    lo, hi = N.vec3(bbox_min), N.vec3(bbox_max)
+    N.check(N.load().knf_sample_volume(dev.handle, int(resolution), C.byref(lo), C.byref(hi), N.ptr(vals), N.MEM_HOST,
+                                       N.current_stream(dev.device)))
+    return vals.astype(np.float64).reshape(resolution, resolution, resolution)

@@ -1,6 +1,6 @@
 #!/bin/bash
-# A/B the tile-kernel variants built as libknf_w{1,2,4}.so
-for w in 1 2 4; do
-  echo "== KNF_TILE_WARPS=$w"
-  KNF_B200_LIB=$PWD/paper_2206_10885_b200/libknf_w$w.so python scripts/gpu_probe.py 2>&1 | grep -E "sdf_query M=|render .* (256x256|1920x1080)"
+# A/B kernel variants built as paper_2206_10885_b200/libknf_*.so (KNF_B200_LIB override)
+for lib in paper_2206_10885_b200/libknf_b200.so paper_2206_10885_b200/libknf_c*.so; do
+  echo "== $lib"
+  KNF_B200_LIB=$PWD/$lib python scripts/gpu_probe.py 2>&1 | grep -E "sdf_query M=4194304|render .* 1920x1080" | cut -c1-150
 done
