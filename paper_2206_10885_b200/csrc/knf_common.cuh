@@ -51,7 +51,10 @@ using ColBlob = BlobLayout<kColIn, kColOutPad>;    // 2756 floats = 11024 B
 // A tile is <= kTilePts requests of one cell and is processed by one warp (one-warp CTAs).
 constexpr int kWarpPts = 64;
 constexpr int kTilePts = kWarpPts;
-constexpr int kWarpCtasPerSm = 10;  // 21.5 KB of shared memory each
+#ifndef KNF_CTAS_PER_SM
+#define KNF_CTAS_PER_SM 8
+#endif
+constexpr int kWarpCtasPerSm = KNF_CTAS_PER_SM;  // 21.9 KB of shared memory each
 
 struct GridGeom {
   int resolution;

@@ -196,3 +196,17 @@ def test_knf_straight_to_device(G, distilled_field, golden_dir):
     assert np.array_equal(G.sdf_query(dev, pts).value, G.sdf_query(distilled_field, pts).value)
     with pytest.raises(OSError):
         load_model_to_device(os.path.join(golden_dir, "rng.npz"))
+
+
+def test_handle_is_thread_safe(G, small_field, small_oracle):
+    """SPEC.md:190-191 / service.py:253-255: pure functions on an immutable field, callable from many
+    host threads (ctypes releases the GIL; the handle serialises calls internally)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    rng = np.random.default_rng(11)
+    batches = [rng.uniform(-1, 1, size=(2000 + 37 * k, 3)).astype(np.float32) for k in range(12)]
+    want = [G.sdf_query(small_field, b).value for b in batches]
+    with ThreadPoolExecutor(max_workers=6) as pool:
+        got = list(pool.map(lambda b: G.sdf_query(small_field, b).value, batches * 3))
+    for k, g in enumerate(got):
+        assert np.array_equal(g, want[k % 12])
