@@ -49,7 +49,7 @@ void DevBuf::release() {
 }
 
 void Workspace::release_all() {
-  DevBuf* all[] = {&req_pt1, &req_cell1, &req_rank1, &req_pt, &req_cell, &req_rank, &perm, &tiles, &cell_count, &cell_offset, &counters, &t, &t_prev,
+  DevBuf* all[] = {&tile_base, &req_pt1, &req_cell1, &req_rank1, &req_pt, &req_cell, &req_rank, &perm, &tiles, &cell_count, &cell_offset, &counters, &t, &t_prev,
                    &d_prev, &t_conv, &d_conv, &t_hit, &steps, &phase, &hit, &live0, &live1, &dval, &hit_list,
                    &hit_count, &sdf_out, &col_v, &col_n, &col_z, &rgb, &origins, &dirs, &t_near, &t_far, &normals64,
                    &colors64, &steps_out, &frame_color, &frame_depth, &frame_normal, &frame_hit};
@@ -84,6 +84,7 @@ int ensure_requests(Field& F, size_t n) {
   bool fresh = W.cell_count.p == nullptr;
   KNF_TRY(W.cell_count.ensure((size_t)F.geom.n_cells * sizeof(int)));
   KNF_TRY(W.cell_offset.ensure(((size_t)F.geom.n_cells + 1) * sizeof(int)));
+  KNF_TRY(W.tile_base.ensure(((size_t)F.geom.n_cells + 1) * sizeof(int)));
   KNF_TRY(W.counters.ensure(kCounterBytes));
   if (fresh) {
     KNF_CUDA(cudaMemset(W.cell_count.p, 0, W.cell_count.cap));
@@ -129,6 +130,7 @@ RouteBuffers route_buffers(Field& F, int slot, int next_slot, int list) {
   R.req_rank = (list ? W.req_rank1 : W.req_rank).as<int>();
   R.cell_count = W.cell_count.as<int>();
   R.cell_offset = W.cell_offset.as<int>();
+  R.tile_base = W.tile_base.as<int>();
   R.perm = W.perm.as<int>();
   R.tiles = W.tiles.as<Tile>();
   R.ctr = counters(F, slot);
@@ -207,7 +209,7 @@ int launch_scan_scatter(Field& F, const RouteBuffers& R, size_t n_upper, cudaStr
                         int* n_seg) {
   ProfScope prof(F, st, SPAN_ROUTE);
   route_scan_kernel<<<1, kScanThreads, 0, st>>>(R, F.geom.n_cells, seg_cell, seg_start, n_seg);
-  route_scatter_kernel<<<blocks_for(n_upper), 256, 0, st>>>(R);
+  route_scatter_kernel<<<blocks_for(std::max<size_t>(n_upper, (size_t)F.geom.n_cells)), 256, 0, st>>>(R, F.geom.n_cells);
   F.stats.kernel_launches += 2;
   KNF_CUDA(cudaGetLastError());
   return 0;

@@ -39,7 +39,7 @@ struct Workspace {
   // routing (two independent sets: A for SDF passes, B for the colour pass of shading)
   DevBuf req_pt, req_cell, req_rank, perm, tiles;
   DevBuf req_pt1, req_cell1, req_rank1;  // second request list: the fused march kernel reads one list while filling the other
-  DevBuf cell_count, cell_offset;
+  DevBuf cell_count, cell_offset, tile_base;
   DevBuf counters;  // RouteCounters[4] + stats counters
   // march state
   DevBuf t, t_prev, d_prev, t_conv, d_conv, t_hit, steps, phase, hit, live0, live1, dval;

@@ -70,6 +70,20 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(M
       }
     }
     zero_pad_rows<kSdfIn>(X, lane);
+    // fp32 box strictly inside the tile's cell: a point inside it is in this cell without redoing the
+    // fp64 cell arithmetic (cell_coord is monotone and its rounding error is ~1e-16 of the extent, the
+    // margin is 1e-6 of it); anything closer to a face takes the exact path.
+    float in_lo[3], in_hi[3];
+    {
+      const int N = A.G.resolution;
+      const int ci[3] = {tile.cell / (N * N), (tile.cell / N) % N, tile.cell % N};
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        const double ext = A.G.hi[a] - A.G.lo[a];
+        in_lo[a] = (float)(A.G.lo[a] + ext * ((double)ci[a] / N) + 1e-6 * ext);
+        in_hi[a] = (float)(A.G.lo[a] + ext * ((double)(ci[a] + 1) / N) - 1e-6 * ext);
+      }
+    }
     int n_active = tile.count;
 
     for (int inner = 0;; inner++) {
@@ -99,7 +113,9 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(M
             px[q] = __double2float_rn(rr[q].o[0] + t_next * rr[q].d[0]);
             py[q] = __double2float_rn(rr[q].o[1] + t_next * rr[q].d[1]);
             pz[q] = __double2float_rn(rr[q].o[2] + t_next * rr[q].d[2]);
-            cell[q] = cell_of(px[q], py[q], pz[q], A.G);
+            const bool well_inside = px[q] > in_lo[0] && px[q] < in_hi[0] && py[q] > in_lo[1] && py[q] < in_hi[1] &&
+                                     pz[q] > in_lo[2] && pz[q] < in_hi[2];
+            cell[q] = well_inside ? tile.cell : cell_of(px[q], py[q], pz[q], A.G);
           }
         }
         stay[q] = want[q] && cell[q] == tile.cell;
@@ -110,12 +126,14 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(M
 #pragma unroll
       for (int q = 0; q < 2; q++) {
         const bool emit = want[q] && !(cont && stay[q]);
-        const int slot = warp_append(&A.next.ctr->n_requests, emit);
-        if (emit) {
-          A.live_out[slot] = ray[q];
-          ray_store(rr[q], A.M, ray[q]);
+        if (__any_sync(0xffffffffu, emit)) {  // warp-uniform: skip the collectives when nobody leaves
+          const int slot = warp_append(&A.next.ctr->n_requests, emit);
+          if (emit) {
+            A.live_out[slot] = ray[q];
+            ray_store(rr[q], A.M, ray[q]);
+          }
+          route_emit_cell(A.next, emit, slot, px[q], py[q], pz[q], cell[q]);
         }
-        route_emit_cell(A.next, emit, slot, px[q], py[q], pz[q], cell[q]);
         active[q] = cont && stay[q];
         if (!active[q]) px[q] = py[q] = pz[q] = 0.f;
       }

@@ -25,6 +25,7 @@ struct RouteBuffers {
   int* req_rank;      // [cap]
   int* cell_count;    // [n_cells], zero on entry to a pass
   int* cell_offset;   // [n_cells + 1]
+  int* tile_base;     // [n_cells + 1] first tile of each cell
   int* perm;          // [cap]
   Tile* tiles;        // [cap / kTilePts + n_cells + 1]
   RouteCounters* ctr; // this pass
@@ -85,13 +86,59 @@ static __global__ void cell_index_kernel(GridGeom G, const T* __restrict__ pts, 
 
 constexpr int kScanThreads = 1024;
 
-// One CTA.  Optionally emits grid.route's occupied segments (cells ascending, starts).
+// Three-lane block-wide exclusive scan step built from warp shuffles (2 block barriers).
+__device__ __forceinline__ void block_scan3(int& a, int& b, int& c, int* s_warp /*[3*32]*/, int& ta, int& tb, int& tc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int ia = a, ib = b, ic = c;  // inclusive within the warp
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    int xa = __shfl_up_sync(0xffffffffu, ia, off), xb = __shfl_up_sync(0xffffffffu, ib, off),
+        xc = __shfl_up_sync(0xffffffffu, ic, off);
+    if (lane >= off) {
+      ia += xa;
+      ib += xb;
+      ic += xc;
+    }
+  }
+  if (lane == 31) {
+    s_warp[warp] = ia;
+    s_warp[32 + warp] = ib;
+    s_warp[64 + warp] = ic;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    int wa = s_warp[lane], wb = s_warp[32 + lane], wc = s_warp[64 + lane];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      int xa = __shfl_up_sync(0xffffffffu, wa, off), xb = __shfl_up_sync(0xffffffffu, wb, off),
+          xc = __shfl_up_sync(0xffffffffu, wc, off);
+      if (lane >= off) {
+        wa += xa;
+        wb += xb;
+        wc += xc;
+      }
+    }
+    s_warp[lane] = wa;  // inclusive warp totals
+    s_warp[32 + lane] = wb;
+    s_warp[64 + lane] = wc;
+  }
+  __syncthreads();
+  const int pa = warp ? s_warp[warp - 1] : 0, pb = warp ? s_warp[32 + warp - 1] : 0, pc = warp ? s_warp[64 + warp - 1] : 0;
+  ta = s_warp[31];
+  tb = s_warp[63];
+  tc = s_warp[95];
+  a = pa + ia - a;  // exclusive prefix of this thread
+  b = pb + ib - b;
+  c = pc + ic - c;
+}
+
+// One CTA: per-cell request offsets and per-cell tile bases (the tile descriptors themselves are
+// written in parallel by route_scatter_kernel).  Optionally emits grid.route's occupied segments
+// (cells ascending, starts).  Re-zeroes the cell counters and the next pass's counters.
 static __global__ void __launch_bounds__(kScanThreads) route_scan_kernel(RouteBuffers R, int n_cells, int* __restrict__ seg_cell,
                                                                   int* __restrict__ seg_start,
                                                                   int* __restrict__ n_seg_out) {
-  __shared__ int s_pts[kScanThreads];
-  __shared__ int s_tiles[kScanThreads];
-  __shared__ int s_segs[kScanThreads];
+  __shared__ int s_warp[96];
   const int tid = threadIdx.x;
   const int per = (n_cells + kScanThreads - 1) / kScanThreads;
   const int c0 = min(tid * per, n_cells);
@@ -103,53 +150,29 @@ static __global__ void __launch_bounds__(kScanThreads) route_scan_kernel(RouteBu
     tl += (k + kTilePts - 1) / kTilePts;
     sg += (k > 0);
   }
-  s_pts[tid] = pts;
-  s_tiles[tid] = tl;
-  s_segs[tid] = sg;
-  __syncthreads();
-  // Hillis-Steele inclusive scan over 1024 partials (three lanes of data)
-  for (int off = 1; off < kScanThreads; off <<= 1) {
-    int a = 0, b = 0, c = 0;
-    if (tid >= off) {
-      a = s_pts[tid - off];
-      b = s_tiles[tid - off];
-      c = s_segs[tid - off];
-    }
-    __syncthreads();
-    s_pts[tid] += a;
-    s_tiles[tid] += b;
-    s_segs[tid] += c;
-    __syncthreads();
-  }
-  int p_base = s_pts[tid] - pts;
-  int t_base = s_tiles[tid] - tl;
-  int g_base = s_segs[tid] - sg;
+  int p_base = pts, t_base = tl, g_base = sg, tot_p, tot_t, tot_g;
+  block_scan3(p_base, t_base, g_base, s_warp, tot_p, tot_t, tot_g);
   for (int c = c0; c < c1; c++) {
     int k = R.cell_count[c];
     R.cell_offset[c] = p_base;
+    R.tile_base[c] = t_base;
     R.cell_count[c] = 0;  // ready for the next pass
     if (k > 0 && seg_cell) {
       seg_cell[g_base] = c;
       seg_start[g_base] = p_base;
       g_base++;
     }
-    for (int s = 0; s < k; s += kTilePts) {
-      Tile t;
-      t.cell = c;
-      t.start = p_base + s;
-      t.count = min(kTilePts, k - s);
-      t.pad = 0;
-      R.tiles[t_base++] = t;
-    }
+    t_base += (k + kTilePts - 1) / kTilePts;
     p_base += k;
   }
   if (tid == kScanThreads - 1) {
-    R.cell_offset[n_cells] = s_pts[tid];
-    R.ctr->n_tiles = s_tiles[tid];
+    R.cell_offset[n_cells] = tot_p;
+    R.tile_base[n_cells] = tot_t;
+    R.ctr->n_tiles = tot_t;
     R.ctr->tile_cursor = 0;
-    if (R.eval_counter) *R.eval_counter += (unsigned long long)s_pts[tid];
-    if (seg_start) seg_start[s_segs[tid]] = s_pts[tid];
-    if (n_seg_out) *n_seg_out = s_segs[tid];
+    if (R.eval_counter) *R.eval_counter += (unsigned long long)tot_p;
+    if (seg_start) seg_start[tot_g] = tot_p;
+    if (n_seg_out) *n_seg_out = tot_g;
     if (R.next_ctr) {
       R.next_ctr->n_requests = 0;
       R.next_ctr->n_tiles = 0;
@@ -158,11 +181,24 @@ static __global__ void __launch_bounds__(kScanThreads) route_scan_kernel(RouteBu
   }
 }
 
-static __global__ void route_scatter_kernel(RouteBuffers R) {
+// perm[offset[cell] + rank] = request slot, and (in the same launch) the tile descriptors of every cell.
+static __global__ void route_scatter_kernel(RouteBuffers R, int n_cells) {
   const int n = R.ctr->n_requests;
-  int stride = gridDim.x * blockDim.x;
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += stride)
-    R.perm[R.cell_offset[R.req_cell[s]] + R.req_rank[s]] = s;
+  const int stride = gridDim.x * blockDim.x;
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int s = gid; s < n; s += stride) R.perm[R.cell_offset[R.req_cell[s]] + R.req_rank[s]] = s;
+  for (int c = gid; c < n_cells; c += stride) {
+    const int start = R.cell_offset[c], k = R.cell_offset[c + 1] - start;
+    int tb = R.tile_base[c];
+    for (int s = 0; s < k; s += kTilePts) {
+      Tile t;
+      t.cell = c;
+      t.start = start + s;
+      t.count = min(kTilePts, k - s);
+      t.pad = 0;
+      R.tiles[tb++] = t;
+    }
+  }
 }
 
 }  // namespace knf
