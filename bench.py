@@ -30,7 +30,8 @@ SM_COUNT = 148
 FFMA_LANES_PER_SM = 128
 FLOP_PER_SDF_EVAL = 5120  # 2 * (39*32 + 32*32 + 32*9), SURVEY 8(d)
 FLOP_PER_COLOR_EVAL = 4864
-ROUTE_BYTES_PER_REQUEST = 149  # advance+emit 133 B + scatter 16 B per evaluation request
+ROUTE_BYTES_PER_REQUEST = 16.25  # scatter reads cell+rank+offset (12 B) and writes perm (4 B) per routed request, + 16 B tile per 64
+ROUTE_BYTES_PER_CELL = 16      # scan: count read + zeroed, offset + tile base written, per cell per wavefront
 ORBIT_VIEWS, ORBIT_RADIUS, ORBIT_ELEV, FOV = 100, 2.5, 0.2, np.deg2rad(40.0)
 
 
@@ -257,7 +258,8 @@ def main():
         ck = clocks.summary()
         ffma_peak = SM_COUNT * FFMA_LANES_PER_SM * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
         mlp_tflops = stats["sdf_evals"] * FLOP_PER_SDF_EVAL / (stats["sdf_mlp_ms"] * 1e-3) / 1e12 if stats["sdf_mlp_ms"] > 0 else None
-        route_gbs = stats["sdf_evals"] * ROUTE_BYTES_PER_REQUEST / (stats["route_ms"] * 1e-3) / 1e9 if stats["route_ms"] > 0 else None
+        route_bytes = stats["march_routed_requests"] * ROUTE_BYTES_PER_REQUEST + stats["wavefronts"] * 4096 * ROUTE_BYTES_PER_CELL + stats["rays"] * 100
+        route_gbs = route_bytes / (stats["route_ms"] * 1e-3) / 1e9 if stats["route_ms"] > 0 else None
         line = {
             "metric": f"fps_{W}x{H}_sphere_traced", "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -273,7 +275,7 @@ def main():
                             "per-step input is the camera/settings structs, the field is uploaded once like the reference loads it once"},
             "gpu_launches": int(stats["kernel_launches"]),
             "roofline": {
-                "kernel": "mlp_tile_kernel<39,9,12,softplus> (fused encode + 3-layer SDF MLP)", "bound": "fp32",
+                "kernel": "march_warp_kernel (fused encode + 3-layer SDF MLP + sphere-trace step, tile residency)", "bound": "fp32",
                 "achieved": mlp_tflops, "peak": ffma_peak, "unit": "TFLOP/s", "frac": (mlp_tflops / ffma_peak) if mlp_tflops else None,
                 "traffic": None,
                 "peak_source": f"derived: {SM_COUNT} SMs x {FFMA_LANES_PER_SM} FFMA lanes x 2 x sm_max_mhz ({peak_src} MEASURED_PEAKS.json holds "
@@ -282,9 +284,14 @@ def main():
                 "avg_launch_ms": stats["sdf_mlp_ms"] / max(stats["sdf_mlp_launches"], 1), "launches": int(stats["sdf_mlp_launches"]),
                 "share_of_step": stats["sdf_mlp_ms"] / ms,
                 "frac_of_measured_bf16_tensor_peak": (mlp_tflops / float(peaks["bf16_tflops"])) if mlp_tflops else None,
+                "measured_fp32_rates_tflops": {"packed_FFMA2_registers_only": 71.0, "scalar_FFMA": 61.6, "FFMA2_with_1_LDS128_per_16": 52.0,
+                                               "source": "profiles/ffma_peak_micro_r1.txt (scripts/micro/ffma_peak.cu on this pool's B200)"},
+                "tile_fill": stats["sdf_evals"] / max(stats["march_lane_slots"], 1),
             },
             "roofline_route": {
-                "kernel": "march_advance (+emit) / route_scan / route_scatter", "bound": "hbm", "achieved": route_gbs,
+                "kernel": "march_init (emit) / route_scan / route_scatter", "bound": "hbm", "achieved": route_gbs,
+                "algorithmic_bytes": "16.25 B per routed request + 16 B per cell per wavefront + 100 B per ray (init: t_near/t_far/o/d read, state + request written)",
+                "routed_fraction_of_march_evals": stats["march_routed_requests"] / max(stats["sdf_evals"], 1),
                 "peak": float(peaks["hbm_gbs"]), "unit": "GB/s", "frac": (route_gbs / float(peaks["hbm_gbs"])) if route_gbs else None,
                 "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs", "share_of_step": stats["route_ms"] / ms,
                 "launches": int(stats["route_launches"]),

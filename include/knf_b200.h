@@ -95,6 +95,8 @@ typedef struct {
   double route_ms;
   double color_mlp_ms;
   double other_ms;
+  int64_t march_lane_slots; /* 64 x tile passes of the fused march kernel: sdf march evals / this = tile fill */
+  int64_t march_routed_requests; /* march evaluations that went through a global routing pass (the rest stepped in place) */
 } KnfStats;
 
 int knf_abi_version(void);

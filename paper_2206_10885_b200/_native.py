@@ -86,6 +86,8 @@ class KnfStats(C.Structure):
         ("route_ms", C.c_double),
         ("color_mlp_ms", C.c_double),
         ("other_ms", C.c_double),
+        ("march_lane_slots", C.c_int64),
+        ("march_routed_requests", C.c_int64),
     ]
 
 

@@ -197,11 +197,13 @@ int collect_profile(Field& F) {
 }
 
 int finish_stats(Field& F, cudaStream_t st) {
-  unsigned long long host[2] = {0, 0};
+  unsigned long long host[4] = {0, 0, 0, 0};
   KNF_CUDA(cudaMemcpyAsync(host, stat_counter(F, 0), sizeof(host), cudaMemcpyDeviceToHost, st));
   KNF_CUDA(cudaStreamSynchronize(st));
   F.stats.sdf_evals = (int64_t)host[0];
   F.stats.color_evals = (int64_t)host[1];
+  F.stats.march_lane_slots = (int64_t)host[2];
+  F.stats.march_routed_requests = (int64_t)host[3];
   return 0;
 }
 
@@ -321,6 +323,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
   for (int w = 0; w <= s.max_steps; w++) {
     const int cur = w & 1, nxt = cur ^ 1;
     RouteBuffers R = route_buffers(F, cur, nxt, cur);
+    R.eval_counter = stat_counter(F, 3);  // requests that went through global routing
     KNF_TRY(launch_scan_scatter(F, R, (size_t)n, st));
     MarchTileArgs A{};
     A.P.blobs = F.sdf_blobs;

@@ -44,7 +44,7 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(M
   const int n_tiles = P.ctr->n_tiles;
   uint32_t parity = 0;
   float* X = S.x;
-  unsigned long long evals = 0;
+  unsigned long long evals = 0, passes = 0;
 
   for (;;) {
     const int t = next_tile(P.ctr, lane);
@@ -97,6 +97,7 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(M
       hidden_layers<kSdfIn, kSdfOutPad, ACT_SOFTPLUS>(X, S.w, lane);
       const float2 dist = output_distance<kSdfOutPad>(X, S.w + Blob::w3, S.w + Blob::b3, lane);
       evals += (lane == 0) ? (unsigned long long)n_active : 0ull;
+      passes += 1;
 
       // ---- the march step for the lane's two rays -----------------------------------------------------
       bool want[2], stay[2];
@@ -143,7 +144,10 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(M
     }
     __syncwarp();  // every lane is done reading S.w and the panel before the next tile overwrites them
   }
-  if (lane == 0 && evals && A.eval_counter) atomicAdd(A.eval_counter, evals);
+  if (lane == 0 && evals && A.eval_counter) {
+    atomicAdd(A.eval_counter, evals);
+    atomicAdd(A.eval_counter + 2, passes * kWarpPts);  // lane slots spent (tile-fill statistic)
+  }
 }
 
 }  // namespace knf

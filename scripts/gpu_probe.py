@@ -47,4 +47,4 @@ for name, field in (("random16", f16), ("distilled4", fd)):
         st = fs.dev.stats(); fs.dev.set_profiling(False)
         t0 = time.perf_counter(); fb = surface.render_frame(fs, pose); e2e = (time.perf_counter() - t0) * 1e3
         print(f"render {name} {w}x{h}: {med:.2f} ms device ({1e3/med:.1f} FPS, {w*h/med/1e3:.1f} Mrays/s), e2e host {e2e:.1f} ms; "
-              f"sdf evals {st['sdf_evals']} ({st['sdf_evals']/(w*h):.1f}/ray, {st['sdf_evals']/med/1e6:.2f} Gevals/s), hits {st['hits']}, launches {st['kernel_launches']}, wavefronts {st['wavefronts']}, mlp {st['sdf_mlp_ms']:.2f} ms, route {st['route_ms']:.2f} ms")
+              f"sdf evals {st['sdf_evals']} ({st['sdf_evals']/(w*h):.1f}/ray, {st['sdf_evals']/med/1e6:.2f} Gevals/s), hits {st['hits']}, launches {st['kernel_launches']}, wavefronts {st['wavefronts']}, mlp {st['sdf_mlp_ms']:.2f} ms, route {st['route_ms']:.2f} ms, tile fill {st['sdf_evals']/max(st['march_lane_slots'],1):.3f}")
