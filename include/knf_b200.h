@@ -205,6 +205,13 @@ int knf_tonemap_u8(const double* img, int64_t n, double divisor, int gamma22, ui
 int knf_sample_volume(knf_field_t f, int32_t resolution, const double bbox_min[3], const double bbox_max[3], float* values,
                       int mem, void* stream);
 
+/* 8(f).3 training._volume_forward (training.py:330-415), forward only: S-density volume rendering of a ray
+ * batch with n_s stratified samples per ray.  jitter (n_rays,n_s) f64 in [0,1) or NULL for 0.5; s_param =
+ * exp(inv_std_param); colors (n_rays,3) f64 in [0,1]. */
+int knf_volume_forward(knf_field_t f, const double* origins, const double* dirs, int64_t n_rays, int32_t n_s,
+                       const double* jitter, const double background[3], double s_param, double* colors, int mem,
+                       void* stream);
+
 /* ---- path tracer: pathtrace.py -------------------------------------------------------------- */
 enum { KNF_OBJ_SPHERE = 0, KNF_OBJ_QUAD = 1, KNF_OBJ_BOX = 2, KNF_OBJ_NEURAL = 3 };
 enum { KNF_MAT_LAMBERTIAN = 0, KNF_MAT_EMISSIVE = 1 };

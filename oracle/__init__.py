@@ -58,6 +58,7 @@ from .trace import (  # noqa: F401
     render,
     pass_image,
 )
+from .volume import volume_forward  # noqa: F401
 from .paths import (  # noqa: F401
     hash_uniform,
     SphereShape,

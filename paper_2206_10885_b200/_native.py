@@ -142,6 +142,7 @@ _SIGNATURES = {
     "knf_render_pass_u8": [_P, C.POINTER(KnfCamera), C.POINTER(KnfSettings), C.POINTER(C.c_double * 3), _I32, _I32, _I32, _I32, _P, _I32, _P],
     "knf_tonemap_u8": [_P, _I64, C.c_double, _I32, _P, _I32, _I32, _P],
     "knf_sample_volume": [_P, C.c_int32, C.POINTER(C.c_double * 3), C.POINTER(C.c_double * 3), _P, _I32, _P],
+    "knf_volume_forward": [_P, _P, _P, _I64, C.c_int32, _P, C.POINTER(C.c_double * 3), C.c_double, _P, _I32, _P],
     "knf_scene_create": [C.POINTER(KnfObject), C.c_int32, C.POINTER(C.c_double * 3), _I32, C.POINTER(_P)],
     "knf_scene_destroy": [_P],
     "knf_rng_uniform": [C.c_uint64, _P, _P, _P, _I64, _P, _I32, _I32, _P],

@@ -186,7 +186,10 @@ static __global__ void route_scatter_kernel(RouteBuffers R, int n_cells) {
   const int n = R.ctr->n_requests;
   const int stride = gridDim.x * blockDim.x;
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-  for (int s = gid; s < n; s += stride) R.perm[R.cell_offset[R.req_cell[s]] + R.req_rank[s]] = s;
+  for (int s = gid; s < n; s += stride) {
+    const int c = R.req_cell[s];  // -1: a slot its producer left empty (knf_volume.cu)
+    if (c >= 0) R.perm[R.cell_offset[c] + R.req_rank[s]] = s;
+  }
   for (int c = gid; c < n_cells; c += stride) {
     const int start = R.cell_offset[c], k = R.cell_offset[c + 1] - start;
     int tb = R.tile_base[c];

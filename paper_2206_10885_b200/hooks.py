@@ -60,3 +60,39 @@ def sample_volume(field, resolution: int, bbox_min=(-1.0, -1.0, -1.0), bbox_max=
     N.check(N.load().knf_sample_volume(dev.handle, int(resolution), C.byref(lo), C.byref(hi), N.ptr(vals), N.MEM_HOST,
                                        N.current_stream(dev.device)))
     return vals.astype(np.float64).reshape(resolution, resolution, resolution)
+
+
+def volume_forward(field, origins, dirs, n_s: int, jitter=None, background=(1.0, 1.0, 1.0), s: float | None = None) -> np.ndarray:
+    """training._volume_forward (training.py:330-415), forward only -> (B,3) float64 colours.
+
+    ``s`` defaults to ``exp(field.inv_std_param)`` like the reference.  (Rays that miss the box return the
+    background clipped to [0,1]; the reference leaves it unclipped when other rays of the batch are active.)
+    """
+    dev = device_field(field)
+    o = np.ascontiguousarray(np.atleast_2d(origins), dtype=np.float64)
+    d = np.ascontiguousarray(np.atleast_2d(dirs), dtype=np.float64)
+    if o.shape != d.shape or o.shape[1] != 3:
+        raise ValueError("origins and dirs must both be (B,3)")
+    B = o.shape[0]
+    jit = None
+    if jitter is not None:
+        jit = np.ascontiguousarray(jitter, dtype=np.float64)
+        if jit.shape != (B, n_s):
+            raise ValueError("jitter must be (B, n_s)")
+    if s is None:
+        s = float(np.exp(field.inv_std_param))
+    out = np.empty((B, 3), dtype=np.float64)
+    bg = N.vec3(background)
+    N.check(N.load().knf_volume_forward(dev.handle, N.ptr(o), N.ptr(d), B, int(n_s), N.ptr(jit), C.byref(bg), float(s), N.ptr(out),
+                                        N.MEM_HOST, N.current_stream(dev.device)))
+    return out
+
+
+def photometric_loss(field, pose, pixels, target, n_s: int, jitter=None, background=(1.0, 1.0, 1.0)) -> float:
+    """training.photometric_loss (training.py:500-517): mean L1 between volume-rendered and target colours.
+    ``target`` is the (B,3) colour of each pixel (the reference indexes image.pixels itself)."""
+    from .cameras import pixel_rays
+
+    origins, dirs = pixel_rays(pose, pixels)
+    colors = volume_forward(field, origins, dirs, n_s, jitter, background)
+    return float(np.abs(colors - np.asarray(target, dtype=np.float64)).sum() / len(colors))

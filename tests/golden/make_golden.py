@@ -188,6 +188,19 @@ def main():
     out = PT.render_pathtraced(analytic, pose_pt, spp=3, seed=11, max_bounces=8, sample_offset=2)
     put("pathtrace_analytic.npz", hdr=out.hdr, ldr=out.ldr)
 
+    # -- 10. volume-render forward (training._volume_forward), distilled field -------------------------------
+    from kilofield import training as T
+
+    rng = np.random.default_rng(606)
+    pose_v = look_at_pose((0.3, 0.5, 2.4), (0, 0, 0), (0, 1, 0), np.deg2rad(40), 64, 64)
+    pix = np.stack([rng.integers(0, 64, 400), rng.integers(0, 64, 400)], axis=1)
+    vo, vd = pixel_rays(pose_v, pix)
+    vo[:20] += [3.0, 0.0, 0.0]  # a few rays that miss the box
+    jit = rng.uniform(size=(400, 24))
+    col, _ = T._volume_forward(fd, vo, vd, 24, jit, (1.0, 1.0, 1.0))
+    col_mid, _ = T._volume_forward(fd, vo, vd, 16, None, (0.2, 0.4, 0.6))
+    put("volume_forward.npz", origins=vo, dirs=vd, jitter=jit, colors=col, colors_nojitter=col_mid, s=np.float64(fd.s))
+
     with open(os.path.join(HERE, "golden_meta.json"), "w") as fh:
         json.dump(meta, fh, indent=1, default=float)
     print("done")

@@ -134,3 +134,11 @@ def test_pathtrace_with_neural_object(distilled_oracle):
     hdr, _ = oracle.render_paths(_scene(oracle.FieldTraceable(distilled_oracle)), cam, spp=2, seed=7, max_bounces=8)
     close = np.abs(hdr - g["hdr"]).max(axis=2) <= 1e-3
     assert close.mean() >= 0.99
+
+
+def test_volume_forward(distilled_oracle):
+    g = golden("volume_forward.npz")
+    col = oracle.volume_forward(distilled_oracle, g["origins"], g["dirs"], 24, g["jitter"], (1.0, 1.0, 1.0), s=float(g["s"]))
+    assert np.abs(col - g["colors"]).max() <= 1e-6
+    col = oracle.volume_forward(distilled_oracle, g["origins"], g["dirs"], 16, None, (0.2, 0.4, 0.6), s=float(g["s"]))
+    assert np.abs(col - g["colors_nojitter"]).max() <= 1e-6
