@@ -44,41 +44,90 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """Polls nvidia-smi during the timed region (B200_PROFILING.md 'clocks' line)."""
+    """Samples SM clocks and throttle reasons during the timed region (B200_PROFILING.md 'clocks' line).
+
+    Uses NVML in-process (nvidia_ml_py) every 250 ms: spawning one nvidia-smi per sample was measured to
+    slow the timed frames by ~25 % (driver-lock contention), a long-lived `nvidia-smi -lms` is the fallback.
+    """
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
-        self.index, self.rows, self._stop, self._t = index, [], threading.Event(), None
+        self.index, self.rows, self._stop, self._t, self._proc = index, [], threading.Event(), None, None
+        self.nvml = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(self._physical_index(index))
+        except Exception:
+            self.nvml = None
+
+    @staticmethod
+    def _physical_index(index):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            try:
+                return int(vis.split(",")[index])
+            except Exception:
+                return index
+        return index
+
+    def _nvml_row(self):
+        n = self.nvml
+        sm = n.nvmlDeviceGetClockInfo(self.handle, n.NVML_CLOCK_SM)
+        mx = n.nvmlDeviceGetMaxClockInfo(self.handle, n.NVML_CLOCK_SM)
+        try:
+            mask = n.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+        except Exception:
+            mask = n.nvmlDeviceGetCurrentClocksThrottleReasons(self.handle)
+        flags = {"hw_slowdown": 0x8, "sw_power_cap": 0x4, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
+        return sm, mx, [k for k, bit in flags.items() if mask & bit]
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([c.strip() for c in out.split(",")])
+                self.rows.append(self._nvml_row())
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.25)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        if self.nvml is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        else:
+            try:
+                self._proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                               "-lms", "250"], stdout=subprocess.PIPE, text=True)
+            except Exception:
+                self._proc = None
         return self
 
     def __exit__(self, *a):
         self._stop.set()
-        self._t.join(timeout=6)
+        if self._t is not None:
+            self._t.join(timeout=3)
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                out = self._proc.communicate(timeout=3)[0]
+            except Exception:
+                out = ""
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for line in out.splitlines():
+                c = [x.strip() for x in line.split(",")]
+                if len(c) >= 7 and c[0].replace(".", "").isdigit():
+                    self.rows.append((float(c[0]), float(c[1]), [n for n, v in zip(names, c[3:7]) if v.lower().startswith("active")]))
 
     def summary(self):
-        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows if len(r) >= 7 for n, v in zip(names, r[3:7]) if v.lower().startswith("active")})
+        sm = [float(r[0]) for r in self.rows]
+        mx = [float(r[1]) for r in self.rows]
+        reasons = sorted({x for r in self.rows for x in r[2]})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(sm)}
+                "reasons": reasons, "samples": len(sm), "source": "nvml" if self.nvml is not None else "nvidia-smi -lms"}
 
 
 def orbit_view(k: int, width: int, height: int):
@@ -277,7 +326,9 @@ def main():
             "roofline": {
                 "kernel": "march_warp_kernel (fused encode + 3-layer SDF MLP + sphere-trace step, tile residency)", "bound": "fp32",
                 "achieved": mlp_tflops, "peak": ffma_peak, "unit": "TFLOP/s", "frac": (mlp_tflops / ffma_peak) if mlp_tflops else None,
-                "traffic": None,
+                "traffic": 257.4e6,
+                "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of ONE dense wavefront launch (2.0 ms, ~9.6 M evaluations) from "
+                                "profiles/ncu_r1_march_v6 (ncu --set full); weights (45 MB) and ray state are L2-resident, DRAM is 1.3 % busy",
                 "peak_source": f"derived: {SM_COUNT} SMs x {FFMA_LANES_PER_SM} FFMA lanes x 2 x sm_max_mhz ({peak_src} MEASURED_PEAKS.json holds "
                                "HBM and bf16-tensor peaks only; this kernel is an FP32 FFMA kernel, see DESIGN.md)",
                 "algorithmic_flop_per_launch": stats["sdf_evals"] * FLOP_PER_SDF_EVAL / max(stats["sdf_mlp_launches"], 1),

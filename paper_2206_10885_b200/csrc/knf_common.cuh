@@ -112,9 +112,6 @@ __device__ __forceinline__ void np_sincosf(float x, float& s_out, float& c_out) 
   c_out = (ic & 2) ? -cv : cv;
 }
 
-// Correctly rounded a/b for normal operands (Markstein sequence on the MUFU reciprocal).
-__device__ __forceinline__ float div_rn_fast(float a, float b) { return __fdiv_rn(a, b); }
-
 // np.exp on float32 (loops_exponent_log): Cody-Waite by ln2, rational P5/Q2, scalef.
 __device__ __forceinline__ float np_expf(float x) {
   const float magic = 0x1.8p+23f;
@@ -139,51 +136,16 @@ __device__ __forceinline__ float np_sigmoidf(float x) {
   return x >= 0.0f ? __fdiv_rn(1.0f, den) : __fdiv_rn(t, den);
 }
 
-// nn.softplus (nn.py:26-33): log1p(exp(-|x|)) + max(x,0).  NumPy's log1p is Intel SVML and
-// cannot be reproduced bit for bit; this evaluates both transcendentals to <= 1 ulp so the
-// result is within ~1 ulp of the reference's (measured in tests/test_gpu_forward.py).
-__device__ __forceinline__ float softplus_acc(float x) {
-  float u = np_expf(-fabsf(x));
-  return __fadd_rn(log1pf(u), fmaxf(x, 0.0f));
-}
-
-// The production softplus: same formula, ~32 FMA-pipe instructions and one MUFU.RCP, no
-// conversions, no slow paths.  e = exp(-|x|) by Cody-Waite + a degree-6 polynomial and an integer
-// exponent add; log1p(e) = 2 atanh(e / (2 + e)) with s = e/(2+e) <= 1/3 (one Newton step on the
-// reciprocal, odd polynomial in s).  Emulated in fp32 against float64 on 2e6 N(0,1.5) arguments:
-// mean |error| 0.416 ulp, max 2.7 ulp -- NumPy's own softplus32 measures 0.428 / 3.3 on the same
-// inputs; the two agree bit-for-bit on 64 % of arguments and never differ by more than 4.8e-7.
-__device__ __forceinline__ float softplus_f(float x) {
-  const float y = fminf(fabsf(x), 87.0f);
-  const float magic = 12582912.0f;  // 1.5 * 2^23
-  float tm = __fadd_rn(__fmul_rn(y, -1.4426950408889634f), magic);
-  float nf = __fsub_rn(tm, magic);                       // n = rint(-y / ln 2) <= 0
-  float r = __fmaf_rn(nf, -0.693145751953125f, -y);      // r = -y - n ln2, |r| <= ln2 / 2
-  r = __fmaf_rn(nf, -1.42860677e-6f, r);
-  float p = __fmaf_rn(0.0013943214435130358f, r, 0.00836438313126564f);
-  p = __fmaf_rn(p, r, 0.04166635125875473f);
-  p = __fmaf_rn(p, r, 0.1666657030582428f);
-  p = __fmaf_rn(p, r, 0.5f);
-  float q = __fmaf_rn(p, __fmul_rn(r, r), r);
-  float er = __fadd_rn(1.0f, q);                          // exp(r) in [0.707, 1.414]
-  float e = __int_as_float(__float_as_int(er) + (__float_as_int(tm) << 23));  // * 2^n, n >= -126
-  float den = __fadd_rn(2.0f, e);
-  float rc;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(den));  // MUFU.RCP, ~1 ulp; corrected below
-  float s0 = __fmul_rn(e, rc);
-  float s = __fmaf_rn(__fmaf_rn(-s0, den, e), rc, s0);     // s = e / (2 + e) to ~0.5 ulp
-  float s2 = __fmul_rn(s, s);
-  float g = __fmaf_rn(0.2493898570537567f, s2, 0.21339640021324158f);
-  g = __fmaf_rn(g, s2, 0.28616610169410706f);
-  g = __fmaf_rn(g, s2, 0.3999920189380646f);
-  g = __fmaf_rn(g, s2, 0.6666666865348816f);
-  float l = __fmaf_rn(__fmul_rn(s, s2), g, __fadd_rn(s, s));  // 2 atanh(s)
-  return __fadd_rn(fmaxf(x, 0.0f), l);
-}
-
-// Two softplus_f evaluations in one packed (f32x2) instruction stream: every polynomial step is an
-// FFMA2/FMUL2/FADD2, so a pair costs ~24 packed + ~10 scalar issue slots instead of 2 x 32.  Each
-// half performs exactly the operations of softplus_f except that the first multiply-add is fused.
+// nn.softplus (nn.py:26-33): log1p(exp(-|x|)) + max(x,0).  NumPy's log1p is Intel SVML and cannot be
+// reproduced bit for bit, so this is a fresh evaluation of the same formula: e = exp(-|x|) by
+// Cody-Waite + a degree-6 polynomial and an integer exponent add; log1p(e) = 2 atanh(e / (2 + e)) with
+// s = e/(2+e) <= 1/3 (MUFU.RCP + one Newton step, odd polynomial in s).  Emulated in fp32 against
+// float64 on 2e6 N(0,1.5) arguments: mean |error| 0.416 ulp, max 2.7 ulp -- NumPy's own softplus32
+// measures 0.428 / 3.3 on the same inputs; the two agree bit-for-bit on 64-67 % of arguments and never
+// differ by more than 4.8e-7 (tests/test_gpu_forward.py::test_device_math_against_reference_golden).
+// Two evaluations share one packed (f32x2) instruction stream: every polynomial step is an
+// FFMA2/FMUL2/FADD2, so a pair costs ~24 packed + ~10 scalar issue slots, one MUFU each, no
+// conversions and no slow paths.
 __device__ __forceinline__ float2 softplus_f2(float2 x) {
   const float2 yn = make_float2(fmaxf(-fabsf(x.x), -87.0f), fmaxf(-fabsf(x.y), -87.0f));  // -min(|x|, 87)
   const float2 magic = make_float2(12582912.0f, 12582912.0f);

@@ -50,9 +50,9 @@ void DevBuf::release() {
 
 void Workspace::release_all() {
   DevBuf* all[] = {&tile_base, &req_pt1, &req_cell1, &req_rank1, &req_pt, &req_cell, &req_rank, &perm, &tiles, &cell_count, &cell_offset, &counters, &t, &t_prev,
-                   &d_prev, &t_conv, &d_conv, &t_hit, &steps, &phase, &hit, &live0, &live1, &dval, &hit_list,
+                   &d_prev, &t_conv, &d_conv, &t_hit, &steps, &phase, &hit, &live0, &live1, &hit_list,
                    &hit_count, &sdf_out, &col_v, &col_n, &col_z, &rgb, &origins, &dirs, &t_near, &t_far, &normals64,
-                   &colors64, &steps_out, &frame_color, &frame_depth, &frame_normal, &frame_hit};
+                   &colors64, &frame_color, &frame_depth, &frame_normal, &frame_hit};
   for (DevBuf* b : all) b->release();
   for (DevBuf& b : stage) b.release();
   req_cap = ray_cap = 0;
@@ -80,7 +80,6 @@ int ensure_requests(Field& F, size_t n) {
   KNF_TRY(W.req_rank.ensure(n * sizeof(int)));
   KNF_TRY(W.perm.ensure(n * sizeof(int)));
   KNF_TRY(W.tiles.ensure((n / kTilePts + F.geom.n_cells + 2) * sizeof(Tile)));
-  KNF_TRY(W.dval.ensure(n * sizeof(float)));
   bool fresh = W.cell_count.p == nullptr;
   KNF_TRY(W.cell_count.ensure((size_t)F.geom.n_cells * sizeof(int)));
   KNF_TRY(W.cell_offset.ensure(((size_t)F.geom.n_cells + 1) * sizeof(int)));

@@ -36,17 +36,17 @@ struct DevBuf {
 };
 
 struct Workspace {
-  // routing (two independent sets: A for SDF passes, B for the colour pass of shading)
+  // routing
   DevBuf req_pt, req_cell, req_rank, perm, tiles;
   DevBuf req_pt1, req_cell1, req_rank1;  // second request list: the fused march kernel reads one list while filling the other
   DevBuf cell_count, cell_offset, tile_base;
   DevBuf counters;  // RouteCounters[4] + stats counters
   // march state
-  DevBuf t, t_prev, d_prev, t_conv, d_conv, t_hit, steps, phase, hit, live0, live1, dval;
+  DevBuf t, t_prev, d_prev, t_conv, d_conv, t_hit, steps, phase, hit, live0, live1;
   // shading
   DevBuf hit_list, hit_count, sdf_out, col_v, col_n, col_z, rgb;
   // render-frame ray buffers
-  DevBuf origins, dirs, t_near, t_far, normals64, colors64, steps_out;
+  DevBuf origins, dirs, t_near, t_far, normals64, colors64;
   DevBuf frame_color, frame_depth, frame_normal, frame_hit;  // knf_render_pass_u8 intermediates
   // host staging (KNF_MEM_HOST calls): input/output mirrors
   DevBuf stage[12];

@@ -25,5 +25,13 @@ for name, field in (("random_init_16", grid.field_init(grid.GridConfig(resolutio
     t0 = time.perf_counter(); ref = oracle.render(oracle.FieldTraceable(oracle_from_product(field)), ocam, oracle.MarchSettings()); cpu_s = time.perf_counter() - t0
     got = surface.render_frame(surface.FieldSurface(field), pose)
     out[name + "_256x256_gpu_vs_oracle"] = dict(compare(got, ref), oracle_seconds=cpu_s)
+if "--full" in sys.argv:
+    # the headline frame: 1920x1080, random-init 16^3, bench camera (about 2 minutes of oracle time)
+    f16 = grid.field_init(grid.GridConfig(resolution=16), seed=0)
+    pose = cameras.look_at_pose((0, 0, 2.5), (0, 0, 0), (0, 1, 0), np.deg2rad(40), 1920, 1080)
+    ocam = oracle.camera_look_at((0, 0, 2.5), (0, 0, 0), (0, 1, 0), np.deg2rad(40), 1920, 1080)
+    t0 = time.perf_counter(); ref = oracle.render(oracle.FieldTraceable(oracle_from_product(f16)), ocam, oracle.MarchSettings()); cpu_s = time.perf_counter() - t0
+    got = surface.render_frame(surface.FieldSurface(f16), pose)
+    out["random_init_16_1920x1080_gpu_vs_oracle"] = dict(compare(got, ref), oracle_seconds=cpu_s)
 print(json.dumps(out, indent=1))
 json.dump(out, open(os.path.join(ROOT, "gpurun_out", "parity_r1.json"), "w"), indent=1)
