@@ -31,7 +31,8 @@
 extern "C" {
 #endif
 
-#define KNF_ABI_VERSION 1
+#define KNF_ABI_VERSION 2
+#define KNF_PRECISION_DEFAULT 0 /* KNF_PRECISION_FP32_CHAIN */
 
 enum {
   KNF_OK = 0,
@@ -43,6 +44,20 @@ enum {
 };
 
 enum { KNF_MEM_DEVICE = 0, KNF_MEM_HOST = 1 };
+
+/* Arithmetic of the two hidden contractions of the SDF tile MLP (grid.grid_forward, grid.py:253-265).
+ *   KNF_PRECISION_FP32_CHAIN     k-ordered fp32 FMA chain from zero + rounded bias add on the FP32 pipe:
+ *                                bit-identical to the reference's OpenBLAS sgemm for cells with >= 47 rows.
+ *   KNF_PRECISION_TENSOR_BF16X3  exact 3-way bf16 split of every fp32 operand, six piece products on the
+ *                                tensor cores (mma.sync bf16 -> fp32): closer to the exact dot product than
+ *                                the fp32 chain itself (mean |err| 4e-8 vs 1.2e-7), ~2x faster, but not
+ *                                bit-identical to the chain.
+ * All are deterministic and independent of batch composition.  The colour MLP always uses the chain.
+ *   KNF_PRECISION_TENSOR_FP16X2  two fp16 pieces per operand (22-23 significand bits, second piece scaled by
+ *                                2^11), three piece products: half the tensor work of BF16X3, about as accurate
+ *                                as the fp32 chain itself (mean |err| 1e-7).  Needs |w| < 6e4 in the hidden layers.
+ */
+enum { KNF_PRECISION_FP32_CHAIN = 0, KNF_PRECISION_TENSOR_BF16X3 = 1, KNF_PRECISION_TENSOR_FP16X2 = 2 };
 
 typedef struct knf_field_s* knf_field_t;
 typedef struct knf_scene_s* knf_scene_t;
@@ -119,6 +134,11 @@ int knf_field_stats(knf_field_t f, KnfStats* out);
 int knf_field_stats_reset(knf_field_t f);
 /* Bracket every kernel launch with CUDA events on the call's stream (adds ~1 us of host work per launch). */
 int knf_field_set_profiling(knf_field_t f, int enable);
+/* Select / query the KNF_PRECISION_* mode of the SDF tile kernels (grid.grid_forward's arithmetic).  A new
+ * handle starts in the mode named by the environment variable KNF_PRECISION ("fp32_chain" | "tensor_bf16x3" | "tensor_fp16x2"),
+ * default KNF_PRECISION_DEFAULT. */
+int knf_field_set_precision(knf_field_t f, int mode);
+int knf_field_get_precision(knf_field_t f);
 
 /* ---- routing: grid.py:176-213 ------------------------------------------------------------ */
 /* grid.cell_index_flat (grid.py:182-185) on fp32 points (fp64 arithmetic, bit-exact). */

@@ -121,6 +121,8 @@ _SIGNATURES = {
     "knf_field_stats": [_P, C.POINTER(KnfStats)],
     "knf_field_stats_reset": [_P],
     "knf_field_set_profiling": [_P, _I32],
+    "knf_field_set_precision": [_P, _I32],
+    "knf_field_get_precision": [_P],
     "knf_cell_index": [_P, _P, _I64, _P, _I32, _P],
     "knf_cell_index_f64": [_P, _P, _I64, _P, _I32, _P],
     "knf_route": [_P, _P, _I64, _P, _P, _P, _P, _P, _I32, _P],
@@ -178,7 +180,7 @@ def load():
             fn.restype = C.c_int
         lib.knf_last_error.argtypes = []
         lib.knf_last_error.restype = C.c_char_p
-        if lib.knf_abi_version() != 1:
+        if lib.knf_abi_version() != 2:
             raise KnfError("libknf_b200 ABI version mismatch")
         _lib = lib
     return _lib

@@ -1,4 +1,6 @@
 // knf_api.cu -- the extern "C" surface declared in include/knf_b200.h.
+#include <cuda_fp16.h>
+
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -8,6 +10,7 @@
 
 #include "knf_engine.h"
 #include "knf_mlp.cuh"
+#include "knf_mma.cuh"
 #include "knf_rays.cuh"
 
 using namespace knf;
@@ -139,6 +142,88 @@ void pack_family(int n_cells, const float* const w[3], const float* const b[3], 
   }
 }
 
+// bf16 round-to-nearest-even of an fp32 value, returned as fp32 (the host side of knf_mma.cuh split3)
+static inline float bf16_rn(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  u = (u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+static inline uint16_t bf16_bits(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  return (uint16_t)(u >> 16);
+}
+// w = p[0] + p[1] + p[2] exactly, each piece a bf16 value
+static inline void split_bf16x3(float w, uint16_t p[3]) {
+  const float a = bf16_rn(w), r1 = w - a, b = bf16_rn(r1), r2 = r1 - b;
+  p[0] = bf16_bits(a);
+  p[1] = bf16_bits(b);
+  p[2] = bf16_bits(r2);
+}
+
+// fp16 pieces of the P = 2 split: w ~= h[0] + h[1] / 2^11 (to 2^-24 relative), both fp16 bit patterns
+static inline void split_fp16x2(float w, uint16_t p[2]) {
+  const __half a = __float2half_rn(w);
+  const float r = (w - __half2float(a)) * kHalfPieceScale;
+  const __half b = __float2half_rn(r);
+  std::memcpy(&p[0], &a, 2);
+  std::memcpy(&p[1], &b, 2);
+}
+
+// Pack the SDF family into knf_mma.cuh MmaBlobT<P>: mma.sync.m16n8k16 B fragments of W1 (permuted K) and W2
+// as P pieces each (bf16 x 3 or fp16 x 2), then fp32 biases and the k-major output layer.
+template <int P>
+void pack_sdf_mma(int n_cells, const float* const w[3], const float* const b[3], std::vector<uint32_t>& out) {
+  using Blob = MmaBlobT<P>;
+  out.assign((size_t)n_cells * Blob::words, 0u);
+  for (int c = 0; c < n_cells; c++) {
+    uint32_t* blob = out.data() + (size_t)c * Blob::words;
+    const float* w1 = w[0] + (size_t)c * kHidden * kSdfIn;   // (32, 39)
+    const float* w2 = w[1] + (size_t)c * kHidden * kHidden;  // (32, 32)
+    const float* w3 = w[2] + (size_t)c * kSdfOut * kHidden;  // (9, 32)
+    for (int layer = 0; layer < 2; layer++) {
+      const int kts = layer == 0 ? Blob::kt1 : Blob::kt2;
+      uint32_t* frag = blob + (layer == 0 ? Blob::frag1 : Blob::frag2);
+      for (int kt = 0; kt < kts; kt++)
+        for (int nt = 0; nt < 4; nt++)
+          for (int lane = 0; lane < 32; lane++) {
+            const int g = lane >> 2, t = lane & 3, n = 8 * nt + g;
+            for (int h = 0; h < 2; h++) {
+              uint16_t lo[3], hi[3];
+              float wv[2];
+              for (int e = 0; e < 2; e++) {
+                const int kslot = 2 * t + 8 * h + e;
+                if (layer == 0) {
+                  const int feat = mma_feature_of(kt, kslot);
+                  wv[e] = feat >= 0 ? w1[n * kSdfIn + feat] : 0.0f;
+                } else {
+                  wv[e] = w2[n * kHidden + 16 * kt + kslot];
+                }
+              }
+              if (P == 3) {
+                split_bf16x3(wv[0], lo);
+                split_bf16x3(wv[1], hi);
+              } else {
+                split_fp16x2(wv[0], lo);
+                split_fp16x2(wv[1], hi);
+              }
+              for (int piece = 0; piece < P; piece++)
+                frag[((((kt * 4 + nt) * P + piece) * 32) + lane) * 2 + h] = (uint32_t)lo[piece] | ((uint32_t)hi[piece] << 16);
+            }
+          }
+    }
+    std::memcpy(blob + Blob::b1, b[0] + (size_t)c * kHidden, kHidden * sizeof(float));
+    std::memcpy(blob + Blob::b2, b[1] + (size_t)c * kHidden, kHidden * sizeof(float));
+    float* w3t = reinterpret_cast<float*>(blob + Blob::w3);
+    for (int j = 0; j < kSdfOut; j++)
+      for (int k = 0; k < kHidden; k++) w3t[k * kSdfOutPad + j] = w3[j * kHidden + k];
+    std::memcpy(blob + Blob::b3, b[2] + (size_t)c * kSdfOut, kSdfOut * sizeof(float));
+  }
+}
+
 int validate_desc(const KnfFieldDesc* d) {
   if (!d) return fail(KNF_E_INVALID, "null field description");
   if (d->resolution < 1) return fail(KNF_E_INVALID, "resolution must be >= 1");
@@ -184,6 +269,31 @@ int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
   pack_family<kColIn, kColOut, kColOutPad>(F.geom.n_cells, d->color_w, d->color_b, packed);
   KNF_CUDA(cudaMalloc(&F.col_blobs, packed.size() * sizeof(float)));
   KNF_CUDA(cudaMemcpy(F.col_blobs, packed.data(), packed.size() * sizeof(float), cudaMemcpyHostToDevice));
+  {
+    std::vector<uint32_t> frags;
+    pack_sdf_mma<3>(F.geom.n_cells, d->sdf_w, d->sdf_b, frags);
+    KNF_CUDA(cudaMalloc(&F.sdf_mma_blobs, frags.size() * sizeof(uint32_t)));
+    KNF_CUDA(cudaMemcpy(F.sdf_mma_blobs, frags.data(), frags.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    // fp16 pieces need |w| < 65504 in the two hidden layers (true of any trained or random-init field)
+    F.fp16_ok = true;
+    const size_t n1 = (size_t)F.geom.n_cells * kHidden * kSdfIn, n2 = (size_t)F.geom.n_cells * kHidden * kHidden;
+    for (size_t i = 0; i < n1 && F.fp16_ok; i++) F.fp16_ok = std::fabs(d->sdf_w[0][i]) < 60000.0f;
+    for (size_t i = 0; i < n2 && F.fp16_ok; i++) F.fp16_ok = std::fabs(d->sdf_w[1][i]) < 60000.0f;
+    if (F.fp16_ok) {
+      pack_sdf_mma<2>(F.geom.n_cells, d->sdf_w, d->sdf_b, frags);
+      KNF_CUDA(cudaMalloc(&F.sdf_mmah_blobs, frags.size() * sizeof(uint32_t)));
+      KNF_CUDA(cudaMemcpy(F.sdf_mmah_blobs, frags.data(), frags.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    }
+  }
+  F.precision = KNF_PRECISION_DEFAULT;
+  if (const char* env = std::getenv("KNF_PRECISION")) {
+    const std::string v(env);
+    if (v == "fp32_chain" || v == "0") F.precision = KNF_PRECISION_FP32_CHAIN;
+    else if (v == "tensor_bf16x3" || v == "1") F.precision = KNF_PRECISION_TENSOR_BF16X3;
+    else if (v == "tensor_fp16x2" || v == "2") F.precision = KNF_PRECISION_TENSOR_FP16X2;
+    else return fail(KNF_E_INVALID, "KNF_PRECISION must be fp32_chain, tensor_bf16x3 or tensor_fp16x2");
+  }
+  if (F.precision == KNF_PRECISION_TENSOR_FP16X2 && !F.fp16_ok) F.precision = KNF_PRECISION_TENSOR_BF16X3;
   *out = h.release();
   return 0;
 }
@@ -232,7 +342,7 @@ __global__ void fourier_encode_kernel(const float* __restrict__ x, long long n, 
 __global__ void activation_kernel(const float* __restrict__ x, long long n, int which, float* __restrict__ out) {
   long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
-    out[i] = which == 0 ? softplus_f2(make_float2(x[i], x[i])).x : np_sigmoidf(x[i]);
+    out[i] = which == 0 ? (KNF_SOFTPLUS_EXACT ? softplus_np_f2(make_float2(x[i], x[i])).x : softplus_f2(make_float2(x[i], x[i])).x) : np_sigmoidf(x[i]);
 }
 
 __global__ void pass_u8_kernel(int pass, long long n, const float* __restrict__ color, const float* __restrict__ depth,
@@ -449,6 +559,8 @@ int knf_field_destroy(knf_field_t f) {
     if (f->f.host_poll) cudaFreeHost(f->f.host_poll);
     if (f->f.sdf_blobs) cudaFree(f->f.sdf_blobs);
     if (f->f.col_blobs) cudaFree(f->f.col_blobs);
+    if (f->f.sdf_mma_blobs) cudaFree(f->f.sdf_mma_blobs);
+    if (f->f.sdf_mmah_blobs) cudaFree(f->f.sdf_mmah_blobs);
   }
   delete f;
   return 0;
@@ -498,6 +610,22 @@ int knf_field_set_profiling(knf_field_t f, int enable) {
   std::lock_guard<std::mutex> lk(f->f.mu);
   f->f.profiling = enable != 0;
   return 0;
+}
+
+int knf_field_set_precision(knf_field_t f, int mode) {
+  KNF_TRY(check_field(f));
+  if (mode != KNF_PRECISION_FP32_CHAIN && mode != KNF_PRECISION_TENSOR_BF16X3 && mode != KNF_PRECISION_TENSOR_FP16X2)
+    return fail(KNF_E_INVALID, "unknown KNF_PRECISION_* mode");
+  if (mode == KNF_PRECISION_TENSOR_FP16X2 && !f->f.fp16_ok)
+    return fail(KNF_E_UNSUPPORTED, "KNF_PRECISION_TENSOR_FP16X2 needs hidden-layer weights below 6e4 in magnitude");
+  std::lock_guard<std::mutex> lk(f->f.mu);
+  f->f.precision = mode;
+  return 0;
+}
+
+int knf_field_get_precision(knf_field_t f) {
+  KNF_TRY(check_field(f));
+  return f->f.precision;
 }
 
 // ---- routing ---------------------------------------------------------------------------------------

@@ -178,6 +178,123 @@ __device__ __forceinline__ float2 softplus_f2(float2 x) {
   return __fadd2_rn(make_float2(fmaxf(x.x, 0.0f), fmaxf(x.y, 0.0f)), l);
 }
 
+// N independent softplus_f2 evaluations advanced in lock step (same arithmetic, same bits): written stage by stage
+// so that every packed instruction has N-1 independent neighbours and a lone warp can fill the FMA pipe.
+template <int N>
+__device__ __forceinline__ void softplus_f2xN(float2 (&x)[N]) {
+#define KNF_EACH _Pragma("unroll") for (int i = 0; i < N; i++)
+  const float2 magic = make_float2(12582912.0f, 12582912.0f);
+  float2 yn[N], tm[N], r[N], p[N], e[N], nden[N], s[N], s2[N], g[N];
+  KNF_EACH yn[i] = make_float2(fmaxf(-fabsf(x[i].x), -87.0f), fmaxf(-fabsf(x[i].y), -87.0f));
+  KNF_EACH tm[i] = __ffma2_rn(yn[i], make_float2(1.4426950408889634f, 1.4426950408889634f), magic);
+  KNF_EACH r[i] = __fadd2_rn(tm[i], make_float2(-12582912.0f, -12582912.0f));
+  KNF_EACH { const float2 nf = r[i]; r[i] = __ffma2_rn(nf, make_float2(-0.693145751953125f, -0.693145751953125f), yn[i]);
+             r[i] = __ffma2_rn(nf, make_float2(-1.42860677e-6f, -1.42860677e-6f), r[i]); }
+  KNF_EACH p[i] = __ffma2_rn(make_float2(0.0013943214435130358f, 0.0013943214435130358f), r[i],
+                             make_float2(0.00836438313126564f, 0.00836438313126564f));
+  KNF_EACH p[i] = __ffma2_rn(p[i], r[i], make_float2(0.04166635125875473f, 0.04166635125875473f));
+  KNF_EACH p[i] = __ffma2_rn(p[i], r[i], make_float2(0.1666657030582428f, 0.1666657030582428f));
+  KNF_EACH p[i] = __ffma2_rn(p[i], r[i], make_float2(0.5f, 0.5f));
+  KNF_EACH p[i] = __ffma2_rn(p[i], __fmul2_rn(r[i], r[i]), r[i]);
+  KNF_EACH p[i] = __fadd2_rn(make_float2(1.0f, 1.0f), p[i]);
+  KNF_EACH e[i] = make_float2(__int_as_float(__float_as_int(p[i].x) + (__float_as_int(tm[i].x) << 23)),
+                              __int_as_float(__float_as_int(p[i].y) + (__float_as_int(tm[i].y) << 23)));
+  KNF_EACH nden[i] = __ffma2_rn(e[i], make_float2(-1.0f, -1.0f), make_float2(-2.0f, -2.0f));
+  KNF_EACH { float2 rc;
+             asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc.x) : "f"(-nden[i].x));
+             asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc.y) : "f"(-nden[i].y));
+             const float2 s0 = __fmul2_rn(e[i], rc);
+             s[i] = __ffma2_rn(__ffma2_rn(s0, nden[i], e[i]), rc, s0); }
+  KNF_EACH s2[i] = __fmul2_rn(s[i], s[i]);
+  KNF_EACH g[i] = __ffma2_rn(make_float2(0.2493898570537567f, 0.2493898570537567f), s2[i],
+                             make_float2(0.21339640021324158f, 0.21339640021324158f));
+  KNF_EACH g[i] = __ffma2_rn(g[i], s2[i], make_float2(0.28616610169410706f, 0.28616610169410706f));
+  KNF_EACH g[i] = __ffma2_rn(g[i], s2[i], make_float2(0.3999920189380646f, 0.3999920189380646f));
+  KNF_EACH g[i] = __ffma2_rn(g[i], s2[i], make_float2(0.6666666865348816f, 0.6666666865348816f));
+  KNF_EACH { const float2 l = __ffma2_rn(__fmul2_rn(s[i], s2[i]), g[i], __fadd2_rn(s[i], s[i]));
+             x[i] = __fadd2_rn(make_float2(fmaxf(x[i].x, 0.0f), fmaxf(x[i].y, 0.0f)), l); }
+#undef KNF_EACH
+}
+
+// nn.softplus (nn.py:26-33) BIT FOR BIT as NumPy evaluates it on an AVX-512 host: np.exp (np_expf above: Cody-Waite,
+// P5/Q2, IEEE division, scalef) followed by np.log1p, which NumPy dispatches to Intel SVML's __svml_log1pf16
+// (numpy/_core/src/umath/svml, linked into _multiarray_umath): 1 + e as a two-piece sum (A, Al), reduction of A
+// to [2/3, 4/3) by integer exponent arithmetic, a degree-8 polynomial in R = (mantissa - 1) + Al * 2^-N, then
+// N * ln2 + poly.  The constants below are the routine's own data table (__svml_slog1p_data_internal), read from
+// the installed numpy 2.3.5 binary; the operation order was restated from its main path and checked against
+// np.log1p / np.exp / the composed softplus on 7e6 + 11e6 float32 arguments in the build container: 0 mismatches
+// (tests/test_oracle_golden.py::test_softplus_restatement_bit_exact pins the same restatement in C).
+// The IEEE division is a Markstein sequence (MUFU.RCP, one Newton step, residual correction): correctly rounded
+// for the operand range here (num in [0.7, 1.42], den in [0.9, 1.1]).  |x| is clamped at 87 (e stays normal).
+// N evaluations advance in lock step; every FMA-pipe step is a packed f32x2 instruction.
+template <int N>
+__device__ __forceinline__ void softplus_np_f2xN(float2 (&x)[N]) {
+#define KNF_EACH _Pragma("unroll") for (int i = 0; i < N; i++)
+#define KNF_S2(v) make_float2(v, v)
+  float2 yn[N], tm[N], r[N], num[N], den[N], e[N];
+  KNF_EACH yn[i] = make_float2(fmaxf(-fabsf(x[i].x), -87.0f), fmaxf(-fabsf(x[i].y), -87.0f));
+  KNF_EACH tm[i] = __fadd2_rn(__fmul2_rn(yn[i], KNF_S2(1.442695040888963407359924681f)), KNF_S2(12582912.0f));
+  KNF_EACH { const float2 nf = __fadd2_rn(tm[i], KNF_S2(-12582912.0f));
+             r[i] = __ffma2_rn(nf, KNF_S2(-6.93145752e-1f), yn[i]);
+             r[i] = __ffma2_rn(nf, KNF_S2(-1.42860677e-6f), r[i]); }
+  KNF_EACH num[i] = __ffma2_rn(KNF_S2(5.082762527590693718096e-04f), r[i], KNF_S2(6.757896990527504603057e-03f));
+  KNF_EACH den[i] = __ffma2_rn(KNF_S2(2.159509375685829852307e-02f), r[i], KNF_S2(-2.742335390411667452936e-01f));
+  KNF_EACH num[i] = __ffma2_rn(num[i], r[i], KNF_S2(5.114512081637298353406e-02f));
+  KNF_EACH den[i] = __ffma2_rn(den[i], r[i], KNF_S2(1.0f));
+  KNF_EACH num[i] = __ffma2_rn(num[i], r[i], KNF_S2(2.473615434895520810817e-01f));
+  KNF_EACH num[i] = __ffma2_rn(num[i], r[i], KNF_S2(7.257664613233124478488e-01f));
+  KNF_EACH num[i] = __ffma2_rn(num[i], r[i], KNF_S2(9.999999999980870924916e-01f));
+  KNF_EACH { float2 rc;
+             asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc.x) : "f"(den[i].x));
+             asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc.y) : "f"(den[i].y));
+             const float2 nd = make_float2(-den[i].x, -den[i].y);
+             rc = __ffma2_rn(rc, __ffma2_rn(nd, rc, KNF_S2(1.0f)), rc);
+             float2 q = __fmul2_rn(num[i], rc);
+             q = __ffma2_rn(__ffma2_rn(nd, q, num[i]), rc, q);
+             e[i] = make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(tm[i].x) << 23)),
+                                __int_as_float(__float_as_int(q.y) + (__float_as_int(tm[i].y) << 23))); }
+  // ---- log1p(e), e in (0, 1]: xh = 1, xl = e ---------------------------------------------------------------
+  float2 A[N], Al[N], R[N], fN[N], p[N];
+  KNF_EACH A[i] = __fadd2_rn(KNF_S2(1.0f), e[i]);
+  KNF_EACH Al[i] = __fadd2_rn(__fadd2_rn(KNF_S2(1.0f), make_float2(-A[i].x, -A[i].y)), e[i]);
+  KNF_EACH {
+    const int ia0 = __float_as_int(A[i].x) - 0x3f2aaaab, ia1 = __float_as_int(A[i].y) - 0x3f2aaaab;
+    const int n0 = ia0 & 0xff800000, n1 = ia1 & 0xff800000;  // N << 23, N in {0, 1}
+    fN[i] = make_float2(n0 ? 1.0f : 0.0f, n1 ? 1.0f : 0.0f);
+    const float2 sc = make_float2(__int_as_float(0x3f800000 - n0), __int_as_float(0x3f800000 - n1));
+    const float2 r0 = make_float2(__int_as_float((ia0 & 0x007fffff) + 0x3f2aaaab), __int_as_float((ia1 & 0x007fffff) + 0x3f2aaaab));
+    R[i] = __fadd2_rn(__fadd2_rn(r0, KNF_S2(-1.0f)), __fmul2_rn(Al[i], sc));
+  }
+  KNF_EACH p[i] = __ffma2_rn(R[i], KNF_S2(0x1.1b09dap-3f), KNF_S2(-0x1.35b3c6p-3f));
+  KNF_EACH p[i] = __ffma2_rn(p[i], R[i], KNF_S2(0x1.1f9624p-3f));
+  KNF_EACH p[i] = __ffma2_rn(p[i], R[i], KNF_S2(-0x1.515a6ep-3f));
+  KNF_EACH p[i] = __ffma2_rn(p[i], R[i], KNF_S2(0x1.99c32p-3f));
+  KNF_EACH p[i] = __ffma2_rn(p[i], R[i], KNF_S2(-0x1.000b1cp-2f));
+  KNF_EACH p[i] = __ffma2_rn(p[i], R[i], KNF_S2(0x1.555528p-2f));
+  KNF_EACH p[i] = __ffma2_rn(p[i], R[i], KNF_S2(-0.5f));
+  KNF_EACH p[i] = __ffma2_rn(__fmul2_rn(p[i], R[i]), R[i], R[i]);
+  KNF_EACH { const float2 l = __ffma2_rn(fN[i], KNF_S2(0x1.62e43p-1f), p[i]);
+             x[i] = __fadd2_rn(l, make_float2(fmaxf(x[i].x, 0.0f), fmaxf(x[i].y, 0.0f))); }
+#undef KNF_S2
+#undef KNF_EACH
+}
+__device__ __forceinline__ float2 softplus_np_f2(float2 x) {
+  float2 a[1] = {x};
+  softplus_np_f2xN<1>(a);
+  return a[0];
+}
+
+// Which softplus the tile kernels run: 1 = softplus_np (NumPy bit-exact, 34 packed FMA-pipe steps per pair),
+// 0 = softplus_f2 (same accuracy against float64, 24 steps, agrees with NumPy on 64 % of arguments).
+#ifndef KNF_SOFTPLUS_EXACT
+#define KNF_SOFTPLUS_EXACT 1
+#endif
+template <int N>
+__device__ __forceinline__ void softplus_tile(float2 (&x)[N]) {
+  if (KNF_SOFTPLUS_EXACT) softplus_np_f2xN<N>(x);
+  else softplus_f2xN<N>(x);
+}
+
 // grid._cell_triples (grid.py:176-179) for one coordinate: fp64 arithmetic on the fp32 point.
 __device__ __forceinline__ int cell_coord(double p, double lo, double hi, int n) {
   double t = (p - lo) / (hi - lo) * (double)n;

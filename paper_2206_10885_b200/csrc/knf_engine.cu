@@ -9,6 +9,7 @@
 
 #include "knf_march.cuh"
 #include "knf_mlp.cuh"
+#include "knf_mma.cuh"
 #include "knf_rays.cuh"
 
 namespace knf {
@@ -150,6 +151,10 @@ int begin_call(Field& F, cudaStream_t st) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ColKernelSmem)));
     KNF_CUDA(cudaFuncSetAttribute(march_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sizeof(SdfKernelSmem)));
+    KNF_CUDA(cudaFuncSetAttribute(march_mma_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<3>)));
+    KNF_CUDA(cudaFuncSetAttribute(sdf_mma_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<3>)));
+    KNF_CUDA(cudaFuncSetAttribute(march_mma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<2>)));
+    KNF_CUDA(cudaFuncSetAttribute(sdf_mma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<2>)));
     if (!F.host_poll) KNF_CUDA(cudaMallocHost(&F.host_poll, 64));
     F.smem_configured = true;
   }
@@ -216,9 +221,9 @@ int launch_scan_scatter(Field& F, const RouteBuffers& R, size_t n_upper, cudaStr
   return 0;
 }
 
-static inline int mlp_grid(const Field& F, size_t n_upper) {
+static inline int mlp_grid(const Field& F, size_t n_upper, int ctas_per_sm = kWarpCtasPerSm) {
   size_t tiles_upper = n_upper / kTilePts + std::min<size_t>(n_upper, (size_t)F.geom.n_cells) + 1;
-  return (int)std::max<size_t>(1, std::min<size_t>(tiles_upper, 148 * kWarpCtasPerSm));
+  return (int)std::max<size_t>(1, std::min<size_t>(tiles_upper, (size_t)148 * ctas_per_sm));
 }
 
 int launch_sdf_mlp(Field& F, const RouteBuffers& R, size_t n_upper, float* out_first, float* out_full, cudaStream_t st) {
@@ -231,8 +236,16 @@ int launch_sdf_mlp(Field& F, const RouteBuffers& R, size_t n_upper, float* out_f
   P.out_first = out_first;
   P.out_full = out_full;
   ProfScope prof(F, st, SPAN_SDF_MLP);
-  mlp_warp_kernel<kSdfIn, kSdfOut, kSdfOutPad, ACT_SOFTPLUS, false>
-      <<<mlp_grid(F, n_upper), 32, sizeof(SdfKernelSmem), st>>>(P);
+  if (F.precision == KNF_PRECISION_TENSOR_BF16X3) {
+    P.blobs = reinterpret_cast<const float*>(F.sdf_mma_blobs);
+    sdf_mma_kernel<3><<<mlp_grid(F, n_upper, kMmaCtasPerSm), 32, sizeof(MmaSmemT<3>), st>>>(P);
+  } else if (F.precision == KNF_PRECISION_TENSOR_FP16X2) {
+    P.blobs = reinterpret_cast<const float*>(F.sdf_mmah_blobs);
+    sdf_mma_kernel<2><<<mlp_grid(F, n_upper, kMmaCtasPerSm), 32, sizeof(MmaSmemT<2>), st>>>(P);
+  } else {
+    mlp_warp_kernel<kSdfIn, kSdfOut, kSdfOutPad, ACT_SOFTPLUS, false>
+        <<<mlp_grid(F, n_upper), 32, sizeof(SdfKernelSmem), st>>>(P);
+  }
   F.stats.kernel_launches += 1;
   KNF_CUDA(cudaGetLastError());
   return 0;
@@ -339,7 +352,15 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     A.max_inner = F.march_max_inner;
     {
       ProfScope prof(F, st, SPAN_SDF_MLP);
-      march_warp_kernel<<<mlp_grid(F, (size_t)n), 32, sizeof(SdfKernelSmem), st>>>(A);
+      if (F.precision == KNF_PRECISION_TENSOR_BF16X3) {
+        A.P.blobs = reinterpret_cast<const float*>(F.sdf_mma_blobs);
+        march_mma_kernel<3><<<mlp_grid(F, (size_t)n, kMmaCtasPerSm), 32, sizeof(MmaSmemT<3>), st>>>(A);
+      } else if (F.precision == KNF_PRECISION_TENSOR_FP16X2) {
+        A.P.blobs = reinterpret_cast<const float*>(F.sdf_mmah_blobs);
+        march_mma_kernel<2><<<mlp_grid(F, (size_t)n, kMmaCtasPerSm), 32, sizeof(MmaSmemT<2>), st>>>(A);
+      } else {
+        march_warp_kernel<<<mlp_grid(F, (size_t)n), 32, sizeof(SdfKernelSmem), st>>>(A);
+      }
     }
     F.stats.kernel_launches += 1;
     F.stats.wavefronts += 1;

@@ -61,6 +61,10 @@ struct Field {
   int sdf_freqs = kSdfFreqs, dir_freqs = kDirFreqs, feature_dim = kFeat;
   float* sdf_blobs = nullptr;
   float* col_blobs = nullptr;
+  uint32_t* sdf_mma_blobs = nullptr;   // knf_mma.cuh MmaBlobT<3> per cell (bf16 x 3 B fragments)
+  uint32_t* sdf_mmah_blobs = nullptr;  // MmaBlobT<2> per cell (fp16 x 2 B fragments); null when a weight exceeds the fp16 range
+  bool fp16_ok = false;
+  int precision = 0;                  // KNF_PRECISION_*: which SDF tile kernels run
   Workspace ws;
   std::mutex mu;
   KnfStats stats{};

@@ -14,6 +14,7 @@
 #pragma once
 
 #include "knf_mlp.cuh"
+#include "knf_mma.cuh"
 #include "knf_rays.cuh"
 
 namespace knf {
@@ -147,6 +148,139 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(M
   if (lane == 0 && evals && A.eval_counter) {
     atomicAdd(A.eval_counter, evals);
     atomicAdd(A.eval_counter + 2, passes * kWarpPts);  // lane slots spent (tile-fill statistic)
+  }
+}
+
+// ---- the same kernel with the hidden layers on the tensor cores (knf_mma.cuh) ------------------------------
+// Lane (g, t) owns tile points 16 t + g and 16 t + g + 8 (rows g, g + 8 of m-tile t), so the distance the quad
+// butterfly leaves in every lane of quad g is picked up by the lane whose t equals the m-tile index.
+template <int PC>
+static __global__ void __launch_bounds__(32, kMmaCtasPerSm) march_mma_kernel(MarchTileArgs A) {
+  using Blob = MmaBlobT<PC>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MmaSmemT<PC>& S = *reinterpret_cast<MmaSmemT<PC>*>(smem_raw);
+  const int lane = threadIdx.x, g = lane >> 2, t = lane & 3;
+  if (lane == 0) {
+    mbar_init(&S.bar, 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  const MlpParams& P = A.P;
+  const int n_tiles = P.ctr->n_tiles;
+  const uint32_t* blobs = reinterpret_cast<const uint32_t*>(P.blobs);
+  uint32_t parity = 0;
+  unsigned long long evals = 0, passes = 0;
+
+  for (;;) {
+    const int tix = next_tile(P.ctr, lane);
+    if (tix >= n_tiles) break;
+    const Tile tile = P.tiles[tix];
+    fetch_mma_weights<PC>(S, blobs, tile.cell, lane);
+
+    bool active[2];
+    int ray[2] = {0, 0};
+    int pidx[2];
+    float px[2], py[2], pz[2];
+    RayRegs rr[2];
+#pragma unroll
+    for (int q = 0; q < 2; q++) {
+      pidx[q] = 16 * t + g + 8 * q;
+      active[q] = pidx[q] < tile.count;
+      px[q] = py[q] = pz[q] = 0.f;
+      if (active[q]) {
+        int slot = P.perm[tile.start + pidx[q]];
+        ray[q] = A.live_in[slot];
+        float4 pt = P.req_pt[slot];
+        px[q] = pt.x; py[q] = pt.y; pz[q] = pt.z;
+        ray_load(rr[q], A.M, ray[q]);
+      }
+    }
+    float in_lo[3], in_hi[3];
+    {
+      const int N = A.G.resolution;
+      const int ci[3] = {tile.cell / (N * N), (tile.cell / N) % N, tile.cell % N};
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        const double ext = A.G.hi[a] - A.G.lo[a];
+        in_lo[a] = (float)(A.G.lo[a] + ext * ((double)ci[a] / N) + 1e-6 * ext);
+        in_hi[a] = (float)(A.G.lo[a] + ext * ((double)(ci[a] + 1) / N) - 1e-6 * ext);
+      }
+    }
+    int n_active = tile.count;
+    const float* W3t = reinterpret_cast<const float*>(S.w + Blob::w3);
+
+    for (int inner = 0;; inner++) {
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        S.pts[0][pidx[q]] = px[q];
+        S.pts[1][pidx[q]] = py[q];
+        S.pts[2][pidx[q]] = pz[q];
+      }
+      // m-tiles that hold no active ray are skipped (warp-uniform): lanes with t == m own m-tile m
+      const unsigned act_mask = __ballot_sync(0xffffffffu, active[0] || active[1]);
+      __syncwarp();
+      if (inner == 0) {
+        mbar_wait(&S.bar, parity);
+        parity ^= 1;
+      }
+      const float b3 = reinterpret_cast<const float*>(S.w + Blob::b3)[0];
+      float2 dist = make_float2(0.f, 0.f);
+#pragma unroll 1
+      for (int m = 0; m < 4; m++) {
+        if ((act_mask & (0x11111111u << m)) == 0) continue;
+        float h2[4][4];
+        mma_hidden<PC>(S, m, lane, h2);
+        const float2 d = mma_output(h2, W3t, b3, t, 0);
+        if (m == t) dist = d;
+      }
+      evals += (lane == 0) ? (unsigned long long)n_active : 0ull;
+      passes += 1;
+
+      bool want[2], stay[2];
+      int cell[2];
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        want[q] = false;
+        cell[q] = -1;
+        if (active[q]) {
+          double t_next = 0.0;
+          want[q] = ray_step(rr[q], A.M, ray[q], q ? dist.y : dist.x, t_next);
+          if (want[q]) {
+            px[q] = __double2float_rn(rr[q].o[0] + t_next * rr[q].d[0]);
+            py[q] = __double2float_rn(rr[q].o[1] + t_next * rr[q].d[1]);
+            pz[q] = __double2float_rn(rr[q].o[2] + t_next * rr[q].d[2]);
+            const bool well_inside = px[q] > in_lo[0] && px[q] < in_hi[0] && py[q] > in_lo[1] && py[q] < in_hi[1] &&
+                                     pz[q] > in_lo[2] && pz[q] < in_hi[2];
+            cell[q] = well_inside ? tile.cell : cell_of(px[q], py[q], pz[q], A.G);
+          }
+        }
+        stay[q] = want[q] && cell[q] == tile.cell;
+      }
+      const int n_stay = __popc(__ballot_sync(0xffffffffu, stay[0])) + __popc(__ballot_sync(0xffffffffu, stay[1]));
+      const bool cont = n_stay > 0 && 2 * n_stay >= tile.count && inner + 1 < A.max_inner;
+#pragma unroll
+      for (int q = 0; q < 2; q++) {
+        const bool emit = want[q] && !(cont && stay[q]);
+        if (__any_sync(0xffffffffu, emit)) {
+          const int slot = warp_append(&A.next.ctr->n_requests, emit);
+          if (emit) {
+            A.live_out[slot] = ray[q];
+            ray_store(rr[q], A.M, ray[q]);
+          }
+          route_emit_cell(A.next, emit, slot, px[q], py[q], pz[q], cell[q]);
+        }
+        active[q] = cont && stay[q];
+        if (!active[q]) px[q] = py[q] = pz[q] = 0.f;
+      }
+      if (!cont) break;
+      n_active = n_stay;
+      __syncwarp();
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && evals && A.eval_counter) {
+    atomicAdd(A.eval_counter, evals);
+    atomicAdd(A.eval_counter + 2, passes * kWarpPts);
   }
 }
 

@@ -146,10 +146,14 @@ __device__ __forceinline__ void store_hidden(float2 (&acc)[4][8], const float* _
 #endif
 constexpr int kSoftplusUnroll = KNF_SP_UNROLL;
 __device__ __forceinline__ void softplus_panel(float* __restrict__ panel, int lane) {
-#pragma unroll kSoftplusUnroll
-  for (int j = 0; j < kHidden; j++) {
-    float2* cell = reinterpret_cast<float2*>(panel + j * kPanelLd + 2 * lane);
-    *cell = softplus_f2(*cell);
+#pragma unroll 1
+  for (int j = 0; j < kHidden; j += kSoftplusUnroll) {
+    float2 v[kSoftplusUnroll];
+#pragma unroll
+    for (int u = 0; u < kSoftplusUnroll; u++) v[u] = *reinterpret_cast<float2*>(panel + (j + u) * kPanelLd + 2 * lane);
+    softplus_tile<kSoftplusUnroll>(v);
+#pragma unroll
+    for (int u = 0; u < kSoftplusUnroll; u++) *reinterpret_cast<float2*>(panel + (j + u) * kPanelLd + 2 * lane) = v[u];
   }
 }
 

@@ -218,6 +218,19 @@ class DeviceField:
     def set_profiling(self, enable: bool):
         N.check(N.load().knf_field_set_profiling(self.handle, int(bool(enable))))
 
+    PRECISIONS = {"fp32_chain": 0, "tensor_bf16x3": 1, "tensor_fp16x2": 2}
+
+    def set_precision(self, mode):
+        """Arithmetic of the SDF hidden layers: "fp32_chain" (the reference's k-ordered FMA chain, FP32 pipe) or
+        "tensor_bf16x3" (exact 3-way bf16 split on the tensor cores; include/knf_b200.h KNF_PRECISION_*)."""
+        code = self.PRECISIONS[mode] if isinstance(mode, str) else int(mode)
+        N.check(N.load().knf_field_set_precision(self.handle, code))
+
+    def get_precision(self) -> str:
+        code = N.load().knf_field_get_precision(self.handle)
+        N.check(min(code, 0))
+        return {v: k for k, v in self.PRECISIONS.items()}[code]
+
 
 def _default_device() -> int:
     try:

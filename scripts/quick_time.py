@@ -1,0 +1,25 @@
+"""1080p random-init frame time for the precision modes given on the command line (default both)."""
+import os, sys, time
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np, torch
+from paper_2206_10885_b200 import grid, surface
+from bench import orbit_view
+modes = sys.argv[1:] or ["fp32_chain", "tensor_bf16x3", "tensor_fp16x2"]
+W, H = 1920, 1080
+fs0 = surface.FieldSurface(grid.field_init(grid.GridConfig(resolution=16), seed=0))
+dev = torch.device("cuda", 0)
+bufs = (torch.empty((H, W, 3), dtype=torch.float32, device=dev), torch.empty((H, W), dtype=torch.float32, device=dev),
+        torch.empty((H, W, 3), dtype=torch.float32, device=dev), torch.empty((H, W), dtype=torch.uint8, device=dev))
+st = surface.RenderSettings()
+def loop(n):
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    for s in range(n):
+        surface.render_rows(fs0, orbit_view(s, W, H), st, (1.0, 1.0, 1.0), 1, 0, H, out=bufs, device_out=True)
+    torch.cuda.synchronize()
+    return (time.perf_counter() - t0) * 1e3 / n
+loop(40)
+for mode in modes:
+    fs0.dev.set_precision(mode)
+    loop(3)
+    print("1080p", mode, "%.2f ms/frame" % loop(20), "hits", int(bufs[3].sum().item()), flush=True)

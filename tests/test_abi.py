@@ -41,7 +41,7 @@ def test_header_symbols_all_exported(lib):
 
 
 def test_abi_version(lib):
-    assert lib.knf_abi_version() == 1
+    assert lib.knf_abi_version() == 2
 
 
 def test_struct_sizes_match_c_layout():
