@@ -112,6 +112,12 @@ typedef struct {
   double other_ms;
   int64_t march_lane_slots; /* 64 x tile passes of the fused march kernel: sdf march evals / this = tile fill */
   int64_t march_routed_requests; /* march evaluations that went through a global routing pass (the rest stepped in place) */
+  /* decision filter of the exact march (knf_field_set_filter): tensor-core predicate evaluations, how many of them
+   * could not be decided and were re-evaluated exactly, and (while profiling) the filter launches' CUDA-event time */
+  int64_t filter_evals;
+  int64_t filter_deferred;
+  int64_t filter_launches;
+  double filter_ms;
 } KnfStats;
 
 int knf_abi_version(void);
@@ -139,6 +145,18 @@ int knf_field_set_profiling(knf_field_t f, int enable);
  * default KNF_PRECISION_DEFAULT. */
 int knf_field_set_precision(knf_field_t f, int mode);
 int knf_field_get_precision(knf_field_t f);
+/* Decision filter of surface.march_rays in KNF_PRECISION_FP32_CHAIN mode (surface.py:185-223).  A ray inside a
+ * negative region advances by the fixed step scale * eps / 2 and the reference consults the distance there only
+ * as the predicate d < -eps (plus, once, as d_prev of the secant step).  With the filter on, those predicates are
+ * answered by a tensor-core evaluation with a proven per-cell error bound; every sample it cannot decide, and
+ * every value the reference uses as a number, is evaluated by the exact fp32 chain kernel.  Results are
+ * bit-identical to filter off.  KNF_FILTER_AUTO probes the first wavefront and switches the filter off when fewer
+ * than 1/8 of the live rays are in a negative region (always the case on a real surface).  Environment variable
+ * KNF_FILTER ("off" | "on" | "auto") sets the initial mode of new handles; default auto. */
+enum { KNF_FILTER_OFF = 0, KNF_FILTER_ON = 1, KNF_FILTER_AUTO = 2 };
+int knf_field_set_filter(knf_field_t f, int mode);
+/* largest per-cell bound |filter distance - exact distance| the field was packed with (for reports) */
+double knf_field_filter_delta(knf_field_t f);
 
 /* ---- routing: grid.py:176-213 ------------------------------------------------------------ */
 /* grid.cell_index_flat (grid.py:182-185) on fp32 points (fp64 arithmetic, bit-exact). */

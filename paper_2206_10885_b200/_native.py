@@ -88,6 +88,10 @@ class KnfStats(C.Structure):
         ("other_ms", C.c_double),
         ("march_lane_slots", C.c_int64),
         ("march_routed_requests", C.c_int64),
+        ("filter_evals", C.c_int64),
+        ("filter_deferred", C.c_int64),
+        ("filter_launches", C.c_int64),
+        ("filter_ms", C.c_double),
     ]
 
 
@@ -123,6 +127,8 @@ _SIGNATURES = {
     "knf_field_set_profiling": [_P, _I32],
     "knf_field_set_precision": [_P, _I32],
     "knf_field_get_precision": [_P],
+    "knf_field_set_filter": [_P, _I32],
+    "knf_field_filter_delta": [_P],
     "knf_cell_index": [_P, _P, _I64, _P, _I32, _P],
     "knf_cell_index_f64": [_P, _P, _I64, _P, _I32, _P],
     "knf_route": [_P, _P, _I64, _P, _P, _P, _P, _P, _I32, _P],
@@ -178,6 +184,7 @@ def load():
             fn = getattr(lib, name)
             fn.argtypes = args
             fn.restype = C.c_int
+        lib.knf_field_filter_delta.restype = C.c_double
         lib.knf_last_error.argtypes = []
         lib.knf_last_error.restype = C.c_char_p
         if lib.knf_abi_version() != 2:

@@ -175,8 +175,50 @@ static inline void split_fp16x2(float w, uint16_t p[2]) {
 
 // Pack the SDF family into knf_mma.cuh MmaBlobT<P>: mma.sync.m16n8k16 B fragments of W1 (permuted K) and W2
 // as P pieces each (bf16 x 3 or fp16 x 2), then fp32 biases and the k-major output layer.
+// Proven bound on |distance from the tensor-core tile kernel with the fast softplus - distance from the exact
+// fp32 chain kernel| for one cell, by forward error analysis over the cell's weights (all sums of magnitudes):
+//   * operand representation: P = 3 pieces are exact; P = 2 leaves |x~ - x| <= 2^-22 |x| per operand and drops
+//     x2 w2 <= 2^-22 |x||w|                                             -> e_rep = 3.1 * 2^-22 (0 for P = 3);
+//   * HMMA accumulation: every mma.sync adds <= 17 addends aligned to the largest exponent and truncated below
+//     2^-23 of it, at most 18 instructions per output                    -> e_acc = 2^-15 of sum |x||w| (generous);
+//   * the exact kernel's own distance to real arithmetic: fp32 FMA chains of <= 48 terms, gamma_48 < 2^-18;
+//   * softplus is 1-Lipschitz; the fast softplus adds kFastSoftplusErr + 2^-22 y, NumPy's adds <= 2^-22 y.
+// Inputs are bounded by 1 (sin / cos) and by the box (raw coordinates).
+static double filter_delta(int pieces, const float* w1, const float* b1, const float* w2, const float* b2, const float* w3,
+                           const float* b3, double x_raw) {
+  const double e_rep = pieces == 2 ? 3.1 * std::ldexp(1.0, -22) : 0.0;
+  const double e = e_rep + std::ldexp(1.0, -15) + std::ldexp(1.0, -18);
+  const double sp_rel = 2.0 * std::ldexp(1.0, -22), sp_abs = (double)kFastSoftplusErr;
+  auto softplus = [](double z) { return std::log1p(std::exp(-std::fabs(z))) + std::max(z, 0.0); };
+  double eh1[kHidden], H1[kHidden], eh2[kHidden], H2[kHidden];
+  for (int n = 0; n < kHidden; n++) {
+    double s = 0.0;
+    for (int k = 0; k < kSdfIn; k++) s += std::fabs((double)w1[n * kSdfIn + k]) * (k < 3 ? x_raw : 1.0);
+    H1[n] = softplus(std::fabs((double)b1[n]) + s);
+    eh1[n] = e * s + std::ldexp(1.0, -22) * (std::fabs((double)b1[n]) + s) + sp_abs + sp_rel * H1[n];
+  }
+  for (int n = 0; n < kHidden; n++) {
+    double s = 0.0, err = 0.0;
+    for (int k = 0; k < kHidden; k++) {
+      const double a = std::fabs((double)w2[n * kHidden + k]);
+      s += a * H1[k];
+      err += a * (eh1[k] + e * (H1[k] + eh1[k]));
+    }
+    H2[n] = softplus(std::fabs((double)b2[n]) + s);
+    eh2[n] = err + std::ldexp(1.0, -22) * (std::fabs((double)b2[n]) + s) + sp_abs + sp_rel * H2[n];
+  }
+  double err = 0.0, s = std::fabs((double)b3[0]);
+  for (int k = 0; k < kHidden; k++) {
+    const double a = std::fabs((double)w3[k]);  // output 0 = the distance
+    s += a * H2[k];
+    err += a * eh2[k];
+  }
+  return 1.05 * (err + std::ldexp(1.0, -17) * s) + 1e-6;
+}
+
 template <int P>
-void pack_sdf_mma(int n_cells, const float* const w[3], const float* const b[3], std::vector<uint32_t>& out) {
+void pack_sdf_mma(int n_cells, const float* const w[3], const float* const b[3], double x_raw, std::vector<uint32_t>& out,
+                  double* delta_max) {
   using Blob = MmaBlobT<P>;
   out.assign((size_t)n_cells * Blob::words, 0u);
   for (int c = 0; c < n_cells; c++) {
@@ -221,6 +263,10 @@ void pack_sdf_mma(int n_cells, const float* const w[3], const float* const b[3],
     for (int j = 0; j < kSdfOut; j++)
       for (int k = 0; k < kHidden; k++) w3t[k * kSdfOutPad + j] = w3[j * kHidden + k];
     std::memcpy(blob + Blob::b3, b[2] + (size_t)c * kSdfOut, kSdfOut * sizeof(float));
+    const double delta = filter_delta(P, w1, b[0] + (size_t)c * kHidden, w2, b[1] + (size_t)c * kHidden, w3, b[2] + (size_t)c * kSdfOut, x_raw);
+    const float delta_f = std::nextafter((float)delta, INFINITY);
+    std::memcpy(blob + Blob::b3 + kFilterDeltaSlot, &delta_f, sizeof(float));
+    if (delta_max) *delta_max = std::max(*delta_max, (double)delta_f);
   }
 }
 
@@ -271,7 +317,10 @@ int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
   KNF_CUDA(cudaMemcpy(F.col_blobs, packed.data(), packed.size() * sizeof(float), cudaMemcpyHostToDevice));
   {
     std::vector<uint32_t> frags;
-    pack_sdf_mma<3>(F.geom.n_cells, d->sdf_w, d->sdf_b, frags);
+    double x_raw = 0.0;
+    for (int a = 0; a < 3; a++) x_raw = std::max(x_raw, std::max(std::fabs(d->bbox_min[a]), std::fabs(d->bbox_max[a])));
+    x_raw *= 1.001;
+    pack_sdf_mma<3>(F.geom.n_cells, d->sdf_w, d->sdf_b, x_raw, frags, nullptr);
     KNF_CUDA(cudaMalloc(&F.sdf_mma_blobs, frags.size() * sizeof(uint32_t)));
     KNF_CUDA(cudaMemcpy(F.sdf_mma_blobs, frags.data(), frags.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     // fp16 pieces need |w| < 65504 in the two hidden layers (true of any trained or random-init field)
@@ -280,7 +329,8 @@ int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
     for (size_t i = 0; i < n1 && F.fp16_ok; i++) F.fp16_ok = std::fabs(d->sdf_w[0][i]) < 60000.0f;
     for (size_t i = 0; i < n2 && F.fp16_ok; i++) F.fp16_ok = std::fabs(d->sdf_w[1][i]) < 60000.0f;
     if (F.fp16_ok) {
-      pack_sdf_mma<2>(F.geom.n_cells, d->sdf_w, d->sdf_b, frags);
+      F.filter_delta_max = 0.0;
+      pack_sdf_mma<2>(F.geom.n_cells, d->sdf_w, d->sdf_b, x_raw, frags, &F.filter_delta_max);
       KNF_CUDA(cudaMalloc(&F.sdf_mmah_blobs, frags.size() * sizeof(uint32_t)));
       KNF_CUDA(cudaMemcpy(F.sdf_mmah_blobs, frags.data(), frags.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     }
@@ -294,6 +344,13 @@ int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
     else return fail(KNF_E_INVALID, "KNF_PRECISION must be fp32_chain, tensor_bf16x3 or tensor_fp16x2");
   }
   if (F.precision == KNF_PRECISION_TENSOR_FP16X2 && !F.fp16_ok) F.precision = KNF_PRECISION_TENSOR_BF16X3;
+  if (const char* env = std::getenv("KNF_FILTER")) {
+    const std::string v(env);
+    if (v == "off" || v == "0") F.filter_mode = KNF_FILTER_OFF;
+    else if (v == "on" || v == "1") F.filter_mode = KNF_FILTER_ON;
+    else if (v == "auto" || v == "2") F.filter_mode = KNF_FILTER_AUTO;
+    else return fail(KNF_E_INVALID, "KNF_FILTER must be off, on or auto");
+  }
   *out = h.release();
   return 0;
 }
@@ -601,7 +658,7 @@ int knf_field_stats_reset(knf_field_t f) {
   KNF_CUDA(cudaDeviceSynchronize());
   KNF_TRY(collect_profile(f->f));
   f->f.stats = KnfStats{};
-  if (f->f.ws.counters.p) KNF_CUDA(cudaMemset(stat_counter(f->f, 0), 0, 4 * sizeof(unsigned long long)));
+  if (f->f.ws.counters.p) KNF_CUDA(cudaMemset(stat_counter(f->f, 0), 0, 8 * sizeof(unsigned long long)));
   return 0;
 }
 
@@ -626,6 +683,19 @@ int knf_field_set_precision(knf_field_t f, int mode) {
 int knf_field_get_precision(knf_field_t f) {
   KNF_TRY(check_field(f));
   return f->f.precision;
+}
+
+int knf_field_set_filter(knf_field_t f, int mode) {
+  KNF_TRY(check_field(f));
+  if (mode != KNF_FILTER_OFF && mode != KNF_FILTER_ON && mode != KNF_FILTER_AUTO) return fail(KNF_E_INVALID, "unknown KNF_FILTER_* mode");
+  std::lock_guard<std::mutex> lk(f->f.mu);
+  f->f.filter_mode = mode;
+  return 0;
+}
+
+double knf_field_filter_delta(knf_field_t f) {
+  if (check_field(f) != 0) return -1.0;
+  return f->f.filter_delta_max;
 }
 
 // ---- routing ---------------------------------------------------------------------------------------

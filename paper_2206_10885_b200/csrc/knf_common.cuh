@@ -284,6 +284,24 @@ __device__ __forceinline__ float2 softplus_np_f2(float2 x) {
   return a[0];
 }
 
+// Decision-filter softplus (knf_march.cuh): MUFU.EX2 / MUFU.LG2, absolute error below kFastSoftplusErr (PTX ISA:
+// ex2.approx.ftz.f32 max relative error 2^-22, lg2.approx.ftz.f32 max absolute error 2^-22 on (0.5, 2); plus four
+// fp32 roundings of values <= max(1, y)).  Never reaches a result: it only feeds the filter's predicate.
+constexpr float kFastSoftplusErr = 1.0e-6f;  // + 2^-22 * y, accounted for in the filter bound
+template <int N>
+__device__ __forceinline__ void softplus_fast_f2xN(float2 (&x)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; i++) {
+    float ex, ey, lx, ly;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ex) : "f"(__fmul_rn(-fabsf(x[i].x), 1.4426950408889634f)));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ey) : "f"(__fmul_rn(-fabsf(x[i].y), 1.4426950408889634f)));
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lx) : "f"(__fadd_rn(1.0f, ex)));
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(ly) : "f"(__fadd_rn(1.0f, ey)));
+    x[i] = __ffma2_rn(make_float2(lx, ly), make_float2(0.6931471805599453f, 0.6931471805599453f),
+                      make_float2(fmaxf(x[i].x, 0.0f), fmaxf(x[i].y, 0.0f)));
+  }
+}
+
 // Which softplus the tile kernels run: 1 = softplus_np (NumPy bit-exact, 34 packed FMA-pipe steps per pair),
 // 0 = softplus_f2 (same accuracy against float64, 24 steps, agrees with NumPy on 64 % of arguments).
 #ifndef KNF_SOFTPLUS_EXACT

@@ -50,7 +50,7 @@ void DevBuf::release() {
 }
 
 void Workspace::release_all() {
-  DevBuf* all[] = {&tile_base, &req_pt1, &req_cell1, &req_rank1, &req_pt, &req_cell, &req_rank, &perm, &tiles, &cell_count, &cell_offset, &counters, &t, &t_prev,
+  DevBuf* all[] = {&req_pt2, &req_cell2, &req_rank2, &req_pt3, &req_cell3, &req_rank3, &cell_count_f, &live2, &live3, &tile_base, &req_pt1, &req_cell1, &req_rank1, &req_pt, &req_cell, &req_rank, &perm, &tiles, &cell_count, &cell_offset, &counters, &t, &t_prev,
                    &d_prev, &t_conv, &d_conv, &t_hit, &steps, &phase, &hit, &live0, &live1, &hit_list,
                    &hit_count, &sdf_out, &col_v, &col_n, &col_z, &rgb, &origins, &dirs, &t_near, &t_far, &normals64,
                    &colors64, &frame_color, &frame_depth, &frame_normal, &frame_hit};
@@ -70,7 +70,9 @@ static inline int blocks_for(size_t n, int threads = 256) {
     if (_rc != 0) return _rc; \
   } while (0)
 
-constexpr size_t kCounterBytes = 4 * sizeof(RouteCounters) + 4 * sizeof(unsigned long long);
+constexpr int kRouteSlots = 6;    // 0/1 exact march queue (ping-pong), 2 SDF forward, 3 colour forward, 4/5 filter march queue
+constexpr int kStatCounters = 8;  // see finish_stats
+constexpr size_t kCounterBytes = kRouteSlots * sizeof(RouteCounters) + kStatCounters * sizeof(unsigned long long);
 
 int ensure_requests(Field& F, size_t n) {
   Workspace& W = F.ws;
@@ -111,6 +113,19 @@ int ensure_rays(Field& F, size_t n) {
   KNF_TRY(W.req_pt1.ensure(n * sizeof(float4)));
   KNF_TRY(W.req_cell1.ensure(n * sizeof(int)));
   KNF_TRY(W.req_rank1.ensure(n * sizeof(int)));
+  KNF_TRY(W.req_pt2.ensure(n * sizeof(float4)));
+  KNF_TRY(W.req_cell2.ensure(n * sizeof(int)));
+  KNF_TRY(W.req_rank2.ensure(n * sizeof(int)));
+  KNF_TRY(W.req_pt3.ensure(n * sizeof(float4)));
+  KNF_TRY(W.req_cell3.ensure(n * sizeof(int)));
+  KNF_TRY(W.req_rank3.ensure(n * sizeof(int)));
+  KNF_TRY(W.live2.ensure(n * 4));
+  KNF_TRY(W.live3.ensure(n * 4));
+  {
+    const bool fresh_f = W.cell_count_f.p == nullptr;
+    KNF_TRY(W.cell_count_f.ensure((size_t)F.geom.n_cells * sizeof(int)));
+    if (fresh_f) KNF_CUDA(cudaMemset(W.cell_count_f.p, 0, W.cell_count_f.cap));
+  }
   KNF_TRY(W.hit_list.ensure(n * 4));
   KNF_TRY(W.hit_count.ensure(16));
   W.ray_cap = std::max(W.ray_cap, n);
@@ -119,16 +134,19 @@ int ensure_rays(Field& F, size_t n) {
 
 RouteCounters* counters(Field& F, int slot) { return F.ws.counters.as<RouteCounters>() + slot; }
 unsigned long long* stat_counter(Field& F, int which) {
-  return reinterpret_cast<unsigned long long*>(F.ws.counters.as<RouteCounters>() + 4) + which;
+  return reinterpret_cast<unsigned long long*>(F.ws.counters.as<RouteCounters>() + kRouteSlots) + which;
 }
 
 RouteBuffers route_buffers(Field& F, int slot, int next_slot, int list) {
   Workspace& W = F.ws;
   RouteBuffers R;
-  R.req_pt = (list ? W.req_pt1 : W.req_pt).as<float4>();
-  R.req_cell = (list ? W.req_cell1 : W.req_cell).as<int>();
-  R.req_rank = (list ? W.req_rank1 : W.req_rank).as<int>();
-  R.cell_count = W.cell_count.as<int>();
+  DevBuf* pts[4] = {&W.req_pt, &W.req_pt1, &W.req_pt2, &W.req_pt3};
+  DevBuf* cells[4] = {&W.req_cell, &W.req_cell1, &W.req_cell2, &W.req_cell3};
+  DevBuf* ranks[4] = {&W.req_rank, &W.req_rank1, &W.req_rank2, &W.req_rank3};
+  R.req_pt = pts[list]->as<float4>();
+  R.req_cell = cells[list]->as<int>();
+  R.req_rank = ranks[list]->as<int>();
+  R.cell_count = (list >= 2 ? W.cell_count_f : W.cell_count).as<int>();
   R.cell_offset = W.cell_offset.as<int>();
   R.tile_base = W.tile_base.as<int>();
   R.perm = W.perm.as<int>();
@@ -143,7 +161,7 @@ int begin_call(Field& F, cudaStream_t st) {
   KNF_CUDA(cudaSetDevice(F.device));
   KNF_TRY(ensure_requests(F, 1024));
   KNF_CUDA(cudaMemsetAsync(F.ws.cell_count.p, 0, (size_t)F.geom.n_cells * sizeof(int), st));
-  KNF_CUDA(cudaMemsetAsync(F.ws.counters.p, 0, 4 * sizeof(RouteCounters), st));  // stat counters persist
+  KNF_CUDA(cudaMemsetAsync(F.ws.counters.p, 0, kRouteSlots * sizeof(RouteCounters), st));  // stat counters persist
   if (!F.smem_configured) {
     KNF_CUDA(cudaFuncSetAttribute(mlp_warp_kernel<kSdfIn, kSdfOut, kSdfOutPad, ACT_SOFTPLUS, false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SdfKernelSmem)));
@@ -151,9 +169,10 @@ int begin_call(Field& F, cudaStream_t st) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ColKernelSmem)));
     KNF_CUDA(cudaFuncSetAttribute(march_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sizeof(SdfKernelSmem)));
-    KNF_CUDA(cudaFuncSetAttribute(march_mma_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<3>)));
+    KNF_CUDA(cudaFuncSetAttribute(march_mma_kernel<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<3>)));
     KNF_CUDA(cudaFuncSetAttribute(sdf_mma_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<3>)));
-    KNF_CUDA(cudaFuncSetAttribute(march_mma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<2>)));
+    KNF_CUDA(cudaFuncSetAttribute(march_mma_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<2>)));
+    KNF_CUDA(cudaFuncSetAttribute(march_mma_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<2>)));
     KNF_CUDA(cudaFuncSetAttribute(sdf_mma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<2>)));
     if (!F.host_poll) KNF_CUDA(cudaMallocHost(&F.host_poll, 64));
     F.smem_configured = true;
@@ -192,6 +211,7 @@ int collect_profile(Field& F) {
       case SPAN_SDF_MLP: F.stats.sdf_mlp_ms += ms; F.stats.sdf_mlp_launches += 1; break;
       case SPAN_ROUTE: F.stats.route_ms += ms; F.stats.route_launches += 1; break;
       case SPAN_COLOR_MLP: F.stats.color_mlp_ms += ms; break;
+      case SPAN_FILTER: F.stats.filter_ms += ms; F.stats.filter_launches += 1; break;
       default: F.stats.other_ms += ms; break;
     }
   }
@@ -201,13 +221,15 @@ int collect_profile(Field& F) {
 }
 
 int finish_stats(Field& F, cudaStream_t st) {
-  unsigned long long host[4] = {0, 0, 0, 0};
+  unsigned long long host[kStatCounters] = {};
   KNF_CUDA(cudaMemcpyAsync(host, stat_counter(F, 0), sizeof(host), cudaMemcpyDeviceToHost, st));
   KNF_CUDA(cudaStreamSynchronize(st));
   F.stats.sdf_evals = (int64_t)host[0];
   F.stats.color_evals = (int64_t)host[1];
   F.stats.march_lane_slots = (int64_t)host[2];
   F.stats.march_routed_requests = (int64_t)host[3];
+  F.stats.filter_evals = (int64_t)host[4];
+  F.stats.filter_deferred = (int64_t)host[5];
   return 0;
 }
 
@@ -317,11 +339,15 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
   M.hit = W.hit.as<unsigned char>();
   M.live[0] = W.live0.as<int>();
   M.live[1] = W.live1.as<int>();
+  M.live[2] = W.live2.as<int>();
+  M.live[3] = W.live3.as<int>();
   M.eps = s.eps_hit;
   M.step_scale = s.step_scale;
   M.max_steps = s.max_steps;
 
   KNF_CUDA(cudaMemsetAsync(counters(F, 0), 0, 2 * sizeof(RouteCounters), st));
+  KNF_CUDA(cudaMemsetAsync(counters(F, 4), 0, 2 * sizeof(RouteCounters), st));
+  KNF_CUDA(cudaMemsetAsync(W.cell_count_f.p, 0, (size_t)F.geom.n_cells * sizeof(int), st));
   const int nb = blocks_for((size_t)n);
   {
     ProfScope prof(F, st, SPAN_ROUTE);
@@ -329,46 +355,82 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     march_init_kernel<<<nb, 256, 0, st>>>(R0, F.geom, M, t_near, (int)n);
     F.stats.kernel_launches += 1;
   }
-  // Global wavefronts.  A ray is evaluated at least once per wavefront it takes part in, so
-  // max_steps stepping evaluations + one secant evaluation bound the count by max_steps + 1; tile
-  // residency usually finishes in far fewer, which the host learns by polling the request count.
-  for (int w = 0; w <= s.max_steps; w++) {
+  // The decision filter (knf_march.cuh) serves the exact mode only; the tensor modes evaluate everything on the
+  // tensor cores anyway.  auto: let the first global wavefront (one sample per ray) show whether rays enter the
+  // negative region at all -- on a real surface they never do and the filter passes would be empty launches.
+  const bool exact_mode = F.precision == KNF_PRECISION_FP32_CHAIN;
+  bool use_filter = exact_mode && F.fp16_ok && F.filter_mode != 0;
+  const bool probing = use_filter && F.filter_mode == 2;
+  bool filter_drained = false;  // the filter queue was seen empty after the filter had been switched off
+  const double crawl_on = -(s.eps_hit + 2.0 * F.filter_delta_max);
+  // Global wavefronts.  Every ray queued in a wavefront either advances a step or (once each) fetches its secant /
+  // re-check sample, so max_steps + 3 bounds the count; tile residency usually finishes in far fewer, which the
+  // host learns by polling the request counts.
+  for (int w = 0; w <= s.max_steps + 2; w++) {
     const int cur = w & 1, nxt = cur ^ 1;
+    const bool filter_pass = exact_mode && F.fp16_ok && F.filter_mode != 0 && !filter_drained && w > 0;
+    MarchTileArgs A{};
+    A.G = F.geom;
+    A.M = M;
+    A.next = route_buffers(F, nxt, -1, nxt);
+    A.next_filter = route_buffers(F, 4 + nxt, -1, 2 + nxt);
+    A.live_out = M.live[nxt];
+    A.live_filter = M.live[2 + nxt];
+    A.eval_counter = stat_counter(F, 0);
+    A.max_inner = (probing && w == 0) ? 1 : F.march_max_inner;
+    A.crawl_below = use_filter ? crawl_on : -INFINITY;
+    if (filter_pass) {
+      // filter queue of this wavefront: tensor-core predicate; undecided samples join the exact queue below
+      RouteBuffers Rf = route_buffers(F, 4 + cur, 4 + nxt, 2 + cur);
+      KNF_TRY(launch_scan_scatter(F, Rf, (size_t)n, st));
+      MarchTileArgs Af = A;
+      Af.P.blobs = reinterpret_cast<const float*>(F.sdf_mmah_blobs);
+      Af.P.perm = Rf.perm;
+      Af.P.tiles = Rf.tiles;
+      Af.P.ctr = Rf.ctr;
+      Af.P.req_pt = Rf.req_pt;
+      Af.live_in = M.live[2 + cur];
+      Af.defer = route_buffers(F, cur, -1, cur);
+      Af.live_defer = M.live[cur];
+      {
+        ProfScope prof(F, st, SPAN_FILTER);
+        march_mma_kernel<2, true><<<mlp_grid(F, (size_t)n, kMmaCtasPerSm), 32, sizeof(MmaSmemT<2>), st>>>(Af);
+      }
+      F.stats.kernel_launches += 1;
+    }
     RouteBuffers R = route_buffers(F, cur, nxt, cur);
     R.eval_counter = stat_counter(F, 3);  // requests that went through global routing
     KNF_TRY(launch_scan_scatter(F, R, (size_t)n, st));
-    MarchTileArgs A{};
     A.P.blobs = F.sdf_blobs;
     A.P.perm = R.perm;
     A.P.tiles = R.tiles;
     A.P.ctr = R.ctr;
     A.P.req_pt = R.req_pt;
-    A.next = route_buffers(F, nxt, -1, nxt);
-    A.G = F.geom;
-    A.M = M;
     A.live_in = M.live[cur];
-    A.live_out = M.live[nxt];
-    A.eval_counter = stat_counter(F, 0);
-    A.max_inner = F.march_max_inner;
     {
       ProfScope prof(F, st, SPAN_SDF_MLP);
       if (F.precision == KNF_PRECISION_TENSOR_BF16X3) {
         A.P.blobs = reinterpret_cast<const float*>(F.sdf_mma_blobs);
-        march_mma_kernel<3><<<mlp_grid(F, (size_t)n, kMmaCtasPerSm), 32, sizeof(MmaSmemT<3>), st>>>(A);
+        march_mma_kernel<3, false><<<mlp_grid(F, (size_t)n, kMmaCtasPerSm), 32, sizeof(MmaSmemT<3>), st>>>(A);
       } else if (F.precision == KNF_PRECISION_TENSOR_FP16X2) {
         A.P.blobs = reinterpret_cast<const float*>(F.sdf_mmah_blobs);
-        march_mma_kernel<2><<<mlp_grid(F, (size_t)n, kMmaCtasPerSm), 32, sizeof(MmaSmemT<2>), st>>>(A);
+        march_mma_kernel<2, false><<<mlp_grid(F, (size_t)n, kMmaCtasPerSm), 32, sizeof(MmaSmemT<2>), st>>>(A);
       } else {
         march_warp_kernel<<<mlp_grid(F, (size_t)n), 32, sizeof(SdfKernelSmem), st>>>(A);
       }
     }
     F.stats.kernel_launches += 1;
     F.stats.wavefronts += 1;
-    const bool poll = (w == 1) || (w == 3) || (w % 8 == 7);
-    if (poll && w < s.max_steps) {
+    const bool poll = (w == 0 && probing) || (w == 1) || (w == 3) || (w % 8 == 7);
+    if (poll && w < s.max_steps + 2) {
+      // n_requests of the next exact queue and of the next filter queue
       KNF_CUDA(cudaMemcpyAsync(F.host_poll, &counters(F, nxt)->n_requests, sizeof(int), cudaMemcpyDeviceToHost, st));
+      KNF_CUDA(cudaMemcpyAsync(F.host_poll + 1, &counters(F, 4 + nxt)->n_requests, sizeof(int), cudaMemcpyDeviceToHost, st));
       KNF_CUDA(cudaStreamSynchronize(st));
-      if (*F.host_poll == 0) break;
+      const int n_exact = F.host_poll[0], n_filter = F.host_poll[1];
+      if (n_exact == 0 && n_filter == 0) break;
+      if (probing && w == 0 && (size_t)n_filter * 8 < (size_t)(n_exact + n_filter)) use_filter = false;  // < 1/8 of the live rays crawl
+      if (!use_filter && n_filter == 0) filter_drained = true;
     }
   }
   if (want_hit_list) KNF_CUDA(cudaMemsetAsync(W.hit_count.p, 0, 16, st));

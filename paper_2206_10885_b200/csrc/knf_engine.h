@@ -39,6 +39,9 @@ struct Workspace {
   // routing
   DevBuf req_pt, req_cell, req_rank, perm, tiles;
   DevBuf req_pt1, req_cell1, req_rank1;  // second request list: the fused march kernel reads one list while filling the other
+  DevBuf req_pt2, req_cell2, req_rank2, req_pt3, req_cell3, req_rank3;  // the decision filter's two request lists
+  DevBuf cell_count_f;                   // per-cell request counts of the filter queue
+  DevBuf live2, live3;
   DevBuf cell_count, cell_offset, tile_base;
   DevBuf counters;  // RouteCounters[4] + stats counters
   // march state
@@ -64,6 +67,8 @@ struct Field {
   uint32_t* sdf_mma_blobs = nullptr;   // knf_mma.cuh MmaBlobT<3> per cell (bf16 x 3 B fragments)
   uint32_t* sdf_mmah_blobs = nullptr;  // MmaBlobT<2> per cell (fp16 x 2 B fragments); null when a weight exceeds the fp16 range
   bool fp16_ok = false;
+  double filter_delta_max = 0.0;       // largest per-cell decision-filter bound (knf_api.cu filter_delta)
+  int filter_mode = 2;                 // decision filter of the exact march: 0 off, 1 on, 2 auto (probe the first wavefront)
   int precision = 0;                  // KNF_PRECISION_*: which SDF tile kernels run
   Workspace ws;
   std::mutex mu;
@@ -82,7 +87,7 @@ struct Field {
   int march_max_inner = 8;    // tile-residency cap (steps in place per tile visit)
 };
 
-enum { SPAN_SDF_MLP = 0, SPAN_ROUTE = 1, SPAN_COLOR_MLP = 2, SPAN_OTHER = 3 };
+enum { SPAN_SDF_MLP = 0, SPAN_ROUTE = 1, SPAN_COLOR_MLP = 2, SPAN_OTHER = 3, SPAN_FILTER = 4 };
 // RAII: records an event pair around the launches issued in its scope when F.profiling is set.
 struct ProfScope {
   Field& F;
@@ -98,7 +103,7 @@ int collect_profile(Field& F);  // syncs; folds finished spans into F.stats
 // ---- drivers (all asynchronous on `st`; pointers are device pointers) -------------------------
 int ensure_requests(Field& F, size_t n_requests);
 int ensure_rays(Field& F, size_t n_rays);
-RouteBuffers route_buffers(Field& F, int counter_slot, int next_slot, int list = 0);
+RouteBuffers route_buffers(Field& F, int counter_slot, int next_slot, int list = 0);  // list 0/1: exact queue, 2/3: filter queue
 RouteCounters* counters(Field& F, int slot);
 unsigned long long* stat_counter(Field& F, int which);  // 0 = sdf evals, 1 = colour evals
 int begin_call(Field& F, cudaStream_t st);              // select device, reset routing invariants

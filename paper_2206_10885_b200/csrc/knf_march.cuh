@@ -20,15 +20,32 @@
 namespace knf {
 
 struct MarchTileArgs {
-  MlpParams P;         // current wavefront: blobs, perm, tiles, counters, request points
-  RouteBuffers next;   // where rays that leave their tile are queued for the next wavefront
+  MlpParams P;              // current wavefront: blobs, perm, tiles, counters, request points
+  RouteBuffers next;        // exact queue of the next wavefront: rays that leave their tile and need an exact distance
+  RouteBuffers next_filter; // filter queue of the next wavefront: rays crawling through the negative region
+  RouteBuffers defer;       // filter kernel only: exact queue of THIS wavefront, for samples the filter cannot decide
   GridGeom G;
   MarchState M;
-  const int* live_in;  // request slot -> ray id (current wavefront)
-  int* live_out;       // same for the next wavefront
-  unsigned long long* eval_counter;  // statistics: SDF evaluations performed
-  int max_inner;       // cap on consecutive in-place steps of one tile
+  const int* live_in;       // request slot -> ray id (the list being consumed)
+  int* live_out;            // ... of `next`
+  int* live_filter;         // ... of `next_filter`
+  int* live_defer;          // ... of `defer`
+  unsigned long long* eval_counter;  // statistics: [0] SDF evaluations, [2] lane slots, [4] filter evaluations, [5] deferred
+  int max_inner;            // cap on consecutive in-place steps of one tile
+  double crawl_below;       // exact kernels: a march step from a distance below this continues in the filter queue (-inf: never)
 };
+
+// Queue one ray's next sample (warp-uniform call; `emit` selects the lanes that take part).
+__device__ __forceinline__ void march_emit(const RouteBuffers& Q, int* live, bool emit, int ray, const RayRegs& rr, const MarchState& M,
+                                           float x, float y, float z, int cell) {
+  if (!__any_sync(0xffffffffu, emit)) return;  // skip the collectives when nobody leaves
+  const int slot = warp_append(&Q.ctr->n_requests, emit);
+  if (emit) {
+    live[slot] = ray;
+    ray_store(rr, M, ray);
+  }
+  route_emit_cell(Q, emit, slot, x, y, z, cell);
+}
 
 static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(MarchTileArgs A) {
   using Blob = SdfBlob;
@@ -101,16 +118,16 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(M
       passes += 1;
 
       // ---- the march step for the lane's two rays -----------------------------------------------------
-      bool want[2], stay[2];
-      int cell[2];
+      int code[2], cell[2];
+      bool stay[2];
 #pragma unroll
       for (int q = 0; q < 2; q++) {
-        want[q] = false;
+        code[q] = STEP_DONE;
         cell[q] = -1;
         if (active[q]) {
           double t_next = 0.0;
-          want[q] = ray_step(rr[q], A.M, ray[q], q ? dist.y : dist.x, t_next);
-          if (want[q]) {
+          code[q] = ray_step(rr[q], A.M, ray[q], q ? dist.y : dist.x, t_next, A.crawl_below);
+          if (code[q] != STEP_DONE) {
             // pts = origins + t * dirs in fp64 (surface.py:184), then the fp32 cast of grid.py:375
             px[q] = __double2float_rn(rr[q].o[0] + t_next * rr[q].d[0]);
             py[q] = __double2float_rn(rr[q].o[1] + t_next * rr[q].d[1]);
@@ -120,22 +137,15 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(M
             cell[q] = well_inside ? tile.cell : cell_of(px[q], py[q], pz[q], A.G);
           }
         }
-        stay[q] = want[q] && cell[q] == tile.cell;
+        stay[q] = code[q] == STEP_EXACT && cell[q] == tile.cell;
       }
       const int n_stay = __popc(__ballot_sync(0xffffffffu, stay[0])) + __popc(__ballot_sync(0xffffffffu, stay[1]));
       // keep stepping in place while at least half of the tile's rays are still here
       const bool cont = n_stay > 0 && 2 * n_stay >= tile.count && inner + 1 < A.max_inner;
 #pragma unroll
       for (int q = 0; q < 2; q++) {
-        const bool emit = want[q] && !(cont && stay[q]);
-        if (__any_sync(0xffffffffu, emit)) {  // warp-uniform: skip the collectives when nobody leaves
-          const int slot = warp_append(&A.next.ctr->n_requests, emit);
-          if (emit) {
-            A.live_out[slot] = ray[q];
-            ray_store(rr[q], A.M, ray[q]);
-          }
-          route_emit_cell(A.next, emit, slot, px[q], py[q], pz[q], cell[q]);
-        }
+        march_emit(A.next, A.live_out, code[q] == STEP_EXACT && !(cont && stay[q]), ray[q], rr[q], A.M, px[q], py[q], pz[q], cell[q]);
+        march_emit(A.next_filter, A.live_filter, code[q] == STEP_FILTER, ray[q], rr[q], A.M, px[q], py[q], pz[q], cell[q]);
         active[q] = cont && stay[q];
         if (!active[q]) px[q] = py[q] = pz[q] = 0.f;
       }
@@ -154,7 +164,17 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(M
 // ---- the same kernel with the hidden layers on the tensor cores (knf_mma.cuh) ------------------------------
 // Lane (g, t) owns tile points 16 t + g and 16 t + g + 8 (rows g, g + 8 of m-tile t), so the distance the quad
 // butterfly leaves in every lane of quad g is picked up by the lane whose t equals the m-tile index.
-template <int PC>
+//
+// FILTER = false: the tensor-core distance IS the evaluation (KNF_PRECISION_TENSOR_*).
+// FILTER = true : the DECISION FILTER of the exact mode.  98.5 % of the march evaluations of the BASELINE frame are
+//   taken by rays crawling through a negative region with the fixed step scale * eps / 2 (surface.py:217-219): the
+//   reference looks at such a distance only to see that it is still below -eps.  This kernel answers that
+//   predicate from a tensor-core evaluation with a proven error bound delta (per cell, stored in the blob):
+//   d_f < -(eps + delta) => d_exact < -eps, and the step is taken with the reference's own fp64 arithmetic.  Every
+//   sample it cannot decide is handed, unchanged, to the exact kernel's queue of the same wavefront; a ray that
+//   converges after filtered steps re-evaluates d_prev exactly first (PH_RECHECK).  Results are bit-identical to
+//   running the exact kernel on every sample (tests/test_gpu_march.py::test_decision_filter_is_exact).
+template <int PC, bool FILTER>
 static __global__ void __launch_bounds__(32, kMmaCtasPerSm) march_mma_kernel(MarchTileArgs A) {
   using Blob = MmaBlobT<PC>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -169,7 +189,7 @@ static __global__ void __launch_bounds__(32, kMmaCtasPerSm) march_mma_kernel(Mar
   const int n_tiles = P.ctr->n_tiles;
   const uint32_t* blobs = reinterpret_cast<const uint32_t*>(P.blobs);
   uint32_t parity = 0;
-  unsigned long long evals = 0, passes = 0;
+  unsigned long long evals = 0, slots = 0, deferred = 0;
 
   for (;;) {
     const int tix = next_tile(P.ctr, lane);
@@ -208,6 +228,7 @@ static __global__ void __launch_bounds__(32, kMmaCtasPerSm) march_mma_kernel(Mar
     }
     int n_active = tile.count;
     const float* W3t = reinterpret_cast<const float*>(S.w + Blob::w3);
+    double safe_below = 0.0;
 
     for (int inner = 0;; inner++) {
 #pragma unroll
@@ -222,6 +243,7 @@ static __global__ void __launch_bounds__(32, kMmaCtasPerSm) march_mma_kernel(Mar
       if (inner == 0) {
         mbar_wait(&S.bar, parity);
         parity ^= 1;
+        if (FILTER) safe_below = -(A.M.eps + (double)reinterpret_cast<const float*>(S.w + Blob::b3)[kFilterDeltaSlot]);
       }
       const float b3 = reinterpret_cast<const float*>(S.w + Blob::b3)[0];
       float2 dist = make_float2(0.f, 0.f);
@@ -229,23 +251,26 @@ static __global__ void __launch_bounds__(32, kMmaCtasPerSm) march_mma_kernel(Mar
       for (int m = 0; m < 4; m++) {
         if ((act_mask & (0x11111111u << m)) == 0) continue;
         float h2[4][4];
-        mma_hidden<PC>(S, m, lane, h2);
+        mma_hidden<PC, FILTER>(S, m, lane, h2);
         const float2 d = mma_output(h2, W3t, b3, t, 0);
         if (m == t) dist = d;
+        slots += 16;
       }
       evals += (lane == 0) ? (unsigned long long)n_active : 0ull;
-      passes += 1;
 
-      bool want[2], stay[2];
-      int cell[2];
+      int code[2], cell[2];
+      bool stay[2];
 #pragma unroll
       for (int q = 0; q < 2; q++) {
-        want[q] = false;
+        code[q] = STEP_DONE;
         cell[q] = -1;
         if (active[q]) {
           double t_next = 0.0;
-          want[q] = ray_step(rr[q], A.M, ray[q], q ? dist.y : dist.x, t_next);
-          if (want[q]) {
+          code[q] = FILTER ? ray_filter_step(rr[q], A.M, ray[q], q ? dist.y : dist.x, safe_below, t_next)
+                           : ray_step(rr[q], A.M, ray[q], q ? dist.y : dist.x, t_next, A.crawl_below);
+          if (FILTER && code[q] == STEP_EXACT) {
+            cell[q] = tile.cell;  // undecided: the same sample goes to the exact queue of this wavefront
+          } else if (code[q] != STEP_DONE) {
             px[q] = __double2float_rn(rr[q].o[0] + t_next * rr[q].d[0]);
             py[q] = __double2float_rn(rr[q].o[1] + t_next * rr[q].d[1]);
             pz[q] = __double2float_rn(rr[q].o[2] + t_next * rr[q].d[2]);
@@ -254,20 +279,21 @@ static __global__ void __launch_bounds__(32, kMmaCtasPerSm) march_mma_kernel(Mar
             cell[q] = well_inside ? tile.cell : cell_of(px[q], py[q], pz[q], A.G);
           }
         }
-        stay[q] = want[q] && cell[q] == tile.cell;
+        // rays that keep this kernel's kind of evaluation and stay in the cell may step in place
+        stay[q] = code[q] == (FILTER ? STEP_FILTER : STEP_EXACT) && cell[q] == tile.cell;
       }
       const int n_stay = __popc(__ballot_sync(0xffffffffu, stay[0])) + __popc(__ballot_sync(0xffffffffu, stay[1]));
       const bool cont = n_stay > 0 && 2 * n_stay >= tile.count && inner + 1 < A.max_inner;
 #pragma unroll
       for (int q = 0; q < 2; q++) {
-        const bool emit = want[q] && !(cont && stay[q]);
-        if (__any_sync(0xffffffffu, emit)) {
-          const int slot = warp_append(&A.next.ctr->n_requests, emit);
-          if (emit) {
-            A.live_out[slot] = ray[q];
-            ray_store(rr[q], A.M, ray[q]);
-          }
-          route_emit_cell(A.next, emit, slot, px[q], py[q], pz[q], cell[q]);
+        const bool leaves = !(cont && stay[q]);
+        if (FILTER) {
+          march_emit(A.next_filter, A.live_filter, code[q] == STEP_FILTER && leaves, ray[q], rr[q], A.M, px[q], py[q], pz[q], cell[q]);
+          march_emit(A.defer, A.live_defer, code[q] == STEP_EXACT, ray[q], rr[q], A.M, px[q], py[q], pz[q], cell[q]);
+          deferred += (code[q] == STEP_EXACT) ? 1ull : 0ull;
+        } else {
+          march_emit(A.next, A.live_out, code[q] == STEP_EXACT && leaves, ray[q], rr[q], A.M, px[q], py[q], pz[q], cell[q]);
+          march_emit(A.next_filter, A.live_filter, code[q] == STEP_FILTER, ray[q], rr[q], A.M, px[q], py[q], pz[q], cell[q]);
         }
         active[q] = cont && stay[q];
         if (!active[q]) px[q] = py[q] = pz[q] = 0.f;
@@ -278,9 +304,16 @@ static __global__ void __launch_bounds__(32, kMmaCtasPerSm) march_mma_kernel(Mar
     }
     __syncwarp();
   }
-  if (lane == 0 && evals && A.eval_counter) {
-    atomicAdd(A.eval_counter, evals);
-    atomicAdd(A.eval_counter + 2, passes * kWarpPts);
+  if (A.eval_counter) {
+    if (FILTER) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) deferred += __shfl_xor_sync(0xffffffffu, deferred, off);
+    }
+    if (lane == 0 && evals) {
+      atomicAdd(A.eval_counter + (FILTER ? 4 : 0), evals);
+      if (FILTER) atomicAdd(A.eval_counter + 5, deferred);
+      else atomicAdd(A.eval_counter + 2, slots);
+    }
   }
 }
 

@@ -56,6 +56,7 @@ struct MmaBlobT {
 };
 using MmaBlob = MmaBlobT<3>;
 using MmaBlobH = MmaBlobT<2>;
+constexpr int kFilterDeltaSlot = kSdfOutPad - 1;  // b3[11]: proven bound on |tensor distance - exact distance| in this cell
 constexpr float kHalfPieceScale = 2048.0f;  // 2^11: the fp16 second piece carries (x - x1) * 2^11
 
 // Which reference feature (nn.fourier_encode column, nn.py:84-93) sits at position `kslot` of k-tile
@@ -162,7 +163,7 @@ __device__ __forceinline__ void mma_layer(const APieces<P> (&A)[KT], const uint2
 }
 
 // h = softplus(big + small [/ 2^11] + bias) on the accumulator fragments: eight independent packed evaluations in flight.
-template <int P>
+template <int P, bool FAST>
 __device__ __forceinline__ void finish_hidden(const float (&small)[4][4], const float (&big)[4][4], const float* __restrict__ bias,
                                               int t, float (&h)[4][4]) {
   float2 r[8];
@@ -176,7 +177,8 @@ __device__ __forceinline__ void finish_hidden(const float (&small)[4][4], const 
       r[2 * nt + hh] = __fadd2_rn(z, b);
     }
   }
-  softplus_tile<8>(r);
+  if (FAST) softplus_fast_f2xN<8>(r);
+  else softplus_tile<8>(r);
 #pragma unroll
   for (int nt = 0; nt < 4; nt++) {
     h[nt][0] = r[2 * nt].x; h[nt][1] = r[2 * nt].y; h[nt][2] = r[2 * nt + 1].x; h[nt][3] = r[2 * nt + 1].y;
@@ -185,7 +187,7 @@ __device__ __forceinline__ void finish_hidden(const float (&small)[4][4], const 
 
 // Hidden activations h2 (after both softplus layers) of m-tile `m` of the warp's 64 points, in accumulator
 // layout: h2[nt][0..1] = row g, columns 8nt+2t, +1 ; h2[nt][2..3] = row g+8.  Coordinates come from S.pts.
-template <int P>
+template <int P, bool FAST>
 __device__ __forceinline__ void mma_hidden(const MmaSmemT<P>& S, int m, int lane, float (&h2)[4][4]) {
   using Blob = MmaBlobT<P>;
   const int g = lane >> 2, t = lane & 3;
@@ -229,7 +231,7 @@ __device__ __forceinline__ void mma_hidden(const MmaSmemT<P>& S, int m, int lane
                 make_float2(v[0][4 * kt + 2], v[0][4 * kt + 3]), make_float2(v[1][4 * kt + 2], v[1][4 * kt + 3]));
     mma_layer<P, Blob::kt1>(A, reinterpret_cast<const uint2*>(S.w + Blob::frag1), lane, small, big);
   }
-  finish_hidden<P>(small, big, reinterpret_cast<const float*>(S.w + Blob::b1), t, h1);
+  finish_hidden<P, FAST>(small, big, reinterpret_cast<const float*>(S.w + Blob::b1), t, h1);
   // ---- second layer: the accumulator fragment is the next A fragment ------------------------------------
   {
     APieces<P> A[Blob::kt2];
@@ -239,7 +241,7 @@ __device__ __forceinline__ void mma_hidden(const MmaSmemT<P>& S, int m, int lane
                 make_float2(h1[2 * kt + 1][0], h1[2 * kt + 1][1]), make_float2(h1[2 * kt + 1][2], h1[2 * kt + 1][3]));
     mma_layer<P, Blob::kt2>(A, reinterpret_cast<const uint2*>(S.w + Blob::frag2), lane, small, big);
   }
-  finish_hidden<P>(small, big, reinterpret_cast<const float*>(S.w + Blob::b2), t, h2);
+  finish_hidden<P, FAST>(small, big, reinterpret_cast<const float*>(S.w + Blob::b2), t, h2);
 }
 
 // Output column j of the 32 -> N3 layer for rows g (.x) and g+8 (.y): the lane's eight hidden units first
@@ -316,7 +318,7 @@ static __global__ void __launch_bounds__(32, kMmaCtasPerSm) sdf_mma_kernel(MlpPa
     const int m_tiles = (tile.count + 15) >> 4;
     for (int m = 0; m < m_tiles; m++) {
       float h2[4][4];
-      mma_hidden<PC>(S, m, lane, h2);
+      mma_hidden<PC, false>(S, m, lane, h2);
       const int s0 = S.slot[16 * m + g], s1 = S.slot[16 * m + g + 8];
       if (P.out_full == nullptr) {
         const float2 d = mma_output(h2, W3t, B3[0], t, 0);

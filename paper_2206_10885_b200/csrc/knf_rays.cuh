@@ -140,7 +140,12 @@ static __global__ void primary_rays_kernel(CameraDev cam, GridGeom box, int sub_
 }
 
 // ---- wavefront march (surface.march_rays, surface.py:162-226) ---------------------------------
-enum : unsigned char { PH_MARCH = 0, PH_REFINE = 1, PH_DONE = 2 };
+// PH_RECHECK: the ray converged while its d_prev came from the low-precision decision filter; the exact distance
+// at t_prev is being fetched before the secant step (surface.py:190-195) may use it.
+enum : unsigned char { PH_MARCH = 0, PH_REFINE = 1, PH_DONE = 2, PH_RECHECK = 3 };
+constexpr unsigned char kPhaseMask = 3, kApproxPrevBit = 0x80;  // stored phase byte: phase | (d_prev is approximate ? 0x80 : 0)
+// What a step asks for next.
+enum { STEP_DONE = 0, STEP_EXACT = 1, STEP_FILTER = 2 };
 
 struct MarchState {
   const double* o;   // (n,3)
@@ -155,7 +160,7 @@ struct MarchState {
   int* steps;
   unsigned char* phase;
   unsigned char* hit;
-  int* live[2];      // request slot -> ray id, double buffered by wavefront parity
+  int* live[4];      // request slot -> ray id: [queue * 2 + wavefront parity], queue 0 = exact, 1 = decision filter
   double eps;
   double step_scale;
   int max_steps;
@@ -202,6 +207,7 @@ struct RayRegs {
   double t, t_far, t_prev, d_prev;
   int steps;
   int phase;
+  int approx;  // d_prev was produced by the decision filter (knf_march.cuh) and is only good as a predicate
 };
 __device__ __forceinline__ void ray_load(RayRegs& R, const MarchState& M, int ray) {
   const size_t r3 = 3 * (size_t)ray;
@@ -215,7 +221,9 @@ __device__ __forceinline__ void ray_load(RayRegs& R, const MarchState& M, int ra
   R.t_prev = M.t_prev[ray];
   R.d_prev = M.d_prev[ray];
   R.steps = M.steps[ray];
-  R.phase = M.phase[ray];
+  const int ph = M.phase[ray];
+  R.phase = ph & kPhaseMask;
+  R.approx = (ph & kApproxPrevBit) ? 1 : 0;
 }
 // Write back what a later tile visit (or the finish kernel) needs.
 __device__ __forceinline__ void ray_store(const RayRegs& R, const MarchState& M, int ray) {
@@ -223,26 +231,45 @@ __device__ __forceinline__ void ray_store(const RayRegs& R, const MarchState& M,
   M.t_prev[ray] = R.t_prev;
   M.d_prev[ray] = R.d_prev;
   M.steps[ray] = R.steps;
-  M.phase[ray] = (unsigned char)R.phase;
+  M.phase[ray] = (unsigned char)(R.phase | (R.approx ? kApproxPrevBit : 0));
 }
 
-// One sphere-trace step of one ray (the body of the reference loop, surface.py:185-223) given the
-// fp32 distance `dval` the MLP just produced at the ray's current parameter.  Returns true when
-// the ray needs another evaluation, at parameter t_next (the next march position or the secant
-// candidate); on false the ray is finished and its result has been written to global memory.
-__device__ __forceinline__ bool ray_step(RayRegs& R, const MarchState& M, int ray, float dval, double& t_next) {
-  const double dv = (double)dval;
-  const double t = R.t;
+// One sphere-trace step of one ray (the body of the reference loop, surface.py:185-223) given the EXACT fp32
+// distance `dval` the MLP produced at the ray's requested parameter.  Returns STEP_DONE when the ray is finished
+// (its result has been written to global memory), otherwise the ray needs another evaluation at t_next:
+// STEP_EXACT, or STEP_FILTER when the ray just took a march step from a distance below `crawl_below` -- it is
+// inside the negative region, where the reference only asks "is d still < -eps?" (decision filter, knf_march.cuh).
+__device__ __forceinline__ int ray_step(RayRegs& R, const MarchState& M, int ray, float dval, double& t_next, double crawl_below) {
+  double dv = (double)dval;
+  double t = R.t;
   if (R.phase == PH_REFINE) {
     // surface.py:203-206: keep the secant point unless it is farther from the surface
     M.t_hit[ray] = (fabs(dv) > fabs(M.d_conv[ray])) ? M.t_conv[ray] : t;
     M.hit[ray] = 1;
     M.phase[ray] = PH_DONE;
     M.steps[ray] = R.steps;
-    return false;
+    return STEP_DONE;
   }
-  R.steps += 1;
-  if (fabs(dv) <= M.eps) {
+  bool converged;
+  if (R.phase == PH_RECHECK) {
+    // dval is the exact distance at t_prev; resume the convergence branch with the stored (t, d)
+    R.d_prev = dv;
+    R.approx = 0;
+    t = M.t_conv[ray];
+    dv = M.d_conv[ray];
+    converged = true;
+  } else {
+    R.steps += 1;
+    converged = fabs(dv) <= M.eps;
+    if (converged && R.approx && isfinite(R.t_prev)) {
+      M.t_conv[ray] = t;
+      M.d_conv[ray] = dv;
+      R.phase = PH_RECHECK;
+      t_next = R.t_prev;
+      return STEP_EXACT;
+    }
+  }
+  if (converged) {
     const double tp = R.t_prev, dp = R.d_prev;
     if (isfinite(tp) && (fabs(dv - dp) > 1e-12)) {
       double root = t - dv * (t - tp) / (dv - dp);
@@ -253,25 +280,52 @@ __device__ __forceinline__ bool ray_step(RayRegs& R, const MarchState& M, int ra
       R.t = root;
       R.phase = PH_REFINE;
       t_next = root;
-      return true;
+      return STEP_EXACT;
     }
     M.t_hit[ray] = t;
     M.hit[ray] = 1;
     M.phase[ray] = PH_DONE;
     M.steps[ray] = R.steps;
-    return false;
+    return STEP_DONE;
   }
   R.t_prev = t;
   R.d_prev = dv;
+  R.approx = 0;
   const double tn = t + M.step_scale * fmax(dv, M.eps / 2);
   R.t = tn;
   if (tn > R.t_far || R.steps >= M.max_steps) {
     M.phase[ray] = PH_DONE;  // left the box, or the step budget is spent: a miss
     M.steps[ray] = R.steps;
-    return false;
+    return STEP_DONE;
   }
   t_next = tn;
-  return true;
+  return dv < crawl_below ? STEP_FILTER : STEP_EXACT;
+}
+
+// The same step driven by an APPROXIMATE distance d_f with |d_f - d_exact| < delta (decision filter).  Only a
+// PH_MARCH ray in the negative region comes here.  If d_f < -(eps + delta) the exact distance is certainly below
+// -eps: the reference neither converges nor uses the value (max(d, eps/2) = eps/2), so the step is taken with the
+// reference's own arithmetic and d_f is remembered as a predicate-only d_prev.  Otherwise nothing is changed and
+// the caller re-queues the same sample for the exact kernel (STEP_EXACT, t_next = t).
+__device__ __forceinline__ int ray_filter_step(RayRegs& R, const MarchState& M, int ray, float d_f, double safe_below, double& t_next) {
+  const double dv = (double)d_f;
+  if (!(dv < safe_below)) {  // also catches NaN
+    t_next = R.t;
+    return STEP_EXACT;
+  }
+  R.steps += 1;
+  R.t_prev = R.t;
+  R.d_prev = dv;
+  R.approx = 1;
+  const double tn = R.t + M.step_scale * fmax(dv, M.eps / 2);
+  R.t = tn;
+  if (tn > R.t_far || R.steps >= M.max_steps) {
+    M.phase[ray] = PH_DONE;
+    M.steps[ray] = R.steps;
+    return STEP_DONE;
+  }
+  t_next = tn;
+  return STEP_FILTER;
 }
 
 // Write the TraceResult arrays (surface.py:225-226) and, optionally, compact the hit rays.

@@ -226,6 +226,17 @@ class DeviceField:
         code = self.PRECISIONS[mode] if isinstance(mode, str) else int(mode)
         N.check(N.load().knf_field_set_precision(self.handle, code))
 
+    FILTERS = {"off": 0, "on": 1, "auto": 2}
+
+    def set_filter(self, mode):
+        """Decision filter of the exact march (include/knf_b200.h knf_field_set_filter): "off" | "on" | "auto".
+        Results are bit-identical either way; it only changes which kernel answers the d < -eps predicates."""
+        code = self.FILTERS[mode] if isinstance(mode, str) else int(mode)
+        N.check(N.load().knf_field_set_filter(self.handle, code))
+
+    def filter_delta(self) -> float:
+        return float(N.load().knf_field_filter_delta(self.handle))
+
     def get_precision(self) -> str:
         code = N.load().knf_field_get_precision(self.handle)
         N.check(min(code, 0))
