@@ -116,6 +116,7 @@ typedef struct {
    * could not be decided and were re-evaluated exactly, and (while profiling) the filter launches' CUDA-event time */
   int64_t filter_evals;
   int64_t filter_deferred;
+  int64_t filter_skipped; /* march steps taken without any evaluation: certified by the cell's Lipschitz bound */
   int64_t filter_launches;
   double filter_ms;
 } KnfStats;

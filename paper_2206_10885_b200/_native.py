@@ -90,6 +90,7 @@ class KnfStats(C.Structure):
         ("march_routed_requests", C.c_int64),
         ("filter_evals", C.c_int64),
         ("filter_deferred", C.c_int64),
+        ("filter_skipped", C.c_int64),
         ("filter_launches", C.c_int64),
         ("filter_ms", C.c_double),
     ]

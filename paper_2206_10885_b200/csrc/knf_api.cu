@@ -216,6 +216,70 @@ static double filter_delta(int pieces, const float* w1, const float* b1, const f
   return 1.05 * (err + std::ldexp(1.0, -17) * s) + 1e-6;
 }
 
+// Proven Lipschitz bound of one cell's distance network d(x) = w3 . softplus(W2 softplus(W1 enc(x) + b1) + b2) + b3:
+// softplus' <= 1, so L <= |w3|_2 * |W2|_2 * sup_x |W1 J_enc(x)|_2.  |W2|_2 is bounded by Gershgorin on (W2^T W2)^16
+// (within 2 % of the true spectral norm).  J_enc is block diagonal per axis a: d/dx_a of (x_a, sin(2^o pi x_a),
+// cos(2^o pi x_a))_o = (1, 2^o pi cos, -2^o pi sin)_o; (cos, -sin) is a unit vector, so the axis-a column of W1 J
+// has norm <= |w_raw_a| + sum_o 2^o pi sigma_max([w_sin_o,a | w_cos_o,a]), and for a unit direction the three
+// axes combine by Cauchy-Schwarz.
+static double lipschitz_bound(const float* w1, const float* w2, const float* w3) {
+  double n3 = 0.0;
+  for (int k = 0; k < kHidden; k++) n3 += (double)w3[k] * (double)w3[k];
+  n3 = std::sqrt(n3);
+  std::vector<double> G(kHidden * kHidden), T(kHidden * kHidden);
+  for (int i = 0; i < kHidden; i++)
+    for (int j = 0; j < kHidden; j++) {
+      double a = 0.0;
+      for (int n = 0; n < kHidden; n++) a += (double)w2[n * kHidden + i] * (double)w2[n * kHidden + j];
+      G[i * kHidden + j] = a;
+    }
+  double log_scale = 0.0;  // G is rescaled between squarings so large weights cannot overflow
+  for (int sq = 0; sq < 4; sq++) {
+    double mx = 0.0;
+    for (double v : G) mx = std::max(mx, std::fabs(v));
+    if (mx > 0.0) {
+      for (double& v : G) v /= mx;
+      log_scale = 2.0 * (log_scale + std::log(mx));
+    } else {
+      log_scale *= 2.0;
+    }
+    for (int i = 0; i < kHidden; i++)
+      for (int j = 0; j < kHidden; j++) {
+        double a = 0.0;
+        for (int n = 0; n < kHidden; n++) a += G[i * kHidden + n] * G[n * kHidden + j];
+        T[i * kHidden + j] = a;
+      }
+    G.swap(T);
+  }
+  double row = 0.0;
+  for (int i = 0; i < kHidden; i++) {
+    double a = 0.0;
+    for (int j = 0; j < kHidden; j++) a += std::fabs(G[i * kHidden + j]);
+    row = std::max(row, a);
+  }
+  // lambda_max(W2^T W2)^16 <= row * exp(log_scale)  =>  |W2|_2 <= (row * exp(log_scale))^(1/32)
+  const double n2 = row > 0.0 ? std::exp((std::log(row) + log_scale) / 32.0) : 0.0;
+  double axes = 0.0;
+  for (int a = 0; a < 3; a++) {
+    double m = 0.0;
+    for (int n = 0; n < kHidden; n++) m += (double)w1[n * kSdfIn + a] * (double)w1[n * kSdfIn + a];
+    m = std::sqrt(m);
+    for (int o = 0; o < kSdfFreqs; o++) {
+      double aa = 0.0, bb = 0.0, ab = 0.0;
+      for (int n = 0; n < kHidden; n++) {
+        const double s = w1[n * kSdfIn + 3 + 6 * o + a], c = w1[n * kSdfIn + 3 + 6 * o + 3 + a];
+        aa += s * s;
+        bb += c * c;
+        ab += s * c;
+      }
+      const double lam = 0.5 * (aa + bb) + std::sqrt(0.25 * (aa - bb) * (aa - bb) + ab * ab);
+      m += std::ldexp(3.14159265358979323846, o) * std::sqrt(lam);
+    }
+    axes += m * m;
+  }
+  return 1.001 * n3 * n2 * std::sqrt(axes) + 1e-12;
+}
+
 template <int P>
 void pack_sdf_mma(int n_cells, const float* const w[3], const float* const b[3], double x_raw, std::vector<uint32_t>& out,
                   double* delta_max) {
@@ -253,7 +317,7 @@ void pack_sdf_mma(int n_cells, const float* const w[3], const float* const b[3],
                 split_fp16x2(wv[1], hi);
               }
               for (int piece = 0; piece < P; piece++)
-                frag[((((kt * 4 + nt) * P + piece) * 32) + lane) * 2 + h] = (uint32_t)lo[piece] | ((uint32_t)hi[piece] << 16);
+                frag[((((kt * 4 + nt) * 32) + lane) * P + piece) * 2 + h] = (uint32_t)lo[piece] | ((uint32_t)hi[piece] << 16);
             }
           }
     }
@@ -267,6 +331,8 @@ void pack_sdf_mma(int n_cells, const float* const w[3], const float* const b[3],
     const float delta_f = std::nextafter((float)delta, INFINITY);
     std::memcpy(blob + Blob::b3 + kFilterDeltaSlot, &delta_f, sizeof(float));
     if (delta_max) *delta_max = std::max(*delta_max, (double)delta_f);
+    const float lip_f = std::nextafter((float)lipschitz_bound(w1, w2, w3), INFINITY);
+    std::memcpy(blob + Blob::b3 + kFilterLipSlot, &lip_f, sizeof(float));
   }
 }
 
@@ -344,6 +410,7 @@ int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
     else return fail(KNF_E_INVALID, "KNF_PRECISION must be fp32_chain, tensor_bf16x3 or tensor_fp16x2");
   }
   if (F.precision == KNF_PRECISION_TENSOR_FP16X2 && !F.fp16_ok) F.precision = KNF_PRECISION_TENSOR_BF16X3;
+  if (const char* env = std::getenv("KNF_FILTER_SKIP")) F.filter_skip = std::atoi(env) != 0;
   if (const char* env = std::getenv("KNF_FILTER")) {
     const std::string v(env);
     if (v == "off" || v == "0") F.filter_mode = KNF_FILTER_OFF;

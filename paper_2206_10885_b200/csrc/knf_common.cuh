@@ -292,13 +292,15 @@ template <int N>
 __device__ __forceinline__ void softplus_fast_f2xN(float2 (&x)[N]) {
 #pragma unroll
   for (int i = 0; i < N; i++) {
-    float ex, ey, lx, ly;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ex) : "f"(__fmul_rn(-fabsf(x[i].x), 1.4426950408889634f)));
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ey) : "f"(__fmul_rn(-fabsf(x[i].y), 1.4426950408889634f)));
-    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lx) : "f"(__fadd_rn(1.0f, ex)));
-    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(ly) : "f"(__fadd_rn(1.0f, ey)));
-    x[i] = __ffma2_rn(make_float2(lx, ly), make_float2(0.6931471805599453f, 0.6931471805599453f),
-                      make_float2(fmaxf(x[i].x, 0.0f), fmaxf(x[i].y, 0.0f)));
+    // 2^(-|x| log2 e): one packed multiply, the -|.| rides on the MUFU operand
+    const float2 u = __fmul2_rn(x[i], make_float2(1.4426950408889634f, 1.4426950408889634f));
+    float2 e, l;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(-fabsf(u.x)));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(-fabsf(u.y)));
+    e = __fadd2_rn(e, make_float2(1.0f, 1.0f));
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l.x) : "f"(e.x));
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l.y) : "f"(e.y));
+    x[i] = __ffma2_rn(l, make_float2(0.6931471805599453f, 0.6931471805599453f), make_float2(fmaxf(x[i].x, 0.0f), fmaxf(x[i].y, 0.0f)));
   }
 }
 

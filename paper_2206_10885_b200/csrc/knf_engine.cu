@@ -169,10 +169,10 @@ int begin_call(Field& F, cudaStream_t st) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ColKernelSmem)));
     KNF_CUDA(cudaFuncSetAttribute(march_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sizeof(SdfKernelSmem)));
-    KNF_CUDA(cudaFuncSetAttribute(march_mma_kernel<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<3>)));
+    KNF_CUDA(cudaFuncSetAttribute(march_mma_kernel<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaMarchSmemT<3>)));
     KNF_CUDA(cudaFuncSetAttribute(sdf_mma_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<3>)));
-    KNF_CUDA(cudaFuncSetAttribute(march_mma_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<2>)));
-    KNF_CUDA(cudaFuncSetAttribute(march_mma_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<2>)));
+    KNF_CUDA(cudaFuncSetAttribute(march_mma_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaMarchSmemT<2>)));
+    KNF_CUDA(cudaFuncSetAttribute(march_mma_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaMarchSmemT<2>)));
     KNF_CUDA(cudaFuncSetAttribute(sdf_mma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<2>)));
     if (!F.host_poll) KNF_CUDA(cudaMallocHost(&F.host_poll, 64));
     F.smem_configured = true;
@@ -230,6 +230,7 @@ int finish_stats(Field& F, cudaStream_t st) {
   F.stats.march_routed_requests = (int64_t)host[3];
   F.stats.filter_evals = (int64_t)host[4];
   F.stats.filter_deferred = (int64_t)host[5];
+  F.stats.filter_skipped = (int64_t)host[6];
   return 0;
 }
 
@@ -379,6 +380,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     A.eval_counter = stat_counter(F, 0);
     A.max_inner = (probing && w == 0) ? 1 : F.march_max_inner;
     A.crawl_below = use_filter ? crawl_on : -INFINITY;
+    A.max_skip = F.filter_skip ? 1 : 0;
     if (filter_pass) {
       // filter queue of this wavefront: tensor-core predicate; undecided samples join the exact queue below
       RouteBuffers Rf = route_buffers(F, 4 + cur, 4 + nxt, 2 + cur);
@@ -394,7 +396,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
       Af.live_defer = M.live[cur];
       {
         ProfScope prof(F, st, SPAN_FILTER);
-        march_mma_kernel<2, true><<<mlp_grid(F, (size_t)n, kMmaCtasPerSm), 32, sizeof(MmaSmemT<2>), st>>>(Af);
+        march_mma_kernel<2, true><<<mlp_grid(F, (size_t)n, march_ctas_per_sm<2>()), 32, sizeof(MmaMarchSmemT<2>), st>>>(Af);
       }
       F.stats.kernel_launches += 1;
     }
@@ -411,10 +413,10 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
       ProfScope prof(F, st, SPAN_SDF_MLP);
       if (F.precision == KNF_PRECISION_TENSOR_BF16X3) {
         A.P.blobs = reinterpret_cast<const float*>(F.sdf_mma_blobs);
-        march_mma_kernel<3, false><<<mlp_grid(F, (size_t)n, kMmaCtasPerSm), 32, sizeof(MmaSmemT<3>), st>>>(A);
+        march_mma_kernel<3, false><<<mlp_grid(F, (size_t)n, march_ctas_per_sm<3>()), 32, sizeof(MmaMarchSmemT<3>), st>>>(A);
       } else if (F.precision == KNF_PRECISION_TENSOR_FP16X2) {
         A.P.blobs = reinterpret_cast<const float*>(F.sdf_mmah_blobs);
-        march_mma_kernel<2, false><<<mlp_grid(F, (size_t)n, kMmaCtasPerSm), 32, sizeof(MmaSmemT<2>), st>>>(A);
+        march_mma_kernel<2, false><<<mlp_grid(F, (size_t)n, march_ctas_per_sm<2>()), 32, sizeof(MmaMarchSmemT<2>), st>>>(A);
       } else {
         march_warp_kernel<<<mlp_grid(F, (size_t)n), 32, sizeof(SdfKernelSmem), st>>>(A);
       }

@@ -68,6 +68,7 @@ struct Field {
   uint32_t* sdf_mmah_blobs = nullptr;  // MmaBlobT<2> per cell (fp16 x 2 B fragments); null when a weight exceeds the fp16 range
   bool fp16_ok = false;
   double filter_delta_max = 0.0;       // largest per-cell decision-filter bound (knf_api.cu filter_delta)
+  bool filter_skip = true;             // certified (Lipschitz) skipping inside the filter; KNF_FILTER_SKIP=0 disables
   int filter_mode = 2;                 // decision filter of the exact march: 0 off, 1 on, 2 auto (probe the first wavefront)
   int precision = 0;                  // KNF_PRECISION_*: which SDF tile kernels run
   Workspace ws;

@@ -30,8 +30,9 @@ struct MarchTileArgs {
   int* live_out;            // ... of `next`
   int* live_filter;         // ... of `next_filter`
   int* live_defer;          // ... of `defer`
-  unsigned long long* eval_counter;  // statistics: [0] SDF evaluations, [2] lane slots, [4] filter evaluations, [5] deferred
+  unsigned long long* eval_counter;  // statistics: [0] SDF evaluations, [2] lane slots, [4] filter evaluations, [5] deferred, [6] certified skips
   int max_inner;            // cap on consecutive in-place steps of one tile
+  int max_skip;             // filter kernel: 0 disables certified skipping
   double crawl_below;       // exact kernels: a march step from a distance below this continues in the filter queue (-inf: never)
 };
 
@@ -175,10 +176,10 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(M
 //   converges after filtered steps re-evaluates d_prev exactly first (PH_RECHECK).  Results are bit-identical to
 //   running the exact kernel on every sample (tests/test_gpu_march.py::test_decision_filter_is_exact).
 template <int PC, bool FILTER>
-static __global__ void __launch_bounds__(32, kMmaCtasPerSm) march_mma_kernel(MarchTileArgs A) {
+static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_kernel(MarchTileArgs A) {
   using Blob = MmaBlobT<PC>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  MmaSmemT<PC>& S = *reinterpret_cast<MmaSmemT<PC>*>(smem_raw);
+  MmaMarchSmemT<PC>& S = *reinterpret_cast<MmaMarchSmemT<PC>*>(smem_raw);
   const int lane = threadIdx.x, g = lane >> 2, t = lane & 3;
   if (lane == 0) {
     mbar_init(&S.bar, 1);
@@ -189,7 +190,7 @@ static __global__ void __launch_bounds__(32, kMmaCtasPerSm) march_mma_kernel(Mar
   const int n_tiles = P.ctr->n_tiles;
   const uint32_t* blobs = reinterpret_cast<const uint32_t*>(P.blobs);
   uint32_t parity = 0;
-  unsigned long long evals = 0, slots = 0, deferred = 0;
+  unsigned long long evals = 0, slots = 0, deferred = 0, skipped = 0;
 
   for (;;) {
     const int tix = next_tile(P.ctr, lane);
@@ -213,6 +214,11 @@ static __global__ void __launch_bounds__(32, kMmaCtasPerSm) march_mma_kernel(Mar
         float4 pt = P.req_pt[slot];
         px[q] = pt.x; py[q] = pt.y; pz[q] = pt.z;
         ray_load(rr[q], A.M, ray[q]);
+#pragma unroll
+        for (int a = 0; a < 3; a++) {  // origin and direction live in shared memory during the visit (own slots only)
+          S.od[a][pidx[q]] = rr[q].o[a];
+          S.od[3 + a][pidx[q]] = rr[q].d[a];
+        }
       }
     }
     float in_lo[3], in_hi[3];
@@ -228,7 +234,7 @@ static __global__ void __launch_bounds__(32, kMmaCtasPerSm) march_mma_kernel(Mar
     }
     int n_active = tile.count;
     const float* W3t = reinterpret_cast<const float*>(S.w + Blob::w3);
-    double safe_below = 0.0;
+    double safe_below = 0.0, inv_lip = 0.0;
 
     for (int inner = 0;; inner++) {
 #pragma unroll
@@ -243,18 +249,33 @@ static __global__ void __launch_bounds__(32, kMmaCtasPerSm) march_mma_kernel(Mar
       if (inner == 0) {
         mbar_wait(&S.bar, parity);
         parity ^= 1;
-        if (FILTER) safe_below = -(A.M.eps + (double)reinterpret_cast<const float*>(S.w + Blob::b3)[kFilterDeltaSlot]);
+        if (FILTER) {
+          safe_below = -(A.M.eps + (double)reinterpret_cast<const float*>(S.w + Blob::b3)[kFilterDeltaSlot]);
+          inv_lip = A.max_skip > 0 ? 1.0 / (double)reinterpret_cast<const float*>(S.w + Blob::b3)[kFilterLipSlot] : 0.0;
+        }
       }
       const float b3 = reinterpret_cast<const float*>(S.w + Blob::b3)[0];
       float2 dist = make_float2(0.f, 0.f);
+      // software pipeline over the active m-tiles: the (serial, FMA-pipe) Fourier recurrence of the next m-tile is
+      // issued alongside the HMMAs of the current one
+      unsigned todo = 0;
+#pragma unroll
+      for (int m = 0; m < 4; m++) todo |= (act_mask & (0x11111111u << m)) ? (1u << m) : 0u;
+      float2 v[12];
+      if (todo) mma_encode<PC>(S, __ffs(todo) - 1, lane, v);
 #pragma unroll 1
-      for (int m = 0; m < 4; m++) {
-        if ((act_mask & (0x11111111u << m)) == 0) continue;
+      while (todo) {
+        const int m = __ffs(todo) - 1;
+        todo &= todo - 1;
+        float2 vn[12];
+        if (todo) mma_encode<PC>(S, __ffs(todo) - 1, lane, vn);
         float h2[4][4];
-        mma_hidden<PC, FILTER>(S, m, lane, h2);
+        mma_hidden_from<PC, FILTER>(S, v, lane, h2);
         const float2 d = mma_output(h2, W3t, b3, t, 0);
         if (m == t) dist = d;
         slots += 16;
+#pragma unroll
+        for (int i = 0; i < 12; i++) v[i] = vn[i];
       }
       evals += (lane == 0) ? (unsigned long long)n_active : 0ull;
 
@@ -271,12 +292,36 @@ static __global__ void __launch_bounds__(32, kMmaCtasPerSm) march_mma_kernel(Mar
           if (FILTER && code[q] == STEP_EXACT) {
             cell[q] = tile.cell;  // undecided: the same sample goes to the exact queue of this wavefront
           } else if (code[q] != STEP_DONE) {
-            px[q] = __double2float_rn(rr[q].o[0] + t_next * rr[q].d[0]);
-            py[q] = __double2float_rn(rr[q].o[1] + t_next * rr[q].d[1]);
-            pz[q] = __double2float_rn(rr[q].o[2] + t_next * rr[q].d[2]);
-            const bool well_inside = px[q] > in_lo[0] && px[q] < in_hi[0] && py[q] > in_lo[1] && py[q] < in_hi[1] &&
-                                     pz[q] > in_lo[2] && pz[q] < in_hi[2];
-            cell[q] = well_inside ? tile.cell : cell_of(px[q], py[q], pz[q], A.G);
+            const float x0 = px[q], y0 = py[q], z0 = pz[q];  // where d_f was evaluated
+            // |d(p) - d(p0)| <= L |p - p0| inside the cell (L: proven Lipschitz bound of the cell's network), so every
+            // sample within `reach` of p0 still has an exact distance below -eps: the reference's evaluation there can
+            // only say "keep crawling", and its step is taken without evaluating (certified skip).
+            const double reach = FILTER ? (safe_below - (double)(q ? dist.y : dist.x)) * inv_lip : 0.0;
+            for (;;) {
+              px[q] = __double2float_rn(S.od[0][pidx[q]] + t_next * S.od[3][pidx[q]]);
+              py[q] = __double2float_rn(S.od[1][pidx[q]] + t_next * S.od[4][pidx[q]]);
+              pz[q] = __double2float_rn(S.od[2][pidx[q]] + t_next * S.od[5][pidx[q]]);
+              const bool well_inside = px[q] > in_lo[0] && px[q] < in_hi[0] && py[q] > in_lo[1] && py[q] < in_hi[1] &&
+                                       pz[q] > in_lo[2] && pz[q] < in_hi[2];
+              cell[q] = well_inside ? tile.cell : cell_of(px[q], py[q], pz[q], A.G);
+              if (!FILTER || !well_inside) break;
+              const float dx = px[q] - x0, dy = py[q] - y0, dz = pz[q] - z0;
+              const float far = sqrtf(dx * dx + dy * dy + dz * dz);
+              if (!((double)far * 1.00001 + 1e-6 < reach)) break;
+              // the reference's march step at t_next (surface.py:217-223) with max(d, eps/2) = eps/2
+              rr[q].steps += 1;
+              rr[q].t_prev = rr[q].t;
+              rr[q].t = rr[q].t + A.M.step_scale * (A.M.eps / 2);
+              skipped += 1;
+              if (rr[q].t > rr[q].t_far || rr[q].steps >= A.M.max_steps) {
+                A.M.phase[ray[q]] = PH_DONE;
+                A.M.steps[ray[q]] = rr[q].steps;
+                code[q] = STEP_DONE;
+                cell[q] = -1;
+                break;
+              }
+              t_next = rr[q].t;
+            }
           }
         }
         // rays that keep this kernel's kind of evaluation and stay in the cell may step in place
@@ -307,11 +352,17 @@ static __global__ void __launch_bounds__(32, kMmaCtasPerSm) march_mma_kernel(Mar
   if (A.eval_counter) {
     if (FILTER) {
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) deferred += __shfl_xor_sync(0xffffffffu, deferred, off);
+      for (int off = 16; off > 0; off >>= 1) {
+        deferred += __shfl_xor_sync(0xffffffffu, deferred, off);
+        skipped += __shfl_xor_sync(0xffffffffu, skipped, off);
+      }
     }
     if (lane == 0 && evals) {
       atomicAdd(A.eval_counter + (FILTER ? 4 : 0), evals);
-      if (FILTER) atomicAdd(A.eval_counter + 5, deferred);
+      if (FILTER) {
+        atomicAdd(A.eval_counter + 5, deferred);
+        atomicAdd(A.eval_counter + 6, skipped);
+      }
       else atomicAdd(A.eval_counter + 2, slots);
     }
   }

@@ -37,8 +37,8 @@ namespace knf {
 // ---- per-cell blob for the MMA path -------------------------------------------------------------
 // P = pieces per operand: 3 -> bf16 x 3 (exact split, six products), 2 -> fp16 x 2 (22-23 significand bits, the
 // second piece scaled by 2^11 to stay normal, three products).
-//   frag1[kt 0..2][nt 0..3][piece 0..P-1][lane 0..31] uint2   B fragments of W1 (K order permuted, see mma_feature_of)
-//   frag2[kt 0..1][nt 0..3][piece 0..P-1][lane 0..31] uint2   B fragments of W2
+//   frag1[kt 0..2][nt 0..3][lane 0..31][piece 0..P-1] uint2   B fragments of W1 (K order permuted, see mma_feature_of)
+//   frag2[kt 0..1][nt 0..3][lane 0..31][piece 0..P-1] uint2   B fragments of W2   (P = 2: one LDS.128 per lane)
 //   b1[32] b2[32] fp32 | W3t[32][12] fp32 (k-major, like BlobLayout) | b3[12] fp32
 template <int P>
 struct MmaBlobT {
@@ -57,6 +57,7 @@ struct MmaBlobT {
 using MmaBlob = MmaBlobT<3>;
 using MmaBlobH = MmaBlobT<2>;
 constexpr int kFilterDeltaSlot = kSdfOutPad - 1;  // b3[11]: proven bound on |tensor distance - exact distance| in this cell
+constexpr int kFilterLipSlot = kSdfOutPad - 2;    // b3[10]: proven Lipschitz bound of the cell's distance network
 constexpr float kHalfPieceScale = 2048.0f;  // 2^11: the fp16 second piece carries (x - x1) * 2^11
 
 // Which reference feature (nn.fourier_encode column, nn.py:84-93) sits at position `kslot` of k-tile
@@ -76,6 +77,12 @@ struct MmaSmemT {
   alignas(16) float pts[3][72];  // coordinate exchange: pts[axis][point], stride 72 keeps the quad reads conflict-free
   int slot[64];                  // batched-forward kernel: request slot of every tile point
   alignas(8) uint64_t bar;
+};
+// The march kernels also park the resident rays' origins and directions here (k-major: conflict-free 8-byte
+// accesses) instead of in 48 registers per lane, which is what lets 13 one-warp CTAs share an SM.
+template <int P>
+struct MmaMarchSmemT : MmaSmemT<P> {
+  alignas(16) double od[6][64];
 };
 
 // ---- device helpers -------------------------------------------------------------------------------
@@ -132,7 +139,7 @@ __device__ __forceinline__ void make_a(APieces<P>& A, float2 v0, float2 v1, floa
 //   P = 3: small += x3w1 + x1w3 + x2w2 + x2w1 + x1w2 ; big += x1w1          (pre-activation = big + small)
 //   P = 2: small += x2'w1 + x1w2'                    ; big += x1w1          (pre-activation = big + small / 2^11)
 template <int P, int KT>
-__device__ __forceinline__ void mma_layer(const APieces<P> (&A)[KT], const uint2* __restrict__ frag /* [kt][nt][piece][lane] */,
+__device__ __forceinline__ void mma_layer(const APieces<P> (&A)[KT], const uint2* __restrict__ frag /* [kt][nt][lane][piece] */,
                                           int lane, float (&small)[4][4], float (&big)[4][4]) {
 #pragma unroll
   for (int nt = 0; nt < 4; nt++)
@@ -142,9 +149,17 @@ __device__ __forceinline__ void mma_layer(const APieces<P> (&A)[KT], const uint2
   for (int kt = 0; kt < KT; kt++) {
     uint2 w[4][P];
 #pragma unroll
-    for (int nt = 0; nt < 4; nt++)
+    for (int nt = 0; nt < 4; nt++) {
+      const uint2* f = frag + ((kt * 4 + nt) * 32 + lane) * P;
+      if (P == 2) {
+        const uint4 q = *reinterpret_cast<const uint4*>(f);
+        w[nt][0] = make_uint2(q.x, q.y);
+        w[nt][1] = make_uint2(q.z, q.w);
+      } else {
 #pragma unroll
-      for (int pc = 0; pc < P; pc++) w[nt][pc] = frag[((kt * 4 + nt) * P + pc) * 32 + lane];
+        for (int pc = 0; pc < P; pc++) w[nt][pc] = f[pc];
+      }
+    }
     if (P == 3) {
 #pragma unroll
       for (int nt = 0; nt < 4; nt++) hmma<P>(small[nt], A[kt].p[P - 1], w[nt][0]);
@@ -156,9 +171,9 @@ __device__ __forceinline__ void mma_layer(const APieces<P> (&A)[KT], const uint2
 #pragma unroll
     for (int nt = 0; nt < 4; nt++) hmma<P>(small[nt], A[kt].p[1], w[nt][0]);
 #pragma unroll
-    for (int nt = 0; nt < 4; nt++) hmma<P>(small[nt], A[kt].p[0], w[nt][1]);
+    for (int nt = 0; nt < 4; nt++) hmma<P>(big[nt], A[kt].p[0], w[nt][0]);  // between the two small products: an accumulator is revisited every 8th HMMA
 #pragma unroll
-    for (int nt = 0; nt < 4; nt++) hmma<P>(big[nt], A[kt].p[0], w[nt][0]);
+    for (int nt = 0; nt < 4; nt++) hmma<P>(small[nt], A[kt].p[0], w[nt][1]);
   }
 }
 
@@ -185,50 +200,54 @@ __device__ __forceinline__ void finish_hidden(const float (&small)[4][4], const 
   }
 }
 
-// Hidden activations h2 (after both softplus layers) of m-tile `m` of the warp's 64 points, in accumulator
-// layout: h2[nt][0..1] = row g, columns 8nt+2t, +1 ; h2[nt][2..3] = row g+8.  Coordinates come from S.pts.
-template <int P, bool FAST>
-__device__ __forceinline__ void mma_hidden(const MmaSmemT<P>& S, int m, int lane, float (&h2)[4][4]) {
-  using Blob = MmaBlobT<P>;
+// First-layer inputs of m-tile `m` of the warp's 64 points, as the lane's A-fragment values: v[i] = (row g, row g+8)
+// of the lane's i-th input (k-tile major).  Lane t < 3 runs nn.fourier_encode's recurrence for axis t of its two
+// rows; lane t = 3 carries the raw coordinates.  Coordinates come from S.pts.
+template <int P>
+__device__ __forceinline__ void mma_encode(const MmaSmemT<P>& S, int m, int lane, float2 (&v)[12]) {
   const int g = lane >> 2, t = lane & 3;
   const float pi_f = 3.14159274101257324e+00f;  // float32(np.pi)
-  // ---- first-layer inputs of rows g, g+8: twelve values each, k-tile major ------------------------------
-  float v[2][12];
   const int p0 = 16 * m + g;
   if (t < 3) {
+    const float2 c = make_float2(S.pts[t][p0], S.pts[t][p0 + 8]);
+    const float2 a = __fmul2_rn(make_float2(pi_f, pi_f), c);
+    float2 s, co;
+    np_sincosf(a.x, s.x, co.x);
+    np_sincosf(a.y, s.y, co.y);
 #pragma unroll
-    for (int r = 0; r < 2; r++) {
-      const float c = S.pts[t][p0 + 8 * r];
-      float s, co;
-      np_sincosf(__fmul_rn(pi_f, c), s, co);
-#pragma unroll
-      for (int o = 0; o < kSdfFreqs; o++) {
-        v[r][2 * o] = s;
-        v[r][2 * o + 1] = co;
-        const float two_s = __fmul_rn(2.0f, s);
-        const float ns = __fmul_rn(two_s, co);                    // 2 s c      (nn.py:88-92)
-        const float nc = __fsub_rn(1.0f, __fmul_rn(two_s, s));    // 1 - 2 s s
+    for (int o = 0; o < kSdfFreqs; o++) {
+      v[2 * o] = s;
+      v[2 * o + 1] = co;
+      if (o + 1 < kSdfFreqs) {
+        const float2 two_s = __fmul2_rn(make_float2(2.0f, 2.0f), s);
+        const float2 ns = __fmul2_rn(two_s, co);                                                       // 2 s c      (nn.py:88-92)
+        const float2 ss = __fmul2_rn(two_s, s);
+        co = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-ss.x, -ss.y));                           // 1 - 2 s s
         s = ns;
-        co = nc;
       }
     }
   } else {
 #pragma unroll
-    for (int r = 0; r < 2; r++) {
-#pragma unroll
-      for (int i = 0; i < 12; i++) v[r][i] = 0.0f;
-      v[r][0] = S.pts[0][p0 + 8 * r];
-      v[r][1] = S.pts[1][p0 + 8 * r];
-      v[r][2] = S.pts[2][p0 + 8 * r];
-    }
+    for (int i = 0; i < 12; i++) v[i] = make_float2(0.0f, 0.0f);
+    v[0] = make_float2(S.pts[0][p0], S.pts[0][p0 + 8]);
+    v[1] = make_float2(S.pts[1][p0], S.pts[1][p0 + 8]);
+    v[2] = make_float2(S.pts[2][p0], S.pts[2][p0 + 8]);
   }
+}
+
+// Hidden activations h2 (after both softplus layers) of one m-tile from its encoded inputs, in accumulator layout:
+// h2[nt][0..1] = row g, columns 8nt+2t, +1 ; h2[nt][2..3] = row g+8.
+template <int P, bool FAST>
+__device__ __forceinline__ void mma_hidden_from(const MmaSmemT<P>& S, const float2 (&v)[12], int lane, float (&h2)[4][4]) {
+  using Blob = MmaBlobT<P>;
+  const int t = lane & 3;
   float h1[4][4], small[4][4], big[4][4];
   {
     APieces<P> A[Blob::kt1];
 #pragma unroll
     for (int kt = 0; kt < Blob::kt1; kt++)
-      make_a<P>(A[kt], make_float2(v[0][4 * kt], v[0][4 * kt + 1]), make_float2(v[1][4 * kt], v[1][4 * kt + 1]),
-                make_float2(v[0][4 * kt + 2], v[0][4 * kt + 3]), make_float2(v[1][4 * kt + 2], v[1][4 * kt + 3]));
+      make_a<P>(A[kt], make_float2(v[4 * kt].x, v[4 * kt + 1].x), make_float2(v[4 * kt].y, v[4 * kt + 1].y),
+                make_float2(v[4 * kt + 2].x, v[4 * kt + 3].x), make_float2(v[4 * kt + 2].y, v[4 * kt + 3].y));
     mma_layer<P, Blob::kt1>(A, reinterpret_cast<const uint2*>(S.w + Blob::frag1), lane, small, big);
   }
   finish_hidden<P, FAST>(small, big, reinterpret_cast<const float*>(S.w + Blob::b1), t, h1);
@@ -242,6 +261,13 @@ __device__ __forceinline__ void mma_hidden(const MmaSmemT<P>& S, int m, int lane
     mma_layer<P, Blob::kt2>(A, reinterpret_cast<const uint2*>(S.w + Blob::frag2), lane, small, big);
   }
   finish_hidden<P, FAST>(small, big, reinterpret_cast<const float*>(S.w + Blob::b2), t, h2);
+}
+
+template <int P, bool FAST>
+__device__ __forceinline__ void mma_hidden(const MmaSmemT<P>& S, int m, int lane, float (&h2)[4][4]) {
+  float2 v[12];
+  mma_encode<P>(S, m, lane, v);
+  mma_hidden_from<P, FAST>(S, v, lane, h2);
 }
 
 // Output column j of the 32 -> N3 layer for rows g (.x) and g+8 (.y): the lane's eight hidden units first
@@ -274,6 +300,12 @@ __device__ __forceinline__ void fetch_mma_weights(MmaSmemT<P>& S, const uint32_t
 #define KNF_MMA_CTAS_PER_SM 12
 #endif
 constexpr int kMmaCtasPerSm = KNF_MMA_CTAS_PER_SM;
+#ifndef KNF_FILTER_CTAS_PER_SM
+#define KNF_FILTER_CTAS_PER_SM 12
+#endif
+// one-warp CTAs per SM of the march kernels: P = 3 is bound by its 21 KB of shared memory, P = 2 by 16 KB
+template <int P>
+constexpr int march_ctas_per_sm() { return P == 2 ? KNF_FILTER_CTAS_PER_SM : 10; }
 
 // ---- batched forward (grid.sdf_query, shading probes) ---------------------------------------------------
 // Tile point p is owned by lane (g = p % 8 ... ) : point 16 t + g (+ 8): lane 4 g + t.

@@ -17,7 +17,7 @@ for name, field in (("random_init_16", grid.field_init(grid.GridConfig(resolutio
         fs.dev.reset_stats()
         frames[mode] = surface.render_frame(fs, orbit_view(3, W, H))
         st = fs.dev.stats()
-        print(" ", mode, "hits", int(frames[mode].hit.sum()), "exact evals", st["sdf_evals"], "filter evals", st["filter_evals"], "deferred", st["filter_deferred"],
+        print(" ", mode, "hits", int(frames[mode].hit.sum()), "exact evals", st["sdf_evals"], "filter evals", st["filter_evals"], "deferred", st["filter_deferred"], "skipped", st["filter_skipped"],
               "wavefronts", st["wavefronts"], "launches", st["kernel_launches"], flush=True)
     for mode in ("on", "auto"):
         same = all(np.array_equal(getattr(frames["off"], k), getattr(frames[mode], k)) for k in ("color", "depth", "normal", "hit"))
