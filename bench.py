@@ -317,16 +317,51 @@ def main():
         e2e_fps = args.steps * world / e2e_s
         ck = clocks.summary()
         ffma_peak = SM_COUNT * FFMA_LANES_PER_SM * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
-        mlp_tflops = stats["sdf_evals"] * FLOP_PER_SDF_EVAL / (stats["sdf_mlp_ms"] * 1e-3) / 1e12 if stats["sdf_mlp_ms"] > 0 else None
+        tensor_peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0)))
+        exact_tflops = stats["sdf_evals"] * FLOP_PER_SDF_EVAL / (stats["sdf_mlp_ms"] * 1e-3) / 1e12 if stats["sdf_mlp_ms"] > 0 else None
+        filter_tflops = stats["filter_evals"] * FLOP_PER_SDF_EVAL / (stats["filter_ms"] * 1e-3) / 1e12 if stats["filter_ms"] > 0 else None
         route_bytes = stats["march_routed_requests"] * ROUTE_BYTES_PER_REQUEST + stats["wavefronts"] * 4096 * ROUTE_BYTES_PER_CELL + stats["rays"] * 100
         route_gbs = route_bytes / (stats["route_ms"] * 1e-3) / 1e9 if stats["route_ms"] > 0 else None
+        # what the reference evaluates for the same frames: every crawl step the filter decided or certified counts once
+        ref_evals = stats["sdf_evals"] + stats["filter_evals"] - stats["filter_deferred"] + stats["filter_skipped"]
+        roof_exact = {
+            "kernel": "march_warp_kernel / mlp_warp_kernel (fused encode + 3-layer SDF MLP as k-ordered fp32 FMA chains + NumPy-exact softplus + sphere-trace step)",
+            "bound": "fp32", "achieved": exact_tflops, "peak": ffma_peak, "unit": "TFLOP/s", "frac": (exact_tflops / ffma_peak) if exact_tflops else None,
+            "peak_source": f"derived: {SM_COUNT} SMs x {FFMA_LANES_PER_SM} FFMA lanes x 2 x sm_max_mhz ({peak_src} MEASURED_PEAKS.json holds HBM and bf16-tensor "
+                           "peaks only); measured attainable FP32 rates on this pool: 71.0 TFLOP/s packed FFMA2, 52.0 with one LDS.128 per 16 FFMA2 (profiles/ffma_peak_micro_r1.txt)",
+            "evals": int(stats["sdf_evals"]), "launches": int(stats["sdf_mlp_launches"]), "avg_launch_ms": stats["sdf_mlp_ms"] / max(stats["sdf_mlp_launches"], 1),
+            "share_of_step": stats["sdf_mlp_ms"] / ms, "tile_fill": stats["sdf_evals"] / max(stats["march_lane_slots"], 1),
+            "note": "after the decision filter only ~4 % of the evaluations reach this kernel, in sparse tiles (tile_fill): achieved counts useful evaluations only",
+        }
+        roof_filter = {
+            "kernel": "march_mma_kernel<2, filter> (decision filter: Fourier recurrence + fp16x2 split mma.sync.m16n8k16 layers chained in registers + MUFU softplus "
+                      "+ sphere-trace crawl step + certified skipping)",
+            "bound": "tensor", "achieved": filter_tflops, "peak": tensor_peak, "unit": "TFLOP/s", "frac": (filter_tflops / tensor_peak) if filter_tflops else None,
+            "traffic": 242.5e6,
+            "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of ONE dense filter launch (0.81 ms, ~9 M evaluations) from profiles/ncu_r1_filter_v1 "
+                            "(ncu --set full); weights (49 MB of fp16 fragments) and ray state are L2-resident, DRAM is 3.7 % busy",
+            "peak_source": f"{peak_src} MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS, tcgen05 path); mma.sync (HMMA.16816) issue peak measured on this pool: "
+                           "553 TFLOP/s (profiles/hmma_split_r1.txt)",
+            "algorithmic_flop_per_launch": stats["filter_evals"] * FLOP_PER_SDF_EVAL / max(stats["filter_launches"], 1),
+            "avg_launch_ms": stats["filter_ms"] / max(stats["filter_launches"], 1), "launches": int(stats["filter_launches"]),
+            "share_of_step": stats["filter_ms"] / ms,
+            "hmma_flop_per_eval": 15360,
+            "hmma_issued_tflops": (stats["filter_evals"] * 15360 / (stats["filter_ms"] * 1e-3) / 1e12) if stats["filter_ms"] > 0 else None,
+            "note": "achieved = filter evaluations x 5120 algorithmic flop; each evaluation issues 3 fp16 piece products over K padded to 48 + 32 "
+                    "(15360 tensor flop).  The kernel is co-limited by issue slots (57 %), the MUFU pipe (45 %) and the tensor pipe (38 %), see profiles/",
+        }
+        dominant = roof_filter if stats["filter_ms"] >= stats["sdf_mlp_ms"] else roof_exact
         line = {
             "metric": f"fps_{W}x{H}_sphere_traced", "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload_config(W, H, world),
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": dict(workload_config(W, H, world), precision=fs.dev.get_precision(),
+                                                                                     decision_filter="auto (results bit-identical to filter off)"),
             "mrays_per_s": fps * W * H / 1e6,
-            "sdf_evals_per_s": stats["sdf_evals"] * world / (ms / 1e3),
-            "sdf_evals_per_ray": stats["sdf_evals"] / max(stats["rays"], 1),
+            "sdf_evals_per_s": ref_evals * world / (ms / 1e3),
+            "sdf_evals_per_ray": ref_evals / max(stats["rays"], 1),
+            "sdf_evals_breakdown": {"exact_fp32_chain": int(stats["sdf_evals"]), "filter_tensor": int(stats["filter_evals"]),
+                                    "filter_undecided_re_evaluated": int(stats["filter_deferred"]), "certified_without_evaluation": int(stats["filter_skipped"]),
+                                    "note": "sdf_evals_per_s / per_ray count what the reference evaluates for these frames (exact + filter - undecided + certified)"},
             "hit_fraction": stats["hits"] / max(stats["rays"], 1),
             "clocks": ck,
             "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": 160 * world,
@@ -334,26 +369,13 @@ def main():
                     "note": "surface.render_frame-equivalent C-ABI call (KNF_MEM_HOST) into pinned host buffers; the only "
                             "per-step input is the camera/settings structs, the field is uploaded once like the reference loads it once"},
             "gpu_launches": int(stats["kernel_launches"]),
-            "roofline": {
-                "kernel": "march_warp_kernel (fused encode + 3-layer SDF MLP + sphere-trace step, tile residency)", "bound": "fp32",
-                "achieved": mlp_tflops, "peak": ffma_peak, "unit": "TFLOP/s", "frac": (mlp_tflops / ffma_peak) if mlp_tflops else None,
-                "traffic": 257.4e6,
-                "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of ONE dense wavefront launch (2.0 ms, ~9.6 M evaluations) from "
-                                "profiles/ncu_r1_march_v6 (ncu --set full); weights (45 MB) and ray state are L2-resident, DRAM is 1.3 % busy",
-                "peak_source": f"derived: {SM_COUNT} SMs x {FFMA_LANES_PER_SM} FFMA lanes x 2 x sm_max_mhz ({peak_src} MEASURED_PEAKS.json holds "
-                               "HBM and bf16-tensor peaks only; this kernel is an FP32 FFMA kernel, see DESIGN.md)",
-                "algorithmic_flop_per_launch": stats["sdf_evals"] * FLOP_PER_SDF_EVAL / max(stats["sdf_mlp_launches"], 1),
-                "avg_launch_ms": stats["sdf_mlp_ms"] / max(stats["sdf_mlp_launches"], 1), "launches": int(stats["sdf_mlp_launches"]),
-                "share_of_step": stats["sdf_mlp_ms"] / ms,
-                "frac_of_measured_bf16_tensor_peak": (mlp_tflops / float(peaks["bf16_tflops"])) if mlp_tflops else None,
-                "measured_fp32_rates_tflops": {"packed_FFMA2_registers_only": 71.0, "scalar_FFMA": 61.6, "FFMA2_with_1_LDS128_per_16": 52.0,
-                                               "source": "profiles/ffma_peak_micro_r1.txt (scripts/micro/ffma_peak.cu on this pool's B200)"},
-                "tile_fill": stats["sdf_evals"] / max(stats["march_lane_slots"], 1),
-            },
+            "roofline": dominant,
+            "roofline_exact": roof_exact,
+            "roofline_filter": roof_filter,
             "roofline_route": {
                 "kernel": "march_init (emit) / route_scan / route_scatter", "bound": "hbm", "achieved": route_gbs,
                 "algorithmic_bytes": "16.25 B per routed request + 16 B per cell per wavefront + 100 B per ray (init: t_near/t_far/o/d read, state + request written)",
-                "routed_fraction_of_march_evals": stats["march_routed_requests"] / max(stats["sdf_evals"], 1),
+                "routed_fraction_of_march_evals": stats["march_routed_requests"] / max(ref_evals, 1),
                 "peak": float(peaks["hbm_gbs"]), "unit": "GB/s", "frac": (route_gbs / float(peaks["hbm_gbs"])) if route_gbs else None,
                 "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs", "share_of_step": stats["route_ms"] / ms,
                 "launches": int(stats["route_launches"]),

@@ -239,3 +239,66 @@ def test_reference_tracer_accepts_gpu_surface(S, distilled_field, distilled_orac
     assert (a.hit == b.hit).mean() >= 0.999
     both = a.hit & b.hit
     assert (np.abs(a.t[both] - b.t[both]) <= 1e-4).mean() >= 0.995
+
+
+def test_decision_filter_is_exact(S, cams, distilled_field):
+    """The decision filter (tensor-core predicate + certified skipping, include/knf_b200.h knf_field_set_filter) may
+    only change WHICH kernel looks at a sample, never a result: frames and march outputs with the filter forced on
+    must equal the filter-off ones bit for bit, on the chaotic random-init field (98 % of evaluations filtered) and
+    on a real surface (nothing to filter)."""
+    from paper_2206_10885_b200 import grid
+
+    for name, field, size in (("random-init 16^3", grid.field_init(grid.GridConfig(resolution=16), seed=0), 160),
+                              ("distilled 4^3", distilled_field, 96)):
+        fs = S.FieldSurface(field)
+        pose = cams.look_at_pose((0.3, 0.4, 2.4), (0, 0, 0), (0, 1, 0), np.deg2rad(40), size, size)
+        o, d, tn, tf = _rays(size // 2, size // 2)
+        out = {}
+        try:
+            for mode in ("off", "on", "auto"):
+                fs.dev.set_filter(mode)
+                fs.dev.reset_stats()
+                fb = S.render_frame(fs, pose)
+                st = fs.dev.stats()
+                out[mode] = (fb, S.march_rays(fs, o, d, tn, tf, S.RenderSettings()), st)
+        finally:
+            fs.dev.set_filter("auto")
+        fb0, m0, st0 = out["off"]
+        assert st0["filter_evals"] == 0 and st0["filter_skipped"] == 0
+        for mode in ("on", "auto"):
+            fb, m, st = out[mode]
+            for k in ("color", "depth", "normal", "hit"):
+                assert np.array_equal(getattr(fb, k), getattr(fb0, k)), (name, mode, k)
+            assert np.array_equal(m.hit, m0.hit) and np.array_equal(m.t, m0.t) and np.array_equal(m.steps, m0.steps)
+            assert np.array_equal(m.position, m0.position)
+        st = out["on"][2]
+        print(f"{name}: filter on -> exact {st['sdf_evals']}, filter {st['filter_evals']}, undecided {st['filter_deferred']}, "
+              f"certified {st['filter_skipped']} (delta {fs.dev.filter_delta():.3g}); off -> exact {st0['sdf_evals']}")
+        if name.startswith("random"):
+            assert st["filter_evals"] > 5 * st["sdf_evals"]  # the filter carries the crawl
+            assert out["auto"][2]["filter_evals"] > 0
+        else:
+            assert out["auto"][2]["filter_evals"] == 0        # auto switches itself off on a real surface
+    with pytest.raises(ValueError):
+        fs.dev.set_filter(5)
+
+
+def test_frame_random_init_256_parity(S, cams):
+    """BASELINE config 1 at full size (256^2, random-init 16^3, the cmd_bench camera) against the oracle run on this
+    host: north_star bars -- hit masks >= 99.9 %, depth 1e-4, normals / RGB 1e-3 on the both-hit pixels."""
+    from paper_2206_10885_b200 import grid
+
+    field = grid.field_init(grid.GridConfig(resolution=16), seed=0)
+    pose = cams.look_at_pose((0, 0, 2.5), (0, 0, 0), (0, 1, 0), np.deg2rad(40), 256, 256)
+    ocam = oracle.camera_look_at((0, 0, 2.5), (0, 0, 0), (0, 1, 0), np.deg2rad(40), 256, 256)
+    ref = oracle.render(oracle.FieldTraceable(oracle_from_product(field)), ocam, oracle.MarchSettings())
+    fb = S.render_frame(S.FieldSurface(field), pose)
+    agree = (fb.hit == ref.hit).mean()
+    both = fb.hit & ref.hit
+    rel = np.abs(fb.depth[both] - ref.depth[both]) / ref.depth[both]
+    nerr = np.abs(fb.normal - ref.normal)[both].max(axis=1)
+    cerr = np.abs(fb.color - ref.color)[both].max(axis=1)
+    print(f"256^2 random-init: hit agreement {agree:.4%} ({int((fb.hit != ref.hit).sum())} flips), depth<=1e-4 {np.mean(rel <= 1e-4):.4%}, "
+          f"normal<=1e-3 {np.mean(nerr <= 1e-3):.4%}, rgb<=1e-3 {np.mean(cerr <= 1e-3):.4%}")
+    assert agree >= 0.999
+    assert np.mean(rel <= 1e-4) >= 0.999 and np.mean(nerr <= 1e-3) >= 0.995 and np.mean(cerr <= 1e-3) >= 0.999

@@ -5,6 +5,8 @@ generated the fixtures; elsewhere OpenBLAS/NumPy SIMD dispatch may move the last
 assertions use 2e-6 (the reference's own grouped-vs-naive tolerance is 1e-6, test_grid.py:81-86).
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -142,3 +144,47 @@ def test_volume_forward(distilled_oracle):
     assert np.abs(col - g["colors"]).max() <= 1e-6
     col = oracle.volume_forward(distilled_oracle, g["origins"], g["dirs"], 16, None, (0.2, 0.4, 0.6), s=float(g["s"]))
     assert np.abs(col - g["colors_nojitter"]).max() <= 1e-6
+
+
+def _np_softplus_lib():
+    import ctypes
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    so = os.path.join(root, "oracle", "_build", "libnp_softplus.so")
+    if not os.path.exists(so):
+        os.makedirs(os.path.dirname(so), exist_ok=True)
+        subprocess.run(["gcc", "-O2", "-mfma", "-ffp-contract=off", "-shared", "-fPIC", "-o", so, os.path.join(root, "oracle", "np_softplus.c"), "-lm"], check=True)
+    return ctypes.CDLL(so)
+
+
+def test_softplus_restatement_bit_exact():
+    """oracle/np_softplus.c restates NumPy's float32 exp (a NumPy source loop) and log1p (Intel SVML, third party,
+    pinned to the installed numpy binary) operation for operation; the device routine softplus_np_f2xN follows it.
+    On an AVX-512 host NumPy dispatches exactly those routines and the restatement must match bit for bit; the
+    committed golden vector (generated by the reference on the build host) is checked on every host."""
+    import ctypes
+
+    lib = _np_softplus_lib()
+
+    def run(name, x):
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        y = np.empty_like(x)
+        getattr(lib, name)(x.ctypes.data_as(ctypes.c_void_p), y.ctypes.data_as(ctypes.c_void_p), ctypes.c_long(x.size))
+        return y
+
+    g = golden("encode_act.npz")
+    assert np.array_equal(run("knf_np_softplus", g["z"].ravel()).reshape(g["z"].shape), g["softplus"])
+    try:
+        from numpy._core._multiarray_umath import __cpu_features__ as feats
+    except Exception:  # pragma: no cover
+        feats = {}
+    if not feats.get("AVX512_SKX", False):
+        pytest.skip("NumPy on this host does not dispatch the AVX-512 SVML log1p; the golden-vector half ran")
+    rng = np.random.default_rng(11)
+    x = np.concatenate([rng.normal(0, 1.5, 1_000_000), rng.normal(0, 6, 500_000), rng.uniform(-40, 40, 250_000)]).astype(np.float32)
+    e = np.exp(-np.abs(x))
+    assert np.array_equal(run("knf_np_exp", -np.abs(x)), e)
+    u = np.concatenate([rng.uniform(0, 1, 1_000_000).astype(np.float32), e])
+    assert np.array_equal(run("knf_np_log1p", u), np.log1p(u))
+    assert np.array_equal(run("knf_np_softplus", x), oracle.softplus32(x))
