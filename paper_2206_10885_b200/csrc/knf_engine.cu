@@ -82,7 +82,7 @@ int ensure_requests(Field& F, size_t n) {
   KNF_TRY(W.req_cell.ensure(n * sizeof(int)));
   KNF_TRY(W.req_rank.ensure(n * sizeof(int)));
   KNF_TRY(W.perm.ensure(n * sizeof(int)));
-  KNF_TRY(W.tiles.ensure((n / kTilePts + F.geom.n_cells + 2) * sizeof(Tile)));
+  KNF_TRY(W.tiles.ensure((n / kTilePts + 3 * (size_t)F.geom.n_cells + 2) * sizeof(Tile)));  // <= 3 small tiles per cell remainder
   bool fresh = W.cell_count.p == nullptr;
   KNF_TRY(W.cell_count.ensure((size_t)F.geom.n_cells * sizeof(int)));
   KNF_TRY(W.cell_offset.ensure(((size_t)F.geom.n_cells + 1) * sizeof(int)));
@@ -154,11 +154,13 @@ RouteBuffers route_buffers(Field& F, int slot, int next_slot, int list) {
   R.ctr = counters(F, slot);
   R.next_ctr = next_slot >= 0 ? counters(F, next_slot) : nullptr;
   R.eval_counter = nullptr;
+  R.small_tiles = 0;
   return R;
 }
 
 int begin_call(Field& F, cudaStream_t st) {
   KNF_CUDA(cudaSetDevice(F.device));
+  F.prof_chain = false;
   KNF_TRY(ensure_requests(F, 1024));
   KNF_CUDA(cudaMemsetAsync(F.ws.cell_count.p, 0, (size_t)F.geom.n_cells * sizeof(int), st));
   KNF_CUDA(cudaMemsetAsync(F.ws.counters.p, 0, kRouteSlots * sizeof(RouteCounters), st));  // stat counters persist
@@ -190,14 +192,21 @@ static cudaEvent_t next_event(Field& F) {
 }
 ProfScope::ProfScope(Field& f, cudaStream_t s, int k) : F(f), st(s), kind(k), on(f.profiling) {
   if (!on) return;
-  e0 = F.events_used;
-  cudaEventRecord(next_event(F), st);
+  // back-to-back scopes on one stream share an event: the previous scope's end is this scope's start
+  if (F.prof_chain && F.prof_last_end != (size_t)-1 && F.prof_last_stream == (void*)st) {
+    e0 = F.prof_last_end;
+  } else {
+    e0 = F.events_used;
+    cudaEventRecord(next_event(F), st);
+  }
 }
 ProfScope::~ProfScope() {
   if (!on) return;
   size_t e1 = F.events_used;
   cudaEventRecord(next_event(F), st);
   F.spans.push_back({kind, e0, e1});
+  F.prof_last_end = e1;
+  F.prof_last_stream = (void*)st;
 }
 int collect_profile(Field& F) {
   KNF_CUDA(cudaDeviceSynchronize());
@@ -217,6 +226,7 @@ int collect_profile(Field& F) {
   }
   F.spans.clear();
   F.events_used = 0;
+  F.prof_last_end = (size_t)-1;
   return 0;
 }
 
@@ -245,7 +255,7 @@ int launch_scan_scatter(Field& F, const RouteBuffers& R, size_t n_upper, cudaStr
 }
 
 static inline int mlp_grid(const Field& F, size_t n_upper, int ctas_per_sm = kWarpCtasPerSm) {
-  size_t tiles_upper = n_upper / kTilePts + std::min<size_t>(n_upper, (size_t)F.geom.n_cells) + 1;
+  size_t tiles_upper = n_upper / kTilePts + std::min<size_t>(n_upper, 3 * (size_t)F.geom.n_cells) + 1;
   return (int)std::max<size_t>(1, std::min<size_t>(tiles_upper, (size_t)148 * ctas_per_sm));
 }
 
@@ -367,6 +377,8 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
   // Global wavefronts.  Every ray queued in a wavefront either advances a step or (once each) fetches its secant /
   // re-check sample, so max_steps + 3 bounds the count; tile residency usually finishes in far fewer, which the
   // host learns by polling the request counts.
+  F.prof_chain = true;  // spans inside the loop are back to back on `st`: one shared event between neighbours
+  F.prof_last_end = (size_t)-1;
   for (int w = 0; w <= s.max_steps + 2; w++) {
     const int cur = w & 1, nxt = cur ^ 1;
     const bool filter_pass = exact_mode && F.fp16_ok && F.filter_mode != 0 && !filter_drained && w > 0;
@@ -402,6 +414,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     }
     RouteBuffers R = route_buffers(F, cur, nxt, cur);
     R.eval_counter = stat_counter(F, 3);  // requests that went through global routing
+    R.small_tiles = exact_mode ? 1 : 0;   // march_warp_kernel has the 16-point path
     KNF_TRY(launch_scan_scatter(F, R, (size_t)n, st));
     A.P.blobs = F.sdf_blobs;
     A.P.perm = R.perm;
@@ -429,12 +442,14 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
       KNF_CUDA(cudaMemcpyAsync(F.host_poll, &counters(F, nxt)->n_requests, sizeof(int), cudaMemcpyDeviceToHost, st));
       KNF_CUDA(cudaMemcpyAsync(F.host_poll + 1, &counters(F, 4 + nxt)->n_requests, sizeof(int), cudaMemcpyDeviceToHost, st));
       KNF_CUDA(cudaStreamSynchronize(st));
+      F.prof_last_end = (size_t)-1;  // the GPU idled during the poll: the next span records its own start
       const int n_exact = F.host_poll[0], n_filter = F.host_poll[1];
       if (n_exact == 0 && n_filter == 0) break;
       if (probing && w == 0 && (size_t)n_filter * 8 < (size_t)(n_exact + n_filter)) use_filter = false;  // < 1/8 of the live rays crawl
       if (!use_filter && n_filter == 0) filter_drained = true;
     }
   }
+  F.prof_chain = false;
   if (want_hit_list) KNF_CUDA(cudaMemsetAsync(W.hit_count.p, 0, 16, st));
   march_finish_kernel<<<nb, 256, 0, st>>>(M, (int)n, hit, t, pos, steps, want_hit_list ? W.hit_list.as<int>() : nullptr,
                                           want_hit_list ? W.hit_count.as<int>() : nullptr);

@@ -84,6 +84,9 @@ struct Field {
   };
   std::vector<Span> spans;
   size_t events_used = 0;
+  size_t prof_last_end = (size_t)-1;  // event index of the last finished span (shared with the next span's start)
+  void* prof_last_stream = nullptr;
+  bool prof_chain = false;            // set by the march loop
   int* host_poll = nullptr;  // pinned; early-out polling of the march loop
   int march_max_inner = 8;    // tile-residency cap (steps in place per tile visit)
 };

@@ -48,6 +48,116 @@ __device__ __forceinline__ void march_emit(const RouteBuffers& Q, int* live, boo
   route_emit_cell(Q, emit, slot, x, y, z, cell);
 }
 
+// One tile visit of the exact kernel.  SMALL = false: up to 64 rays, two per lane (panel columns 2 lane, 2 lane + 1);
+// SMALL = true: up to 16 rays, one in each of lanes 0..15 (panel column = lane), evaluated by the 4 x 4 register
+// tiles of knf_mlp.cuh -- a quarter of the work for the sparse tiles that dominate once the decision filter has
+// taken the crawling rays away.
+template <bool SMALL>
+__device__ __forceinline__ void march_exact_tile(const MarchTileArgs& A, MlpSmem<kSdfIn, kSdfOutPad>& S, const Tile& tile, int lane,
+                                                 uint32_t& parity, unsigned long long& evals, unsigned long long& slots) {
+  using Blob = SdfBlob;
+  constexpr int NQ = SMALL ? 1 : 2;
+  const MlpParams& P = A.P;
+  float* X = S.x;
+  bool active[NQ];
+  int ray[NQ], col[NQ];
+  float px[NQ], py[NQ], pz[NQ];
+  RayRegs rr[NQ];  // the lane's rays live in registers for the whole tile visit
+#pragma unroll
+  for (int q = 0; q < NQ; q++) {
+    col[q] = SMALL ? lane : 2 * lane + q;
+    active[q] = col[q] < tile.count;
+    ray[q] = 0;
+    px[q] = py[q] = pz[q] = 0.f;
+    if (active[q]) {
+      int slot = P.perm[tile.start + col[q]];
+      ray[q] = A.live_in[slot];
+      float4 pt = P.req_pt[slot];
+      px[q] = pt.x; py[q] = pt.y; pz[q] = pt.z;
+      ray_load(rr[q], A.M, ray[q]);  // in flight during the first MLP pass
+    }
+  }
+  zero_pad_rows<kSdfIn>(X, lane);
+  // fp32 box strictly inside the tile's cell: a point inside it is in this cell without redoing the
+  // fp64 cell arithmetic (cell_coord is monotone and its rounding error is ~1e-16 of the extent, the
+  // margin is 1e-6 of it); anything closer to a face takes the exact path.
+  float in_lo[3], in_hi[3];
+  {
+    const int N = A.G.resolution;
+    const int ci[3] = {tile.cell / (N * N), (tile.cell / N) % N, tile.cell % N};
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      const double ext = A.G.hi[a] - A.G.lo[a];
+      in_lo[a] = (float)(A.G.lo[a] + ext * ((double)ci[a] / N) + 1e-6 * ext);
+      in_hi[a] = (float)(A.G.lo[a] + ext * ((double)(ci[a] + 1) / N) - 1e-6 * ext);
+    }
+  }
+  int n_active = tile.count;
+
+  for (int inner = 0;; inner++) {
+    if (SMALL) {
+      if (lane < kSmallTilePts) encode_into<kSdfFreqs>(X, 0, lane, px[0], py[0], pz[0]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < NQ; q++) encode_into<kSdfFreqs>(X, 0, col[q], px[q], py[q], pz[q]);
+    }
+    __syncwarp();
+    if (inner == 0) {
+      mbar_wait(&S.bar, parity);  // weights have landed
+      parity ^= 1;
+    }
+    float dist[NQ];
+    if (SMALL) {
+      hidden_layers_small<kSdfIn, kSdfOutPad, ACT_SOFTPLUS>(X, S.w, lane);
+      dist[0] = lane < kSmallTilePts ? output_distance_col<kSdfOutPad>(X, S.w + Blob::w3, S.w + Blob::b3, lane) : 0.0f;
+    } else {
+      hidden_layers<kSdfIn, kSdfOutPad, ACT_SOFTPLUS>(X, S.w, lane);
+      const float2 d2 = output_distance<kSdfOutPad>(X, S.w + Blob::w3, S.w + Blob::b3, lane);
+      dist[0] = d2.x;
+      dist[NQ - 1] = d2.y;
+    }
+    evals += (lane == 0) ? (unsigned long long)n_active : 0ull;
+    slots += SMALL ? kSmallTilePts : kWarpPts;
+
+    // ---- the march step for the lane's rays -----------------------------------------------------------
+    int code[NQ], cell[NQ];
+    bool stay[NQ];
+    int n_stay = 0;
+#pragma unroll
+    for (int q = 0; q < NQ; q++) {
+      code[q] = STEP_DONE;
+      cell[q] = -1;
+      if (active[q]) {
+        double t_next = 0.0;
+        code[q] = ray_step(rr[q], A.M, ray[q], dist[q], t_next, A.crawl_below);
+        if (code[q] != STEP_DONE) {
+          // pts = origins + t * dirs in fp64 (surface.py:184), then the fp32 cast of grid.py:375
+          px[q] = __double2float_rn(rr[q].o[0] + t_next * rr[q].d[0]);
+          py[q] = __double2float_rn(rr[q].o[1] + t_next * rr[q].d[1]);
+          pz[q] = __double2float_rn(rr[q].o[2] + t_next * rr[q].d[2]);
+          const bool well_inside = px[q] > in_lo[0] && px[q] < in_hi[0] && py[q] > in_lo[1] && py[q] < in_hi[1] &&
+                                   pz[q] > in_lo[2] && pz[q] < in_hi[2];
+          cell[q] = well_inside ? tile.cell : cell_of(px[q], py[q], pz[q], A.G);
+        }
+      }
+      stay[q] = code[q] == STEP_EXACT && cell[q] == tile.cell;
+      n_stay += __popc(__ballot_sync(0xffffffffu, stay[q]));
+    }
+    // keep stepping in place while at least half of the tile's rays are still here
+    const bool cont = n_stay > 0 && 2 * n_stay >= tile.count && inner + 1 < A.max_inner;
+#pragma unroll
+    for (int q = 0; q < NQ; q++) {
+      march_emit(A.next, A.live_out, code[q] == STEP_EXACT && !(cont && stay[q]), ray[q], rr[q], A.M, px[q], py[q], pz[q], cell[q]);
+      march_emit(A.next_filter, A.live_filter, code[q] == STEP_FILTER, ray[q], rr[q], A.M, px[q], py[q], pz[q], cell[q]);
+      active[q] = cont && stay[q];
+      if (!active[q]) px[q] = py[q] = pz[q] = 0.f;
+    }
+    if (!cont) break;
+    n_active = n_stay;
+    __syncwarp();
+  }
+}
+
 static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(MarchTileArgs A) {
   using Blob = SdfBlob;
   using Smem = MlpSmem<kSdfIn, kSdfOutPad>;
@@ -62,103 +172,20 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(M
   const MlpParams& P = A.P;
   const int n_tiles = P.ctr->n_tiles;
   uint32_t parity = 0;
-  float* X = S.x;
-  unsigned long long evals = 0, passes = 0;
+  unsigned long long evals = 0, slots = 0;
 
   for (;;) {
     const int t = next_tile(P.ctr, lane);
     if (t >= n_tiles) break;
     const Tile tile = P.tiles[t];
     fetch_weights<Blob>(S.w, P.blobs, tile.cell, &S.bar, lane);
-
-    bool active[2];
-    int ray[2] = {0, 0};
-    float px[2], py[2], pz[2];
-    RayRegs rr[2];  // the lane's two rays live in registers for the whole tile visit
-#pragma unroll
-    for (int q = 0; q < 2; q++) {
-      int p = 2 * lane + q;
-      active[q] = p < tile.count;
-      px[q] = py[q] = pz[q] = 0.f;
-      if (active[q]) {
-        int slot = P.perm[tile.start + p];
-        ray[q] = A.live_in[slot];
-        float4 pt = P.req_pt[slot];
-        px[q] = pt.x; py[q] = pt.y; pz[q] = pt.z;
-        ray_load(rr[q], A.M, ray[q]);  // in flight during the first MLP pass
-      }
-    }
-    zero_pad_rows<kSdfIn>(X, lane);
-    // fp32 box strictly inside the tile's cell: a point inside it is in this cell without redoing the
-    // fp64 cell arithmetic (cell_coord is monotone and its rounding error is ~1e-16 of the extent, the
-    // margin is 1e-6 of it); anything closer to a face takes the exact path.
-    float in_lo[3], in_hi[3];
-    {
-      const int N = A.G.resolution;
-      const int ci[3] = {tile.cell / (N * N), (tile.cell / N) % N, tile.cell % N};
-#pragma unroll
-      for (int a = 0; a < 3; a++) {
-        const double ext = A.G.hi[a] - A.G.lo[a];
-        in_lo[a] = (float)(A.G.lo[a] + ext * ((double)ci[a] / N) + 1e-6 * ext);
-        in_hi[a] = (float)(A.G.lo[a] + ext * ((double)(ci[a] + 1) / N) - 1e-6 * ext);
-      }
-    }
-    int n_active = tile.count;
-
-    for (int inner = 0;; inner++) {
-      encode_into<kSdfFreqs>(X, 0, 2 * lane + 0, px[0], py[0], pz[0]);
-      encode_into<kSdfFreqs>(X, 0, 2 * lane + 1, px[1], py[1], pz[1]);
-      __syncwarp();
-      if (inner == 0) {
-        mbar_wait(&S.bar, parity);  // weights have landed
-        parity ^= 1;
-      }
-      hidden_layers<kSdfIn, kSdfOutPad, ACT_SOFTPLUS>(X, S.w, lane);
-      const float2 dist = output_distance<kSdfOutPad>(X, S.w + Blob::w3, S.w + Blob::b3, lane);
-      evals += (lane == 0) ? (unsigned long long)n_active : 0ull;
-      passes += 1;
-
-      // ---- the march step for the lane's two rays -----------------------------------------------------
-      int code[2], cell[2];
-      bool stay[2];
-#pragma unroll
-      for (int q = 0; q < 2; q++) {
-        code[q] = STEP_DONE;
-        cell[q] = -1;
-        if (active[q]) {
-          double t_next = 0.0;
-          code[q] = ray_step(rr[q], A.M, ray[q], q ? dist.y : dist.x, t_next, A.crawl_below);
-          if (code[q] != STEP_DONE) {
-            // pts = origins + t * dirs in fp64 (surface.py:184), then the fp32 cast of grid.py:375
-            px[q] = __double2float_rn(rr[q].o[0] + t_next * rr[q].d[0]);
-            py[q] = __double2float_rn(rr[q].o[1] + t_next * rr[q].d[1]);
-            pz[q] = __double2float_rn(rr[q].o[2] + t_next * rr[q].d[2]);
-            const bool well_inside = px[q] > in_lo[0] && px[q] < in_hi[0] && py[q] > in_lo[1] && py[q] < in_hi[1] &&
-                                     pz[q] > in_lo[2] && pz[q] < in_hi[2];
-            cell[q] = well_inside ? tile.cell : cell_of(px[q], py[q], pz[q], A.G);
-          }
-        }
-        stay[q] = code[q] == STEP_EXACT && cell[q] == tile.cell;
-      }
-      const int n_stay = __popc(__ballot_sync(0xffffffffu, stay[0])) + __popc(__ballot_sync(0xffffffffu, stay[1]));
-      // keep stepping in place while at least half of the tile's rays are still here
-      const bool cont = n_stay > 0 && 2 * n_stay >= tile.count && inner + 1 < A.max_inner;
-#pragma unroll
-      for (int q = 0; q < 2; q++) {
-        march_emit(A.next, A.live_out, code[q] == STEP_EXACT && !(cont && stay[q]), ray[q], rr[q], A.M, px[q], py[q], pz[q], cell[q]);
-        march_emit(A.next_filter, A.live_filter, code[q] == STEP_FILTER, ray[q], rr[q], A.M, px[q], py[q], pz[q], cell[q]);
-        active[q] = cont && stay[q];
-        if (!active[q]) px[q] = py[q] = pz[q] = 0.f;
-      }
-      if (!cont) break;
-      n_active = n_stay;
-      __syncwarp();
-    }
+    if (tile.count <= kSmallTilePts) march_exact_tile<true>(A, S, tile, lane, parity, evals, slots);
+    else march_exact_tile<false>(A, S, tile, lane, parity, evals, slots);
     __syncwarp();  // every lane is done reading S.w and the panel before the next tile overwrites them
   }
   if (lane == 0 && evals && A.eval_counter) {
     atomicAdd(A.eval_counter, evals);
-    atomicAdd(A.eval_counter + 2, passes * kWarpPts);  // lane slots spent (tile-fill statistic)
+    atomicAdd(A.eval_counter + 2, slots);  // lane slots spent (tile-fill statistic)
   }
 }
 

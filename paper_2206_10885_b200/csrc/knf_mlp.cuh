@@ -191,6 +191,104 @@ __device__ __forceinline__ void zero_pad_rows(float* __restrict__ X, int lane) {
   for (int r = K1; r < pad_k(K1); r++) *reinterpret_cast<float2*>(X + r * kPanelLd + 2 * lane) = make_float2(0.f, 0.f);
 }
 
+// ---- the same arithmetic for a SMALL tile (<= 16 points in panel columns 0..15) ---------------------------------
+// Late in a march the exact queue holds a handful of rays per cell; a 64-column pass would spend 3/4 of its FFMA2
+// on empty columns.  Here a lane accumulates 4 points x 4 neurons (4 point groups x 8 neuron groups), one LDS.128
+// of activations + one of weights per 8 FFMA2.  Every output is still the k-ordered FMA chain from zero followed by
+// the rounded bias add, so a point's value does not depend on which tile shape evaluated it.
+constexpr int kSmallTilePts = 16;
+
+template <int K>
+__device__ __forceinline__ void layer_4x4(const float* __restrict__ In, const float* __restrict__ Wt, int pg, int ng,
+                                          float2 (&acc)[2][4]) {
+  static_assert(K % 8 == 0, "pad K to a multiple of 8");
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++) acc[i][j] = make_float2(0.0f, 0.0f);
+  const float* xp = In + pg * 4;
+  const float* wp = Wt + ng * 4;
+#pragma unroll 1
+  for (int k0 = 0; k0 < K; k0 += 8) {
+#pragma unroll
+    for (int kk = 0; kk < 8; kk++) {
+      const float4 x = *reinterpret_cast<const float4*>(xp + (k0 + kk) * kPanelLd);
+      const float4 w = *reinterpret_cast<const float4*>(wp + (k0 + kk) * kHidden);
+      const float2 x01 = make_float2(x.x, x.y), x23 = make_float2(x.z, x.w);
+      const float ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        acc[0][j] = __ffma2_rn(x01, splat(ws[j]), acc[0][j]);
+        acc[1][j] = __ffma2_rn(x23, splat(ws[j]), acc[1][j]);
+      }
+    }
+  }
+}
+
+template <int ACT>
+__device__ __forceinline__ void store_hidden_small(float2 (&acc)[2][4], const float* __restrict__ bias, float* __restrict__ Out,
+                                                   int pg, int ng) {
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    const int neuron = ng * 4 + j;
+    const float2 b = splat(bias[neuron]);
+    float2 v0 = __fadd2_rn(acc[0][j], b), v1 = __fadd2_rn(acc[1][j], b);
+    if (ACT == ACT_RELU) {
+      v0 = make_float2(fmaxf(v0.x, 0.0f), fmaxf(v0.y, 0.0f));
+      v1 = make_float2(fmaxf(v1.x, 0.0f), fmaxf(v1.y, 0.0f));
+    }
+    *reinterpret_cast<float4*>(Out + neuron * kPanelLd + pg * 4) = make_float4(v0.x, v0.y, v1.x, v1.y);
+  }
+}
+
+// In-place softplus over panel rows 0..31, columns 0..15: lane owns columns 2 (lane & 7), +1 of rows (lane >> 3) + 4 i.
+__device__ __forceinline__ void softplus_panel_small(float* __restrict__ panel, int lane) {
+  float* base = panel + (lane >> 3) * kPanelLd + 2 * (lane & 7);
+#pragma unroll 1
+  for (int i0 = 0; i0 < 8; i0 += 4) {
+    float2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) v[u] = *reinterpret_cast<float2*>(base + 4 * (i0 + u) * kPanelLd);
+    softplus_tile<4>(v);
+#pragma unroll
+    for (int u = 0; u < 4; u++) *reinterpret_cast<float2*>(base + 4 * (i0 + u) * kPanelLd) = v[u];
+  }
+}
+
+template <int K1, int N3P, int HIDDEN_ACT>
+__device__ __forceinline__ void hidden_layers_small(float* __restrict__ X, const float* __restrict__ W, int lane) {
+  using Blob = BlobLayout<K1, N3P>;
+  const int pg = lane >> 3;  // 4 point groups of 4 points
+  const int ng = lane & 7;   // 8 neuron groups of 4 neurons
+  float2 acc[2][4];
+  layer_4x4<pad_k(K1)>(X, W + Blob::w1, pg, ng, acc);
+  __syncwarp();
+  store_hidden_small<HIDDEN_ACT>(acc, W + Blob::b1, X, pg, ng);
+  __syncwarp();
+  if (HIDDEN_ACT == ACT_SOFTPLUS) {
+    softplus_panel_small(X, lane);
+    __syncwarp();
+  }
+  layer_4x4<kHidden>(X, W + Blob::w2, pg, ng, acc);
+  __syncwarp();
+  store_hidden_small<HIDDEN_ACT>(acc, W + Blob::b2, X, pg, ng);
+  __syncwarp();
+  if (HIDDEN_ACT == ACT_SOFTPLUS) {
+    softplus_panel_small(X, lane);
+    __syncwarp();  // the output layer reads column `lane`, written by other lanes
+  }
+}
+
+// Output 0 (the distance) of the 32 -> N3 layer for panel column p (same chain as output_distance).
+template <int N3P>
+__device__ __forceinline__ float output_distance_col(const float* __restrict__ X, const float* __restrict__ W3,
+                                                     const float* __restrict__ B3, int p) {
+  float d = 0.0f;
+#pragma unroll 8
+  for (int k = 0; k < kHidden; k++) d = __fmaf_rn(X[k * kPanelLd + p], W3[k * N3P], d);
+  return __fadd_rn(d, B3[0]);
+}
+
 // Layers 1 and 2 (+ activations) of one 64-point warp tile; leaves h2 in the panel.
 template <int K1, int N3P, int HIDDEN_ACT>
 __device__ __forceinline__ void hidden_layers(float* __restrict__ X, const float* __restrict__ W, int lane) {

@@ -31,7 +31,17 @@ struct RouteBuffers {
   RouteCounters* ctr; // this pass
   RouteCounters* next_ctr;  // zeroed by scan (may equal nullptr)
   unsigned long long* eval_counter;  // += n_requests per pass (nullable); statistics only
+  int small_tiles;    // cut the last < 49 requests of a cell into tiles of <= 16 (kernels with a small-tile path)
 };
+
+// How a cell's k requests are cut into tiles: full 64-request tiles, then the remainder r either as one tile
+// (r >= 49, or small tiles off) or as ceil(r / 16) tiles of <= 16 requests.
+constexpr int kSmallTile = 16, kSmallTileMaxRemainder = 48;
+__device__ __forceinline__ int tiles_of_cell(int k, int small_tiles) {
+  const int full = k / kTilePts, r = k - full * kTilePts;
+  if (r == 0) return full;
+  return full + ((small_tiles && r <= kSmallTileMaxRemainder) ? (r + kSmallTile - 1) / kSmallTile : 1);
+}
 
 // Record request `slot` at fp32 point (x,y,z) whose cell is already known.  Must be reached by
 // all 32 lanes; `active` is false for lanes that have nothing to emit.
@@ -147,7 +157,7 @@ static __global__ void __launch_bounds__(kScanThreads) route_scan_kernel(RouteBu
   for (int c = c0; c < c1; c++) {
     int k = R.cell_count[c];
     pts += k;
-    tl += (k + kTilePts - 1) / kTilePts;
+    tl += tiles_of_cell(k, R.small_tiles);
     sg += (k > 0);
   }
   int p_base = pts, t_base = tl, g_base = sg, tot_p, tot_t, tot_g;
@@ -162,7 +172,7 @@ static __global__ void __launch_bounds__(kScanThreads) route_scan_kernel(RouteBu
       seg_start[g_base] = p_base;
       g_base++;
     }
-    t_base += (k + kTilePts - 1) / kTilePts;
+    t_base += tiles_of_cell(k, R.small_tiles);
     p_base += k;
   }
   if (tid == kScanThreads - 1) {
@@ -193,13 +203,16 @@ static __global__ void route_scatter_kernel(RouteBuffers R, int n_cells) {
   for (int c = gid; c < n_cells; c += stride) {
     const int start = R.cell_offset[c], k = R.cell_offset[c + 1] - start;
     int tb = R.tile_base[c];
-    for (int s = 0; s < k; s += kTilePts) {
+    for (int s = 0; s < k;) {
+      const int left = k - s;
+      const int take = left >= kTilePts ? kTilePts : ((R.small_tiles && left <= kSmallTileMaxRemainder) ? min(kSmallTile, left) : left);
       Tile t;
       t.cell = c;
       t.start = start + s;
-      t.count = min(kTilePts, k - s);
+      t.count = take;
       t.pad = 0;
       R.tiles[tb++] = t;
+      s += take;
     }
   }
 }
