@@ -363,6 +363,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   } while (!done);
 }
 
+// 8-byte asynchronous global -> shared copy (LDGSTS): no register staging, completion via cp_async_wait_all().
+__device__ __forceinline__ void cp_async_8(void* dst_smem, const void* src_gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src_gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // Warp-aggregated append: every active lane with `want` gets a unique slot from *counter.
 // Must be reached by all 32 lanes of the warp (callers keep their loops warp-uniform).
 __device__ __forceinline__ int warp_append(int* counter, bool want) {

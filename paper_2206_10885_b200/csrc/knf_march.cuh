@@ -240,11 +240,11 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
         ray[q] = A.live_in[slot];
         float4 pt = P.req_pt[slot];
         px[q] = pt.x; py[q] = pt.y; pz[q] = pt.z;
-        ray_load(rr[q], A.M, ray[q]);
+        ray_load_scalars(rr[q], A.M, ray[q]);  // in flight during the first pass
 #pragma unroll
-        for (int a = 0; a < 3; a++) {  // origin and direction live in shared memory during the visit (own slots only)
-          S.od[a][pidx[q]] = rr[q].o[a];
-          S.od[3 + a][pidx[q]] = rr[q].d[a];
+        for (int a = 0; a < 3; a++) {  // origin and direction go straight to shared memory (own slots only), also in flight
+          cp_async_8(&S.od[a][32 * q + lane], A.M.o + 3 * (size_t)ray[q] + a);
+          cp_async_8(&S.od[3 + a][32 * q + lane], A.M.d + 3 * (size_t)ray[q] + a);
         }
       }
     }
@@ -283,28 +283,17 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
       }
       const float b3 = reinterpret_cast<const float*>(S.w + Blob::b3)[0];
       float2 dist = make_float2(0.f, 0.f);
-      // software pipeline over the active m-tiles: the (serial, FMA-pipe) Fourier recurrence of the next m-tile is
-      // issued alongside the HMMAs of the current one
-      unsigned todo = 0;
-#pragma unroll
-      for (int m = 0; m < 4; m++) todo |= (act_mask & (0x11111111u << m)) ? (1u << m) : 0u;
-      float2 v[12];
-      if (todo) mma_encode<PC>(S, __ffs(todo) - 1, lane, v);
 #pragma unroll 1
-      while (todo) {
-        const int m = __ffs(todo) - 1;
-        todo &= todo - 1;
-        float2 vn[12];
-        if (todo) mma_encode<PC>(S, __ffs(todo) - 1, lane, vn);
+      for (int m = 0; m < 4; m++) {
+        if ((act_mask & (0x11111111u << m)) == 0) continue;
         float h2[4][4];
-        mma_hidden_from<PC, FILTER>(S, v, lane, h2);
+        mma_hidden<PC, FILTER>(S, m, lane, h2);
         const float2 d = mma_output(h2, W3t, b3, t, 0);
         if (m == t) dist = d;
         slots += 16;
-#pragma unroll
-        for (int i = 0; i < 12; i++) v[i] = vn[i];
       }
       evals += (lane == 0) ? (unsigned long long)n_active : 0ull;
+      if (inner == 0) cp_async_wait_all();  // the lane's own origin / direction slots
 
       int code[2], cell[2];
       bool stay[2];
@@ -325,9 +314,9 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
             // only say "keep crawling", and its step is taken without evaluating (certified skip).
             const double reach = FILTER ? (safe_below - (double)(q ? dist.y : dist.x)) * inv_lip : 0.0;
             for (;;) {
-              px[q] = __double2float_rn(S.od[0][pidx[q]] + t_next * S.od[3][pidx[q]]);
-              py[q] = __double2float_rn(S.od[1][pidx[q]] + t_next * S.od[4][pidx[q]]);
-              pz[q] = __double2float_rn(S.od[2][pidx[q]] + t_next * S.od[5][pidx[q]]);
+              px[q] = __double2float_rn(S.od[0][32 * q + lane] + t_next * S.od[3][32 * q + lane]);
+              py[q] = __double2float_rn(S.od[1][32 * q + lane] + t_next * S.od[4][32 * q + lane]);
+              pz[q] = __double2float_rn(S.od[2][32 * q + lane] + t_next * S.od[5][32 * q + lane]);
               const bool well_inside = px[q] > in_lo[0] && px[q] < in_hi[0] && py[q] > in_lo[1] && py[q] < in_hi[1] &&
                                        pz[q] > in_lo[2] && pz[q] < in_hi[2];
               cell[q] = well_inside ? tile.cell : cell_of(px[q], py[q], pz[q], A.G);

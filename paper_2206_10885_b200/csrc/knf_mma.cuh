@@ -82,7 +82,7 @@ struct MmaSmemT {
 // accesses) instead of in 48 registers per lane, which is what lets 13 one-warp CTAs share an SM.
 template <int P>
 struct MmaMarchSmemT : MmaSmemT<P> {
-  alignas(16) double od[6][64];
+  alignas(16) double od[6][64];  // [component][32 q + lane]: each lane touches only its own two slots
 };
 
 // ---- device helpers -------------------------------------------------------------------------------

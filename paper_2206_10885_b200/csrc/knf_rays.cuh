@@ -225,6 +225,17 @@ __device__ __forceinline__ void ray_load(RayRegs& R, const MarchState& M, int ra
   R.phase = ph & kPhaseMask;
   R.approx = (ph & kApproxPrevBit) ? 1 : 0;
 }
+// The same without origin / direction (kernels that park those in shared memory with cp.async).
+__device__ __forceinline__ void ray_load_scalars(RayRegs& R, const MarchState& M, int ray) {
+  R.t = M.t[ray];
+  R.t_far = M.t_far[ray];
+  R.t_prev = M.t_prev[ray];
+  R.d_prev = M.d_prev[ray];
+  R.steps = M.steps[ray];
+  const int ph = M.phase[ray];
+  R.phase = ph & kPhaseMask;
+  R.approx = (ph & kApproxPrevBit) ? 1 : 0;
+}
 // Write back what a later tile visit (or the finish kernel) needs.
 __device__ __forceinline__ void ray_store(const RayRegs& R, const MarchState& M, int ray) {
   M.t[ray] = R.t;
