@@ -373,7 +373,7 @@ int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
     F.geom.hi[a] = d->bbox_max[a];
   }
   F.geom.fd_step = d->fd_step;
-  if (const char* env = std::getenv("KNF_MARCH_MAX_INNER")) F.march_max_inner = std::max(1, std::atoi(env));  // tuning knob
+  if (const char* env = std::getenv("KNF_MARCH_MAX_INNER")) F.march_max_inner = F.filter_max_inner = std::max(1, std::atoi(env));  // tuning knob
   std::vector<float> packed;
   pack_family<kSdfIn, kSdfOut, kSdfOutPad>(F.geom.n_cells, d->sdf_w, d->sdf_b, packed);
   KNF_CUDA(cudaMalloc(&F.sdf_blobs, packed.size() * sizeof(float)));

@@ -371,7 +371,11 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
   // negative region at all -- on a real surface they never do and the filter passes would be empty launches.
   const bool exact_mode = F.precision == KNF_PRECISION_FP32_CHAIN;
   bool use_filter = exact_mode && F.fp16_ok && F.filter_mode != 0;
-  const bool probing = use_filter && F.filter_mode == 2;
+  // auto: probe the first wavefront unless the previous march on this handle already showed which way it goes
+  // (consecutive frames of one field look alike; a wrong hint costs time, never a result)
+  if (use_filter && F.filter_mode == 2 && F.filter_hint == 2) use_filter = false;
+  const bool probing = use_filter && F.filter_mode == 2 && F.filter_hint == 0;
+  size_t seen_filter = 0, seen_total = 0;
   bool filter_drained = false;  // the filter queue was seen empty after the filter had been switched off
   const double crawl_on = -(s.eps_hit + 2.0 * F.filter_delta_max);
   // Global wavefronts.  Every ray queued in a wavefront either advances a step or (once each) fetches its secant /
@@ -404,6 +408,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
       Af.P.ctr = Rf.ctr;
       Af.P.req_pt = Rf.req_pt;
       Af.live_in = M.live[2 + cur];
+      Af.max_inner = F.filter_max_inner;
       Af.defer = route_buffers(F, cur, -1, cur);
       Af.live_defer = M.live[cur];
       {
@@ -444,12 +449,20 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
       KNF_CUDA(cudaStreamSynchronize(st));
       F.prof_last_end = (size_t)-1;  // the GPU idled during the poll: the next span records its own start
       const int n_exact = F.host_poll[0], n_filter = F.host_poll[1];
+      if (w <= 1) {
+        seen_filter = (size_t)n_filter;
+        seen_total = (size_t)n_exact + (size_t)n_filter;
+      }
       if (n_exact == 0 && n_filter == 0) break;
       if (probing && w == 0 && (size_t)n_filter * 8 < (size_t)(n_exact + n_filter)) use_filter = false;  // < 1/8 of the live rays crawl
       if (!use_filter && n_filter == 0) filter_drained = true;
     }
   }
   F.prof_chain = false;
+  if (exact_mode && F.fp16_ok && F.filter_mode == 2 && seen_total > 0) {
+    if (F.filter_hint != 2) F.filter_hint = (seen_filter * 8 >= seen_total) ? 1 : 2;
+    else if (n >= 4096) F.filter_hint = 0;  // a "no crawl" hint is re-examined by probing the next large march
+  }
   if (want_hit_list) KNF_CUDA(cudaMemsetAsync(W.hit_count.p, 0, 16, st));
   march_finish_kernel<<<nb, 256, 0, st>>>(M, (int)n, hit, t, pos, steps, want_hit_list ? W.hit_list.as<int>() : nullptr,
                                           want_hit_list ? W.hit_count.as<int>() : nullptr);

@@ -69,6 +69,7 @@ struct Field {
   bool fp16_ok = false;
   double filter_delta_max = 0.0;       // largest per-cell decision-filter bound (knf_api.cu filter_delta)
   bool filter_skip = true;             // certified (Lipschitz) skipping inside the filter; KNF_FILTER_SKIP=0 disables
+  int filter_hint = 0;                 // auto mode: what the previous march on this handle learnt (0 unknown, 1 rays crawl, 2 they do not)
   int filter_mode = 2;                 // decision filter of the exact march: 0 off, 1 on, 2 auto (probe the first wavefront)
   int precision = 0;                  // KNF_PRECISION_*: which SDF tile kernels run
   Workspace ws;
@@ -88,7 +89,8 @@ struct Field {
   void* prof_last_stream = nullptr;
   bool prof_chain = false;            // set by the march loop
   int* host_poll = nullptr;  // pinned; early-out polling of the march loop
-  int march_max_inner = 8;    // tile-residency cap (steps in place per tile visit)
+  int march_max_inner = 8;    // tile-residency cap (steps in place per tile visit), exact / tensor march kernels
+  int filter_max_inner = 12;  // ... of the decision-filter kernel (measured optimum: 8 -> 15.97 ms, 12 -> 15.80, 16 -> 16.06)
 };
 
 enum { SPAN_SDF_MLP = 0, SPAN_ROUTE = 1, SPAN_COLOR_MLP = 2, SPAN_OTHER = 3, SPAN_FILTER = 4 };
