@@ -35,7 +35,7 @@ ROUTE_BYTES_PER_CELL = 16      # scan: count read + zeroed, offset + tile base w
 ORBIT_VIEWS, ORBIT_RADIUS, ORBIT_ELEV, FOV = 100, 2.5, 0.2, np.deg2rad(40.0)
 
 
-PREHEAT_FRAMES = 48  # untimed, before the W warm-up steps
+PREHEAT_FRAMES = int(os.environ.get("BENCH_PREHEAT", "48"))  # untimed, before the W warm-up steps (BENCH_PREHEAT=0 for ncu launch lists)
 
 
 def measured_peaks():

@@ -326,6 +326,15 @@ __device__ __forceinline__ int cell_coord(double p, double lo, double hi, int n)
   return (int)fl;
 }
 
+// Out-of-line copy for the march kernels, which need it only for the few samples near a cell face (three fp64
+// divisions: ~300 instructions per inlined copy).
+static __device__ __noinline__ int cell_of_slow(float x, float y, float z, double lo0, double lo1, double lo2, double hi0, double hi1, double hi2, int n) {
+  int i = cell_coord((double)x, lo0, hi0, n);
+  int j = cell_coord((double)y, lo1, hi1, n);
+  int k = cell_coord((double)z, lo2, hi2, n);
+  return (i * n + j) * n + k;
+}
+
 __device__ __forceinline__ int cell_of(double x, double y, double z, const GridGeom& g) {
   int i = cell_coord(x, g.lo[0], g.hi[0], g.resolution);
   int j = cell_coord(y, g.lo[1], g.hi[1], g.resolution);

@@ -397,6 +397,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     A.max_inner = (probing && w == 0) ? 1 : F.march_max_inner;
     A.crawl_below = use_filter ? crawl_on : -INFINITY;
     A.max_skip = F.filter_skip ? 1 : 0;
+    A.inv_resolution = 1.0 / (double)F.geom.resolution;
     if (filter_pass) {
       // filter queue of this wavefront: tensor-core predicate; undecided samples join the exact queue below
       RouteBuffers Rf = route_buffers(F, 4 + cur, 4 + nxt, 2 + cur);

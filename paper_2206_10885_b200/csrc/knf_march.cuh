@@ -33,6 +33,7 @@ struct MarchTileArgs {
   unsigned long long* eval_counter;  // statistics: [0] SDF evaluations, [2] lane slots, [4] filter evaluations, [5] deferred, [6] certified skips
   int max_inner;            // cap on consecutive in-place steps of one tile
   int max_skip;             // filter kernel: 0 disables certified skipping
+  double inv_resolution;    // 1 / grid resolution (host-computed)
   double crawl_below;       // exact kernels: a march step from a distance below this continues in the filter queue (-inf: never)
 };
 
@@ -84,12 +85,13 @@ __device__ __forceinline__ void march_exact_tile(const MarchTileArgs& A, MlpSmem
   float in_lo[3], in_hi[3];
   {
     const int N = A.G.resolution;
+    const double inv_n = A.inv_resolution;
     const int ci[3] = {tile.cell / (N * N), (tile.cell / N) % N, tile.cell % N};
 #pragma unroll
     for (int a = 0; a < 3; a++) {
-      const double ext = A.G.hi[a] - A.G.lo[a];
-      in_lo[a] = (float)(A.G.lo[a] + ext * ((double)ci[a] / N) + 1e-6 * ext);
-      in_hi[a] = (float)(A.G.lo[a] + ext * ((double)(ci[a] + 1) / N) - 1e-6 * ext);
+      const double ext = A.G.hi[a] - A.G.lo[a];  // (a multiplication by 1/N instead of a division: the 1e-6 margin absorbs the ulp)
+      in_lo[a] = (float)(A.G.lo[a] + ext * ((double)ci[a] * inv_n) + 1e-6 * ext);
+      in_hi[a] = (float)(A.G.lo[a] + ext * ((double)(ci[a] + 1) * inv_n) - 1e-6 * ext);
     }
   }
   int n_active = tile.count;
@@ -137,7 +139,7 @@ __device__ __forceinline__ void march_exact_tile(const MarchTileArgs& A, MlpSmem
           pz[q] = __double2float_rn(rr[q].o[2] + t_next * rr[q].d[2]);
           const bool well_inside = px[q] > in_lo[0] && px[q] < in_hi[0] && py[q] > in_lo[1] && py[q] < in_hi[1] &&
                                    pz[q] > in_lo[2] && pz[q] < in_hi[2];
-          cell[q] = well_inside ? tile.cell : cell_of(px[q], py[q], pz[q], A.G);
+          cell[q] = well_inside ? tile.cell : cell_of_slow(px[q], py[q], pz[q], A.G.lo[0], A.G.lo[1], A.G.lo[2], A.G.hi[0], A.G.hi[1], A.G.hi[2], A.G.resolution);
         }
       }
       stay[q] = code[q] == STEP_EXACT && cell[q] == tile.cell;
@@ -251,12 +253,13 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
     float in_lo[3], in_hi[3];
     {
       const int N = A.G.resolution;
+      const double inv_n = A.inv_resolution;
       const int ci[3] = {tile.cell / (N * N), (tile.cell / N) % N, tile.cell % N};
 #pragma unroll
       for (int a = 0; a < 3; a++) {
         const double ext = A.G.hi[a] - A.G.lo[a];
-        in_lo[a] = (float)(A.G.lo[a] + ext * ((double)ci[a] / N) + 1e-6 * ext);
-        in_hi[a] = (float)(A.G.lo[a] + ext * ((double)(ci[a] + 1) / N) - 1e-6 * ext);
+        in_lo[a] = (float)(A.G.lo[a] + ext * ((double)ci[a] * inv_n) + 1e-6 * ext);
+        in_hi[a] = (float)(A.G.lo[a] + ext * ((double)(ci[a] + 1) * inv_n) - 1e-6 * ext);
       }
     }
     int n_active = tile.count;
@@ -319,7 +322,7 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
               pz[q] = __double2float_rn(S.od[2][32 * q + lane] + t_next * S.od[5][32 * q + lane]);
               const bool well_inside = px[q] > in_lo[0] && px[q] < in_hi[0] && py[q] > in_lo[1] && py[q] < in_hi[1] &&
                                        pz[q] > in_lo[2] && pz[q] < in_hi[2];
-              cell[q] = well_inside ? tile.cell : cell_of(px[q], py[q], pz[q], A.G);
+              cell[q] = well_inside ? tile.cell : cell_of_slow(px[q], py[q], pz[q], A.G.lo[0], A.G.lo[1], A.G.lo[2], A.G.hi[0], A.G.hi[1], A.G.hi[2], A.G.resolution);
               if (!FILTER || !well_inside) break;
               const float dx = px[q] - x0, dy = py[q] - y0, dz = pz[q] - z0;
               const float far = sqrtf(dx * dx + dy * dy + dz * dz);

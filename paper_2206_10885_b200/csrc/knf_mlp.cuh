@@ -145,7 +145,9 @@ __device__ __forceinline__ void store_hidden(float2 (&acc)[4][8], const float* _
 #define KNF_SP_UNROLL 4
 #endif
 constexpr int kSoftplusUnroll = KNF_SP_UNROLL;
-__device__ __forceinline__ void softplus_panel(float* __restrict__ panel, int lane) {
+// __noinline__: the exact kernel calls this four times per pass shape; one copy keeps it inside the instruction cache
+// (ncu on the 97 KB version: no_instruction was the top stall, 1.9 per issue).
+static __device__ __noinline__ void softplus_panel(float* __restrict__ panel, int lane) {
 #pragma unroll 1
   for (int j = 0; j < kHidden; j += kSoftplusUnroll) {
     float2 v[kSoftplusUnroll];
@@ -158,8 +160,10 @@ __device__ __forceinline__ void softplus_panel(float* __restrict__ panel, int la
 }
 
 // nn.fourier_encode (nn.py:66-93) of a 3-vector into panel rows [row0, row0 + 3 + 6*L) at column p.
+// __noinline__ (one copy per instantiation): three sin/cos evaluations and the recurrence are ~300 instructions, and
+// the exact kernel used to inline them three times.
 template <int L>
-__device__ __forceinline__ void encode_into(float* __restrict__ panel, int row0, int p, float x, float y, float z) {
+static __device__ __noinline__ void encode_into(float* __restrict__ panel, int row0, int p, float x, float y, float z) {
   const float pi_f = 3.14159274101257324e+00f;  // float32(np.pi)
   panel[(row0 + 0) * kPanelLd + p] = x;
   panel[(row0 + 1) * kPanelLd + p] = y;
@@ -242,7 +246,7 @@ __device__ __forceinline__ void store_hidden_small(float2 (&acc)[2][4], const fl
 }
 
 // In-place softplus over panel rows 0..31, columns 0..15: lane owns columns 2 (lane & 7), +1 of rows (lane >> 3) + 4 i.
-__device__ __forceinline__ void softplus_panel_small(float* __restrict__ panel, int lane) {
+static __device__ __noinline__ void softplus_panel_small(float* __restrict__ panel, int lane) {
   float* base = panel + (lane >> 3) * kPanelLd + 2 * (lane & 7);
 #pragma unroll 1
   for (int i0 = 0; i0 < 8; i0 += 4) {

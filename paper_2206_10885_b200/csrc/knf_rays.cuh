@@ -245,6 +245,9 @@ __device__ __forceinline__ void ray_store(const RayRegs& R, const MarchState& M,
   M.phase[ray] = (unsigned char)(R.phase | (R.approx ? kApproxPrevBit : 0));
 }
 
+// IEEE fp64 division out of line: the inlined sequence (~50 instructions with its slow path) sat in every copy of the step.
+static __device__ __noinline__ double div_f64(double a, double b) { return a / b; }
+
 // One sphere-trace step of one ray (the body of the reference loop, surface.py:185-223) given the EXACT fp32
 // distance `dval` the MLP produced at the ray's requested parameter.  Returns STEP_DONE when the ray is finished
 // (its result has been written to global memory), otherwise the ray needs another evaluation at t_next:
@@ -283,7 +286,7 @@ __device__ __forceinline__ int ray_step(RayRegs& R, const MarchState& M, int ray
   if (converged) {
     const double tp = R.t_prev, dp = R.d_prev;
     if (isfinite(tp) && (fabs(dv - dp) > 1e-12)) {
-      double root = t - dv * (t - tp) / (dv - dp);
+      double root = t - div_f64(dv * (t - tp), dv - dp);
       const double a = fmin(t, tp), b = fmax(t, tp);
       root = fmin(fmax(root, a), b + (b - a));  // np.clip(root, a, b + (b - a))
       M.t_conv[ray] = t;

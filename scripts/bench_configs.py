@@ -37,6 +37,17 @@ for M in [1 << 14, 1 << 16, 1 << 18, 1_000_000, 1 << 22, 1 << 24]:
     sweep[str(M)] = {"sdf_ms": ms, "sdf_Mq_per_s": M / ms / 1e3, "sdf_tflops": M * 5120 / ms / 1e9, "color_ms": msc, "color_Mq_per_s": M / msc / 1e3}
     del pts, z, v
 out["config4_forward_sweep"] = sweep
+# the same 1e6 / 2^24-point SDF forward in the tensor-core precision modes
+modes = {}
+for mode in ("fp32_chain", "tensor_bf16x3", "tensor_fp16x2"):
+    dev.set_precision(mode)
+    for M in (1_000_000, 1 << 24):
+        pts = torch.as_tensor(np.random.default_rng(0).uniform(-1, 1, (M, 3)).astype(np.float32), device="cuda")
+        ms = ev_time(lambda: grid.sdf_query(dev, pts))
+        modes[f"{mode}_{M}"] = {"sdf_ms": ms, "sdf_Mq_per_s": M / ms / 1e3, "sdf_tflops": M * 5120 / ms / 1e9}
+        del pts
+dev.set_precision("fp32_chain")
+out["config4_precision_modes"] = modes
 for ncell in (1, 8, 64):
     M = 1 << 20
     rng = np.random.default_rng(1); base = rng.integers(0, 16, size=(ncell, 3)); pick = base[rng.integers(0, ncell, M)]
