@@ -326,6 +326,7 @@ void pack_sdf_mma(int n_cells, const float* const w[3], const float* const b[3],
     float* w3t = reinterpret_cast<float*>(blob + Blob::w3);
     for (int j = 0; j < kSdfOut; j++)
       for (int k = 0; k < kHidden; k++) w3t[k * kSdfOutPad + j] = w3[j * kHidden + k];
+    std::memcpy(blob + Blob::w3d, w3, kHidden * sizeof(float));  // row 0 of (9, 32): the distance output
     std::memcpy(blob + Blob::b3, b[2] + (size_t)c * kSdfOut, kSdfOut * sizeof(float));
     const double delta = filter_delta(P, w1, b[0] + (size_t)c * kHidden, w2, b[1] + (size_t)c * kHidden, w3, b[2] + (size_t)c * kSdfOut, x_raw);
     const float delta_f = std::nextafter((float)delta, INFINITY);

@@ -225,7 +225,7 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
     const int tix = next_tile(P.ctr, lane);
     if (tix >= n_tiles) break;
     const Tile tile = P.tiles[tix];
-    fetch_mma_weights<PC>(S, blobs, tile.cell, lane);
+    fetch_mma_weights<PC, Blob::march_bytes>(S, blobs, tile.cell, lane);
 
     bool active[2];
     int ray[2] = {0, 0};
@@ -263,7 +263,7 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
       }
     }
     int n_active = tile.count;
-    const float* W3t = reinterpret_cast<const float*>(S.w + Blob::w3);
+    const float* W3d = reinterpret_cast<const float*>(S.w + Blob::w3d);  // output-layer column 0
     double safe_below = 0.0, inv_lip = 0.0;
 
     for (int inner = 0;; inner++) {
@@ -290,8 +290,8 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
       for (int m = 0; m < 4; m++) {
         if ((act_mask & (0x11111111u << m)) == 0) continue;
         float h2[4][4];
-        mma_hidden<PC, FILTER>(S, m, lane, h2);
-        const float2 d = mma_output(h2, W3t, b3, t, 0);
+        mma_hidden<PC, FILTER, MmaMarchSmemT<PC>>(S, m, lane, h2);
+        const float2 d = mma_output<1>(h2, W3d, b3, t, 0);
         if (m == t) dist = d;
         slots += 16;
       }

@@ -39,7 +39,8 @@ namespace knf {
 // second piece scaled by 2^11 to stay normal, three products).
 //   frag1[kt 0..2][nt 0..3][lane 0..31][piece 0..P-1] uint2   B fragments of W1 (K order permuted, see mma_feature_of)
 //   frag2[kt 0..1][nt 0..3][lane 0..31][piece 0..P-1] uint2   B fragments of W2   (P = 2: one LDS.128 per lane)
-//   b1[32] b2[32] fp32 | W3t[32][12] fp32 (k-major, like BlobLayout) | b3[12] fp32
+//   b1[32] b2[32] fp32 | w3d[32] fp32 (output-layer column 0: the distance) | b3[12] fp32      <- march kernels copy up to here
+//   W3t[32][12] fp32 (k-major, like BlobLayout: all nine outputs, batched-forward kernel only)
 template <int P>
 struct MmaBlobT {
   static constexpr int pieces = P;
@@ -48,11 +49,14 @@ struct MmaBlobT {
   static constexpr int frag2 = frag1 + kt1 * 4 * P * 32 * 2;
   static constexpr int b1 = frag2 + kt2 * 4 * P * 32 * 2;
   static constexpr int b2 = b1 + kHidden;
-  static constexpr int w3 = b2 + kHidden;
-  static constexpr int b3 = w3 + kHidden * kSdfOutPad;
-  static constexpr int words = b3 + kSdfOutPad;  // P = 3: 4300 (17200 B); P = 2: 3020 (12080 B)
+  static constexpr int w3d = b2 + kHidden;
+  static constexpr int b3 = w3d + kHidden;
+  static constexpr int march_words = b3 + kSdfOutPad;  // what a march kernel needs: P = 3: 2956 (11824 B... see bytes), P = 2: 2668 (10672 B)
+  static constexpr int w3 = march_words;
+  static constexpr int words = w3 + kHidden * kSdfOutPad;  // P = 3: 4332 (17328 B); P = 2: 3052 (12208 B)
   static constexpr int bytes = words * 4;
-  static_assert(bytes % 16 == 0, "blob must be a multiple of 16 B for cp.async.bulk");
+  static constexpr int march_bytes = march_words * 4;
+  static_assert(bytes % 16 == 0 && march_bytes % 16 == 0, "blob (parts) must be multiples of 16 B for cp.async.bulk");
 };
 using MmaBlob = MmaBlobT<3>;
 using MmaBlobH = MmaBlobT<2>;
@@ -81,8 +85,11 @@ struct MmaSmemT {
 // The march kernels also park the resident rays' origins and directions here (k-major: conflict-free 8-byte
 // accesses) instead of in 48 registers per lane, which is what lets 13 one-warp CTAs share an SM.
 template <int P>
-struct MmaMarchSmemT : MmaSmemT<P> {
+struct MmaMarchSmemT {
+  alignas(16) uint32_t w[MmaBlobT<P>::march_words];
+  alignas(16) float pts[3][72];
   alignas(16) double od[6][64];  // [component][32 q + lane]: each lane touches only its own two slots
+  alignas(8) uint64_t bar;
 };
 
 // ---- device helpers -------------------------------------------------------------------------------
@@ -203,8 +210,8 @@ __device__ __forceinline__ void finish_hidden(const float (&small)[4][4], const 
 // First-layer inputs of m-tile `m` of the warp's 64 points, as the lane's A-fragment values: v[i] = (row g, row g+8)
 // of the lane's i-th input (k-tile major).  Lane t < 3 runs nn.fourier_encode's recurrence for axis t of its two
 // rows; lane t = 3 carries the raw coordinates.  Coordinates come from S.pts.
-template <int P>
-__device__ __forceinline__ void mma_encode(const MmaSmemT<P>& S, int m, int lane, float2 (&v)[12]) {
+template <int P, class SmemT>
+__device__ __forceinline__ void mma_encode(const SmemT& S, int m, int lane, float2 (&v)[12]) {
   const int g = lane >> 2, t = lane & 3;
   const float pi_f = 3.14159274101257324e+00f;  // float32(np.pi)
   const int p0 = 16 * m + g;
@@ -237,8 +244,8 @@ __device__ __forceinline__ void mma_encode(const MmaSmemT<P>& S, int m, int lane
 
 // Hidden activations h2 (after both softplus layers) of one m-tile from its encoded inputs, in accumulator layout:
 // h2[nt][0..1] = row g, columns 8nt+2t, +1 ; h2[nt][2..3] = row g+8.
-template <int P, bool FAST>
-__device__ __forceinline__ void mma_hidden_from(const MmaSmemT<P>& S, const float2 (&v)[12], int lane, float (&h2)[4][4]) {
+template <int P, bool FAST, class SmemT>
+__device__ __forceinline__ void mma_hidden_from(const SmemT& S, const float2 (&v)[12], int lane, float (&h2)[4][4]) {
   using Blob = MmaBlobT<P>;
   const int t = lane & 3;
   float h1[4][4], small[4][4], big[4][4];
@@ -263,22 +270,23 @@ __device__ __forceinline__ void mma_hidden_from(const MmaSmemT<P>& S, const floa
   finish_hidden<P, FAST>(small, big, reinterpret_cast<const float*>(S.w + Blob::b2), t, h2);
 }
 
-template <int P, bool FAST>
-__device__ __forceinline__ void mma_hidden(const MmaSmemT<P>& S, int m, int lane, float (&h2)[4][4]) {
+template <int P, bool FAST, class SmemT>
+__device__ __forceinline__ void mma_hidden(const SmemT& S, int m, int lane, float (&h2)[4][4]) {
   float2 v[12];
-  mma_encode<P>(S, m, lane, v);
-  mma_hidden_from<P, FAST>(S, v, lane, h2);
+  mma_encode<P, SmemT>(S, m, lane, v);
+  mma_hidden_from<P, FAST, SmemT>(S, v, lane, h2);
 }
 
 // Output column j of the 32 -> N3 layer for rows g (.x) and g+8 (.y): the lane's eight hidden units first
 // (fp32 FMA, fixed order), then the quad butterfly; every lane of the quad ends up with the full sum.
+template <int LD = kSdfOutPad>
 __device__ __forceinline__ float2 mma_output(const float (&h2)[4][4], const float* __restrict__ W3t, float bias, int t, int j) {
   float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
   for (int nt = 0; nt < 4; nt++) {
     const int k = 8 * nt + 2 * t;
-    acc = __ffma2_rn(make_float2(h2[nt][0], h2[nt][2]), splat(W3t[k * kSdfOutPad + j]), acc);
-    acc = __ffma2_rn(make_float2(h2[nt][1], h2[nt][3]), splat(W3t[(k + 1) * kSdfOutPad + j]), acc);
+    acc = __ffma2_rn(make_float2(h2[nt][0], h2[nt][2]), splat(W3t[k * LD + j]), acc);
+    acc = __ffma2_rn(make_float2(h2[nt][1], h2[nt][3]), splat(W3t[(k + 1) * LD + j]), acc);
   }
   acc.x = __fadd_rn(acc.x, __shfl_xor_sync(0xffffffffu, acc.x, 1));
   acc.y = __fadd_rn(acc.y, __shfl_xor_sync(0xffffffffu, acc.y, 1));
@@ -287,12 +295,12 @@ __device__ __forceinline__ float2 mma_output(const float (&h2)[4][4], const floa
   return __fadd2_rn(acc, splat(bias));
 }
 
-template <int P>
-__device__ __forceinline__ void fetch_mma_weights(MmaSmemT<P>& S, const uint32_t* __restrict__ blobs, int cell, int lane) {
+template <int P, int BYTES, class SmemT>
+__device__ __forceinline__ void fetch_mma_weights(SmemT& S, const uint32_t* __restrict__ blobs, int cell, int lane) {
   if (lane == 0) {
     fence_proxy_async();
-    mbar_expect_tx(&S.bar, MmaBlobT<P>::bytes);
-    bulk_copy_g2s(S.w, blobs + (size_t)cell * MmaBlobT<P>::words, MmaBlobT<P>::bytes, &S.bar);
+    mbar_expect_tx(&S.bar, BYTES);
+    bulk_copy_g2s(S.w, blobs + (size_t)cell * MmaBlobT<P>::words, BYTES, &S.bar);
   }
 }
 
@@ -301,11 +309,11 @@ __device__ __forceinline__ void fetch_mma_weights(MmaSmemT<P>& S, const uint32_t
 #endif
 constexpr int kMmaCtasPerSm = KNF_MMA_CTAS_PER_SM;
 #ifndef KNF_FILTER_CTAS_PER_SM
-#define KNF_FILTER_CTAS_PER_SM 12
+#define KNF_FILTER_CTAS_PER_SM 14
 #endif
 // one-warp CTAs per SM of the march kernels: P = 3 is bound by its 21 KB of shared memory, P = 2 by 16 KB
 template <int P>
-constexpr int march_ctas_per_sm() { return P == 2 ? KNF_FILTER_CTAS_PER_SM : 10; }
+constexpr int march_ctas_per_sm() { return P == 2 ? KNF_FILTER_CTAS_PER_SM : 12; }
 
 // ---- batched forward (grid.sdf_query, shading probes) ---------------------------------------------------
 // Tile point p is owned by lane (g = p % 8 ... ) : point 16 t + g (+ 8): lane 4 g + t.
@@ -327,7 +335,7 @@ static __global__ void __launch_bounds__(32, kMmaCtasPerSm) sdf_mma_kernel(MlpPa
     const int tix = next_tile(P.ctr, lane);
     if (tix >= n_tiles) break;
     const Tile tile = P.tiles[tix];
-    fetch_mma_weights<PC>(S, blobs, tile.cell, lane);
+    fetch_mma_weights<PC, Blob::bytes>(S, blobs, tile.cell, lane);
 #pragma unroll
     for (int q = 0; q < 2; q++) {
       const int p = 16 * t + g + 8 * q;
@@ -350,7 +358,7 @@ static __global__ void __launch_bounds__(32, kMmaCtasPerSm) sdf_mma_kernel(MlpPa
     const int m_tiles = (tile.count + 15) >> 4;
     for (int m = 0; m < m_tiles; m++) {
       float h2[4][4];
-      mma_hidden<PC, false>(S, m, lane, h2);
+      mma_hidden<PC, false, MmaSmemT<PC>>(S, m, lane, h2);
       const int s0 = S.slot[16 * m + g], s1 = S.slot[16 * m + g + 8];
       if (P.out_full == nullptr) {
         const float2 d = mma_output(h2, W3t, B3[0], t, 0);
