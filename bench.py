@@ -337,9 +337,9 @@ def main():
             "kernel": "march_mma_kernel<2, filter> (decision filter: Fourier recurrence + fp16x2 split mma.sync.m16n8k16 layers chained in registers + MUFU softplus "
                       "+ sphere-trace crawl step + certified skipping)",
             "bound": "tensor", "achieved": filter_tflops, "peak": tensor_peak, "unit": "TFLOP/s", "frac": (filter_tflops / tensor_peak) if filter_tflops else None,
-            "traffic": 242.5e6,
-            "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of ONE dense filter launch (0.81 ms, ~9 M evaluations) from profiles/ncu_r1_filter_v1 "
-                            "(ncu --set full); weights (49 MB of fp16 fragments) and ray state are L2-resident, DRAM is 3.7 % busy",
+            "traffic": 215.7e6,
+            "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of ONE dense filter launch (1.14 ms under ncu, ~13 M evaluations) from "
+                            "profiles/ncu_r1_filter_v3.summary.txt (ncu --set full); weights (50 MB of fp16 fragments) and ray state are L2-resident, DRAM is 2.3 % busy",
             "peak_source": f"{peak_src} MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS, tcgen05 path); mma.sync (HMMA.16816) issue peak measured on this pool: "
                            "553 TFLOP/s (profiles/hmma_split_r1.txt)",
             "algorithmic_flop_per_launch": stats["filter_evals"] * FLOP_PER_SDF_EVAL / max(stats["filter_launches"], 1),

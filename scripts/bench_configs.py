@@ -62,7 +62,7 @@ ms = ev_time(lambda: pathtrace.pathtrace_rows(scene, pose, 1, 0, 8, 0, 0, 2160, 
 out["config5_pathtrace_3840x2160_spp1_distilled"] = {"ms": ms, "Mpaths_per_s": 3840 * 2160 / ms / 1e3}
 scene16 = pathtrace.Scene([pathtrace.QuadObj((-3, -1.0, -3), (6, 0, 0), (0, 0, 6), pathtrace.Lambertian((0.7, 0.7, 0.7))),
                            pathtrace.NeuralObject(surface.FieldSurface(f16))], pathtrace.ConstantEnv((1, 1, 1)))
-ms = ev_time(lambda: pathtrace.pathtrace_rows(scene16, pose, 1, 0, 8, 0, 0, 2160, device_out=True), warm=0, it=1)
+ms = ev_time(lambda: pathtrace.pathtrace_rows(scene16, pose, 1, 0, 8, 0, 0, 2160, device_out=True), warm=1, it=2)
 out["config5_pathtrace_3840x2160_spp1_random_init"] = {"ms": ms, "Mpaths_per_s": 3840 * 2160 / ms / 1e3}
 print(json.dumps(out, indent=1))
 json.dump(out, open(os.path.join(ROOT, "gpurun_out", "configs_r1.json"), "w"), indent=1)
