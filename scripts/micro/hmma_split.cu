@@ -91,7 +91,7 @@ __global__ void dot_kernel(const float* __restrict__ X, const float* __restrict_
 
 template <int K>
 void accuracy(const char* what, bool positive_inputs) {
-  const int tiles = 2048, rows = tiles * 64;
+  const int tiles = 8192, rows = tiles * 64;
   std::vector<float> X((size_t)rows * K), W((size_t)K * 32), Y((size_t)rows * 32);
   srand(12345);
   auto u = []() { return (rand() + 0.5) / (RAND_MAX + 1.0); };
@@ -102,21 +102,23 @@ void accuracy(const char* what, bool positive_inputs) {
   }
   double lim = sqrt(6.0 / K);
   for (auto& w : W) w = (float)((2 * u() - 1) * lim);
-  std::vector<double> exact((size_t)rows * 32);
+  std::vector<double> exact((size_t)rows * 32), mag((size_t)rows * 32);
   std::vector<float> chain((size_t)rows * 32);
   for (int r = 0; r < rows; r++)
     for (int n = 0; n < 32; n++) {
-      double s = 0;
+      double s = 0, m = 0;
       float c = 0;
       for (int k = 0; k < K; k++) {
+        m += fabs((double)X[(size_t)r * K + k] * (double)W[k * 32 + n]);
         s += (double)X[(size_t)r * K + k] * (double)W[k * 32 + n];
         c = fmaf(X[(size_t)r * K + k], W[k * 32 + n], c);
       }
       exact[(size_t)r * 32 + n] = s;
+      mag[(size_t)r * 32 + n] = m;
       chain[(size_t)r * 32 + n] = c;
     }
   auto report = [&](const char* name, const float* y) {
-    double se = 0, sa = 0, sb = 0, mx = 0, sabs = 0;
+    double se = 0, sa = 0, sb = 0, mx = 0, sabs = 0, worst_rel = 0;
     size_t n = exact.size(), differ = 0;
     for (size_t i = 0; i < n; i++) {
       double e = (double)y[i] - exact[i];
@@ -124,9 +126,10 @@ void accuracy(const char* what, bool positive_inputs) {
       double eu = e / ulp;
       se += eu * eu; sa += fabs(eu); sb += eu * (exact[i] >= 0 ? 1 : -1); mx = fmax(mx, fabs(eu)); sabs += fabs(e);
       differ += (y[i] != chain[i]);
+      worst_rel = fmax(worst_rel, fabs(e) / (mag[i] + 1e-300));
     }
-    printf("  %-44s mean|e| %.3f ulp  rms %.3f  max %.2f  bias(toward +|y|) %+.3f  mean abs %.3e  differs from fp32 chain %.1f %%\n", name,
-           sa / n, sqrt(se / n), mx, sb / n, sabs / n, 100.0 * differ / n);
+    printf("  %-44s mean|e| %.3f ulp  rms %.3f  max %.2f  bias(toward +|y|) %+.3f  mean abs %.3e  differs from fp32 chain %.1f %%  worst |e| / sum|x w| = %.3e = 2^%.1f\n", name,
+           sa / n, sqrt(se / n), mx, sb / n, sabs / n, 100.0 * differ / n, worst_rel, log2(worst_rel));
   };
   printf("%s (K=%d, %d rows x 32 outputs)\n", what, K, rows);
   report("fp32 k-ordered FMA chain (reference sgemm)", chain.data());
