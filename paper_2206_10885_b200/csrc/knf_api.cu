@@ -222,9 +222,10 @@ static double filter_delta(int pieces, const float* w1, const float* b1, const f
 // softplus' <= 1, so L <= |w3|_2 * |W2|_2 * sup_x |W1 J_enc(x)|_2.  |W2|_2 is bounded by Gershgorin on (W2^T W2)^16
 // (within 2 % of the true spectral norm).  J_enc is block diagonal per axis a: d/dx_a of (x_a, sin(2^o pi x_a),
 // cos(2^o pi x_a))_o = (1, 2^o pi cos, -2^o pi sin)_o; (cos, -sin) is a unit vector, so the axis-a column of W1 J
-// has norm <= |w_raw_a| + sum_o 2^o pi sigma_max([w_sin_o,a | w_cos_o,a]), and for a unit direction the three
-// axes combine by Cauchy-Schwarz.
-static double lipschitz_bound(const float* w1, const float* w2, const float* w3) {
+// has norm <= |w_raw_a| + sum_o 2^o pi sigma_max([w_sin_o,a | w_cos_o,a]).
+// Returns the three per-axis bounds L_a = |w3| |W2| |column a of W1 J|: |d(p) - d(q)| <= sum_a L_a |p_a - q_a| (triangle
+// inequality over the axes -- tighter than one constant times the Euclidean distance for rays near an axis).
+static void lipschitz_bound(const float* w1, const float* w2, const float* w3, double out[3]) {
   double n3 = 0.0;
   for (int k = 0; k < kHidden; k++) n3 += (double)w3[k] * (double)w3[k];
   n3 = std::sqrt(n3);
@@ -261,7 +262,6 @@ static double lipschitz_bound(const float* w1, const float* w2, const float* w3)
   }
   // lambda_max(W2^T W2)^16 <= row * exp(log_scale)  =>  |W2|_2 <= (row * exp(log_scale))^(1/32)
   const double n2 = row > 0.0 ? std::exp((std::log(row) + log_scale) / 32.0) : 0.0;
-  double axes = 0.0;
   for (int a = 0; a < 3; a++) {
     double m = 0.0;
     for (int n = 0; n < kHidden; n++) m += (double)w1[n * kSdfIn + a] * (double)w1[n * kSdfIn + a];
@@ -277,9 +277,8 @@ static double lipschitz_bound(const float* w1, const float* w2, const float* w3)
       const double lam = 0.5 * (aa + bb) + std::sqrt(0.25 * (aa - bb) * (aa - bb) + ab * ab);
       m += std::ldexp(3.14159265358979323846, o) * std::sqrt(lam);
     }
-    axes += m * m;
+    out[a] = 1.001 * n3 * n2 * m + 1e-12;
   }
-  return 1.001 * n3 * n2 * std::sqrt(axes) + 1e-12;
 }
 
 template <int P>
@@ -334,8 +333,12 @@ void pack_sdf_mma(int n_cells, const float* const w[3], const float* const b[3],
     const float delta_f = std::nextafter((float)delta, INFINITY);
     std::memcpy(blob + Blob::b3 + kFilterDeltaSlot, &delta_f, sizeof(float));
     if (delta_max) *delta_max = std::max(*delta_max, (double)delta_f);
-    const float lip_f = std::nextafter((float)lipschitz_bound(w1, w2, w3), INFINITY);
-    std::memcpy(blob + Blob::b3 + kFilterLipSlot, &lip_f, sizeof(float));
+    double lip[3];
+    lipschitz_bound(w1, w2, w3, lip);
+    for (int a = 0; a < 3; a++) {
+      const float lip_f = std::nextafter((float)lip[a], INFINITY);
+      std::memcpy(blob + Blob::b3 + kFilterLipSlot + a, &lip_f, sizeof(float));
+    }
   }
 }
 

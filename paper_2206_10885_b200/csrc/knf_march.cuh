@@ -264,7 +264,8 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
     }
     int n_active = tile.count;
     const float* W3d = reinterpret_cast<const float*>(S.w + Blob::w3d);  // output-layer column 0
-    double safe_below = 0.0, inv_lip = 0.0;
+    double safe_below = 0.0;
+    float lip[3] = {0.f, 0.f, 0.f};
 
     for (int inner = 0;; inner++) {
 #pragma unroll
@@ -281,7 +282,8 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
         parity ^= 1;
         if (FILTER) {
           safe_below = -(A.M.eps + (double)reinterpret_cast<const float*>(S.w + Blob::b3)[kFilterDeltaSlot]);
-          inv_lip = A.max_skip > 0 ? 1.0 / (double)reinterpret_cast<const float*>(S.w + Blob::b3)[kFilterLipSlot] : 0.0;
+#pragma unroll
+          for (int a = 0; a < 3; a++) lip[a] = reinterpret_cast<const float*>(S.w + Blob::b3)[kFilterLipSlot + a];
         }
       }
       const float b3 = reinterpret_cast<const float*>(S.w + Blob::b3)[0];
@@ -312,10 +314,10 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
             cell[q] = tile.cell;  // undecided: the same sample goes to the exact queue of this wavefront
           } else if (code[q] != STEP_DONE) {
             const float x0 = px[q], y0 = py[q], z0 = pz[q];  // where d_f was evaluated
-            // |d(p) - d(p0)| <= L |p - p0| inside the cell (L: proven Lipschitz bound of the cell's network), so every
-            // sample within `reach` of p0 still has an exact distance below -eps: the reference's evaluation there can
-            // only say "keep crawling", and its step is taken without evaluating (certified skip).
-            const double reach = FILTER ? (safe_below - (double)(q ? dist.y : dist.x)) * inv_lip : 0.0;
+            // |d(p) - d(p0)| <= sum_a L_a |p_a - p0_a| inside the cell (L_a: proven per-axis Lipschitz bounds of the cell's
+            // network), so every sample whose bound stays below `room` still has an exact distance below -eps: the
+            // reference's evaluation there can only say "keep crawling", and its step is taken without evaluating.
+            const double room = (FILTER && A.max_skip > 0) ? safe_below - (double)(q ? dist.y : dist.x) : 0.0;
             for (;;) {
               px[q] = __double2float_rn(S.od[0][32 * q + lane] + t_next * S.od[3][32 * q + lane]);
               py[q] = __double2float_rn(S.od[1][32 * q + lane] + t_next * S.od[4][32 * q + lane]);
@@ -324,9 +326,9 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
                                        pz[q] > in_lo[2] && pz[q] < in_hi[2];
               cell[q] = well_inside ? tile.cell : cell_of_slow(px[q], py[q], pz[q], A.G.lo[0], A.G.lo[1], A.G.lo[2], A.G.hi[0], A.G.hi[1], A.G.hi[2], A.G.resolution);
               if (!FILTER || !well_inside) break;
-              const float dx = px[q] - x0, dy = py[q] - y0, dz = pz[q] - z0;
-              const float far = sqrtf(dx * dx + dy * dy + dz * dz);
-              if (!((double)far * 1.00001 + 1e-6 < reach)) break;
+              // (+ 1e-6 per axis: the fp32 roundings of the two points; * 1.00001: the fp32 arithmetic of this line)
+              const float rise = lip[0] * (fabsf(px[q] - x0) + 1e-6f) + lip[1] * (fabsf(py[q] - y0) + 1e-6f) + lip[2] * (fabsf(pz[q] - z0) + 1e-6f);
+              if (!((double)rise * 1.00001 < room)) break;
               // the reference's march step at t_next (surface.py:217-223) with max(d, eps/2) = eps/2
               rr[q].steps += 1;
               rr[q].t_prev = rr[q].t;

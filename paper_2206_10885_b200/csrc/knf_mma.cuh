@@ -51,7 +51,7 @@ struct MmaBlobT {
   static constexpr int b2 = b1 + kHidden;
   static constexpr int w3d = b2 + kHidden;
   static constexpr int b3 = w3d + kHidden;
-  static constexpr int march_words = b3 + kSdfOutPad;  // what a march kernel needs: P = 3: 2956 (11824 B... see bytes), P = 2: 2668 (10672 B)
+  static constexpr int march_words = b3 + kSdfOutPad + 4;  // + 4 words of filter constants  // what a march kernel needs: P = 3: 2956 (11824 B... see bytes), P = 2: 2668 (10672 B)
   static constexpr int w3 = march_words;
   static constexpr int words = w3 + kHidden * kSdfOutPad;  // P = 3: 4332 (17328 B); P = 2: 3052 (12208 B)
   static constexpr int bytes = words * 4;
@@ -60,8 +60,9 @@ struct MmaBlobT {
 };
 using MmaBlob = MmaBlobT<3>;
 using MmaBlobH = MmaBlobT<2>;
-constexpr int kFilterDeltaSlot = kSdfOutPad - 1;  // b3[11]: proven bound on |tensor distance - exact distance| in this cell
-constexpr int kFilterLipSlot = kSdfOutPad - 2;    // b3[10]: proven Lipschitz bound of the cell's distance network
+// per-cell constants of the decision filter, stored after b3 (b3[9..11] = per-axis Lipschitz bounds, then 4 words):
+constexpr int kFilterLipSlot = kSdfOut;           // b3[9 + a]: proven bound on |d d / d x_a| over the cell, a = 0, 1, 2
+constexpr int kFilterDeltaSlot = kSdfOutPad;      // b3[12]: proven bound on |tensor distance - exact distance| in this cell
 constexpr float kHalfPieceScale = 2048.0f;  // 2^11: the fp16 second piece carries (x - x1) * 2^11
 
 // Which reference feature (nn.fourier_encode column, nn.py:84-93) sits at position `kslot` of k-tile
