@@ -82,7 +82,7 @@ int ensure_requests(Field& F, size_t n) {
   KNF_TRY(W.req_cell.ensure(n * sizeof(int)));
   KNF_TRY(W.req_rank.ensure(n * sizeof(int)));
   KNF_TRY(W.perm.ensure(n * sizeof(int)));
-  KNF_TRY(W.tiles.ensure((n / kTilePts + 3 * (size_t)F.geom.n_cells + 2) * sizeof(Tile)));  // <= 3 small tiles per cell remainder
+  KNF_TRY(W.tiles.ensure((n / kSmallTile + (size_t)F.geom.n_cells + 2) * sizeof(Tile)));  // worst case: every tile holds <= 16 requests
   bool fresh = W.cell_count.p == nullptr;
   KNF_TRY(W.cell_count.ensure((size_t)F.geom.n_cells * sizeof(int)));
   KNF_TRY(W.cell_offset.ensure(((size_t)F.geom.n_cells + 1) * sizeof(int)));
@@ -171,6 +171,7 @@ int begin_call(Field& F, cudaStream_t st) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ColKernelSmem)));
     KNF_CUDA(cudaFuncSetAttribute(march_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sizeof(SdfKernelSmem)));
+    KNF_CUDA(cudaFuncSetAttribute(march_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SdfSmallSmem)));
     KNF_CUDA(cudaFuncSetAttribute(march_mma_kernel<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaMarchSmemT<3>)));
     KNF_CUDA(cudaFuncSetAttribute(sdf_mma_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<3>)));
     KNF_CUDA(cudaFuncSetAttribute(march_mma_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaMarchSmemT<2>)));
@@ -255,7 +256,7 @@ int launch_scan_scatter(Field& F, const RouteBuffers& R, size_t n_upper, cudaStr
 }
 
 static inline int mlp_grid(const Field& F, size_t n_upper, int ctas_per_sm = kWarpCtasPerSm) {
-  size_t tiles_upper = n_upper / kTilePts + std::min<size_t>(n_upper, 3 * (size_t)F.geom.n_cells) + 1;
+  size_t tiles_upper = n_upper / kSmallTile + std::min<size_t>(n_upper, (size_t)F.geom.n_cells) + 1;
   return (int)std::max<size_t>(1, std::min<size_t>(tiles_upper, (size_t)148 * ctas_per_sm));
 }
 
@@ -377,6 +378,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
   const bool probing = use_filter && F.filter_mode == 2 && F.filter_hint == 0;
   size_t seen_filter = 0, seen_total = 0;
   bool filter_drained = false;  // the filter queue was seen empty after the filter had been switched off
+  bool exact_sparse = false;    // last poll: the exact queue holds < 1/16 of the rays -> small-tile-only kernel
   const double crawl_on = -(s.eps_hit + 2.0 * F.filter_delta_max);
   // Global wavefronts.  Every ray queued in a wavefront either advances a step or (once each) fetches its secant /
   // re-check sample, so max_steps + 3 bounds the count; tile residency usually finishes in far fewer, which the
@@ -420,7 +422,8 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     }
     RouteBuffers R = route_buffers(F, cur, nxt, cur);
     R.eval_counter = stat_counter(F, 3);  // requests that went through global routing
-    R.small_tiles = exact_mode ? 1 : 0;   // march_warp_kernel has the 16-point path
+    const bool small_only = exact_mode && exact_sparse && F.sparse_small_kernel;
+    R.small_tiles = exact_mode ? (small_only ? 2 : 1) : 0;  // march_warp_kernel has the 16-point path, march_small_kernel only that
     KNF_TRY(launch_scan_scatter(F, R, (size_t)n, st));
     A.P.blobs = F.sdf_blobs;
     A.P.perm = R.perm;
@@ -436,6 +439,8 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
       } else if (F.precision == KNF_PRECISION_TENSOR_FP16X2) {
         A.P.blobs = reinterpret_cast<const float*>(F.sdf_mmah_blobs);
         march_mma_kernel<2, false><<<mlp_grid(F, (size_t)n, march_ctas_per_sm<2>()), 32, sizeof(MmaMarchSmemT<2>), st>>>(A);
+      } else if (small_only) {
+        march_small_kernel<<<mlp_grid(F, (size_t)n, kSmallCtasPerSm), 32, sizeof(SdfSmallSmem), st>>>(A);
       } else {
         march_warp_kernel<<<mlp_grid(F, (size_t)n), 32, sizeof(SdfKernelSmem), st>>>(A);
       }
@@ -455,6 +460,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
         seen_total = (size_t)n_exact + (size_t)n_filter;
       }
       if (n_exact == 0 && n_filter == 0) break;
+      exact_sparse = (size_t)n_exact * 16 < (size_t)n;
       if (probing && w == 0 && (size_t)n_filter * 8 < (size_t)(n_exact + n_filter)) use_filter = false;  // < 1/8 of the live rays crawl
       if (!use_filter && n_filter == 0) filter_drained = true;
     }

@@ -53,10 +53,11 @@ __device__ __forceinline__ void march_emit(const RouteBuffers& Q, int* live, boo
 // SMALL = true: up to 16 rays, one in each of lanes 0..15 (panel column = lane), evaluated by the 4 x 4 register
 // tiles of knf_mlp.cuh -- a quarter of the work for the sparse tiles that dominate once the decision filter has
 // taken the crawling rays away.
-template <bool SMALL>
-__device__ __forceinline__ void march_exact_tile(const MarchTileArgs& A, MlpSmem<kSdfIn, kSdfOutPad>& S, const Tile& tile, int lane,
+template <bool SMALL, class SmemT, int PLD>
+__device__ __forceinline__ void march_exact_tile(const MarchTileArgs& A, SmemT& S, const Tile& tile, int lane,
                                                  uint32_t& parity, unsigned long long& evals, unsigned long long& slots) {
   using Blob = SdfBlob;
+  static_assert(SMALL || PLD == kPanelLd, "the 64-point path needs the full panel");
   constexpr int NQ = SMALL ? 1 : 2;
   const MlpParams& P = A.P;
   float* X = S.x;
@@ -78,7 +79,12 @@ __device__ __forceinline__ void march_exact_tile(const MarchTileArgs& A, MlpSmem
       ray_load(rr[q], A.M, ray[q]);  // in flight during the first MLP pass
     }
   }
-  zero_pad_rows<kSdfIn>(X, lane);
+  if (PLD == kPanelLd) {
+    zero_pad_rows<kSdfIn>(X, lane);
+  } else if (lane < kSmallTilePts) {
+#pragma unroll
+    for (int r = kSdfIn; r < pad_k(kSdfIn); r++) X[r * PLD + lane] = 0.f;
+  }
   // fp32 box strictly inside the tile's cell: a point inside it is in this cell without redoing the
   // fp64 cell arithmetic (cell_coord is monotone and its rounding error is ~1e-16 of the extent, the
   // margin is 1e-6 of it); anything closer to a face takes the exact path.
@@ -98,7 +104,7 @@ __device__ __forceinline__ void march_exact_tile(const MarchTileArgs& A, MlpSmem
 
   for (int inner = 0;; inner++) {
     if (SMALL) {
-      if (lane < kSmallTilePts) encode_into<kSdfFreqs>(X, 0, lane, px[0], py[0], pz[0]);
+      if (lane < kSmallTilePts) encode_into<kSdfFreqs, PLD>(X, 0, lane, px[0], py[0], pz[0]);
     } else {
 #pragma unroll
       for (int q = 0; q < NQ; q++) encode_into<kSdfFreqs>(X, 0, col[q], px[q], py[q], pz[q]);
@@ -110,9 +116,9 @@ __device__ __forceinline__ void march_exact_tile(const MarchTileArgs& A, MlpSmem
     }
     float dist[NQ];
     if (SMALL) {
-      hidden_layers_small<kSdfIn, kSdfOutPad, ACT_SOFTPLUS>(X, S.w, lane);
-      dist[0] = lane < kSmallTilePts ? output_distance_col<kSdfOutPad>(X, S.w + Blob::w3, S.w + Blob::b3, lane) : 0.0f;
-    } else {
+      hidden_layers_small<kSdfIn, kSdfOutPad, ACT_SOFTPLUS, PLD>(X, S.w, lane);
+      dist[0] = lane < kSmallTilePts ? output_distance_col<kSdfOutPad, PLD>(X, S.w + Blob::w3, S.w + Blob::b3, lane) : 0.0f;
+    } else if (PLD == kPanelLd) {
       hidden_layers<kSdfIn, kSdfOutPad, ACT_SOFTPLUS>(X, S.w, lane);
       const float2 d2 = output_distance<kSdfOutPad>(X, S.w + Blob::w3, S.w + Blob::b3, lane);
       dist[0] = d2.x;
@@ -181,13 +187,48 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(M
     if (t >= n_tiles) break;
     const Tile tile = P.tiles[t];
     fetch_weights<Blob>(S.w, P.blobs, tile.cell, &S.bar, lane);
-    if (tile.count <= kSmallTilePts) march_exact_tile<true>(A, S, tile, lane, parity, evals, slots);
-    else march_exact_tile<false>(A, S, tile, lane, parity, evals, slots);
+    if (tile.count <= kSmallTilePts) march_exact_tile<true, Smem, kPanelLd>(A, S, tile, lane, parity, evals, slots);
+    else march_exact_tile<false, Smem, kPanelLd>(A, S, tile, lane, parity, evals, slots);
     __syncwarp();  // every lane is done reading S.w and the panel before the next tile overwrites them
   }
   if (lane == 0 && evals && A.eval_counter) {
     atomicAdd(A.eval_counter, evals);
     atomicAdd(A.eval_counter + 2, slots);  // lane slots spent (tile-fill statistic)
+  }
+}
+
+// The exact kernel for SPARSE wavefronts: every tile was cut to <= 16 requests (RouteBuffers::small_tiles = 2) and this
+// kernel holds nothing but the 4 x 4 path -- 14.3 KB of shared memory, half the registers and less than half the
+// instruction footprint of march_warp_kernel, whose top stall in such wavefronts was instruction fetch.
+#ifndef KNF_SMALL_CTAS_PER_SM
+#define KNF_SMALL_CTAS_PER_SM 14
+#endif
+constexpr int kSmallCtasPerSm = KNF_SMALL_CTAS_PER_SM;
+static __global__ void __launch_bounds__(32, kSmallCtasPerSm) march_small_kernel(MarchTileArgs A) {
+  using Blob = SdfBlob;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SdfSmallSmem& S = *reinterpret_cast<SdfSmallSmem*>(smem_raw);
+  const int lane = threadIdx.x;
+  if (lane == 0) {
+    mbar_init(&S.bar, 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  const MlpParams& P = A.P;
+  const int n_tiles = P.ctr->n_tiles;
+  uint32_t parity = 0;
+  unsigned long long evals = 0, slots = 0;
+  for (;;) {
+    const int t = next_tile(P.ctr, lane);
+    if (t >= n_tiles) break;
+    const Tile tile = P.tiles[t];
+    fetch_weights<Blob>(S.w, P.blobs, tile.cell, &S.bar, lane);
+    march_exact_tile<true, SdfSmallSmem, kSmallPanelLd>(A, S, tile, lane, parity, evals, slots);
+    __syncwarp();
+  }
+  if (lane == 0 && evals && A.eval_counter) {
+    atomicAdd(A.eval_counter, evals);
+    atomicAdd(A.eval_counter + 2, slots);
   }
 }
 

@@ -162,8 +162,9 @@ static __device__ __noinline__ void softplus_panel(float* __restrict__ panel, in
 // nn.fourier_encode (nn.py:66-93) of a 3-vector into panel rows [row0, row0 + 3 + 6*L) at column p.
 // __noinline__ (one copy per instantiation): three sin/cos evaluations and the recurrence are ~300 instructions, and
 // the exact kernel used to inline them three times.
-template <int L>
+template <int L, int PLD = kPanelLd>
 static __device__ __noinline__ void encode_into(float* __restrict__ panel, int row0, int p, float x, float y, float z) {
+  constexpr int kPanelLd = PLD;  // row stride of this panel
   const float pi_f = 3.14159274101257324e+00f;  // float32(np.pi)
   panel[(row0 + 0) * kPanelLd + p] = x;
   panel[(row0 + 1) * kPanelLd + p] = y;
@@ -202,9 +203,12 @@ __device__ __forceinline__ void zero_pad_rows(float* __restrict__ X, int lane) {
 // the rounded bias add, so a point's value does not depend on which tile shape evaluated it.
 constexpr int kSmallTilePts = 16;
 
-template <int K>
+constexpr int kSmallPanelLd = kSmallTilePts + 4;  // 20: row stride of the compact panel of the small-tile kernel
+
+template <int K, int PLD>
 __device__ __forceinline__ void layer_4x4(const float* __restrict__ In, const float* __restrict__ Wt, int pg, int ng,
                                           float2 (&acc)[2][4]) {
+  constexpr int kPanelLd = PLD;
   static_assert(K % 8 == 0, "pad K to a multiple of 8");
 #pragma unroll
   for (int i = 0; i < 2; i++)
@@ -229,9 +233,10 @@ __device__ __forceinline__ void layer_4x4(const float* __restrict__ In, const fl
   }
 }
 
-template <int ACT>
+template <int ACT, int PLD>
 __device__ __forceinline__ void store_hidden_small(float2 (&acc)[2][4], const float* __restrict__ bias, float* __restrict__ Out,
                                                    int pg, int ng) {
+  constexpr int kPanelLd = PLD;
 #pragma unroll
   for (int j = 0; j < 4; j++) {
     const int neuron = ng * 4 + j;
@@ -246,7 +251,9 @@ __device__ __forceinline__ void store_hidden_small(float2 (&acc)[2][4], const fl
 }
 
 // In-place softplus over panel rows 0..31, columns 0..15: lane owns columns 2 (lane & 7), +1 of rows (lane >> 3) + 4 i.
+template <int PLD>
 static __device__ __noinline__ void softplus_panel_small(float* __restrict__ panel, int lane) {
+  constexpr int kPanelLd = PLD;
   float* base = panel + (lane >> 3) * kPanelLd + 2 * (lane & 7);
 #pragma unroll 1
   for (int i0 = 0; i0 < 8; i0 += 4) {
@@ -259,34 +266,35 @@ static __device__ __noinline__ void softplus_panel_small(float* __restrict__ pan
   }
 }
 
-template <int K1, int N3P, int HIDDEN_ACT>
+template <int K1, int N3P, int HIDDEN_ACT, int PLD>
 __device__ __forceinline__ void hidden_layers_small(float* __restrict__ X, const float* __restrict__ W, int lane) {
   using Blob = BlobLayout<K1, N3P>;
   const int pg = lane >> 3;  // 4 point groups of 4 points
   const int ng = lane & 7;   // 8 neuron groups of 4 neurons
   float2 acc[2][4];
-  layer_4x4<pad_k(K1)>(X, W + Blob::w1, pg, ng, acc);
+  layer_4x4<pad_k(K1), PLD>(X, W + Blob::w1, pg, ng, acc);
   __syncwarp();
-  store_hidden_small<HIDDEN_ACT>(acc, W + Blob::b1, X, pg, ng);
+  store_hidden_small<HIDDEN_ACT, PLD>(acc, W + Blob::b1, X, pg, ng);
   __syncwarp();
   if (HIDDEN_ACT == ACT_SOFTPLUS) {
-    softplus_panel_small(X, lane);
+    softplus_panel_small<PLD>(X, lane);
     __syncwarp();
   }
-  layer_4x4<kHidden>(X, W + Blob::w2, pg, ng, acc);
+  layer_4x4<kHidden, PLD>(X, W + Blob::w2, pg, ng, acc);
   __syncwarp();
-  store_hidden_small<HIDDEN_ACT>(acc, W + Blob::b2, X, pg, ng);
+  store_hidden_small<HIDDEN_ACT, PLD>(acc, W + Blob::b2, X, pg, ng);
   __syncwarp();
   if (HIDDEN_ACT == ACT_SOFTPLUS) {
-    softplus_panel_small(X, lane);
+    softplus_panel_small<PLD>(X, lane);
     __syncwarp();  // the output layer reads column `lane`, written by other lanes
   }
 }
 
 // Output 0 (the distance) of the 32 -> N3 layer for panel column p (same chain as output_distance).
-template <int N3P>
+template <int N3P, int PLD>
 __device__ __forceinline__ float output_distance_col(const float* __restrict__ X, const float* __restrict__ W3,
                                                      const float* __restrict__ B3, int p) {
+  constexpr int kPanelLd = PLD;
   float d = 0.0f;
 #pragma unroll 8
   for (int k = 0; k < kHidden; k++) d = __fmaf_rn(X[k * kPanelLd + p], W3[k * N3P], d);
@@ -454,7 +462,16 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) mlp_warp_kernel(Mlp
   }
 }
 
+// Shared memory of the small-tile-only kernel: the same weight blob, a 40 x 20 panel -- 14.3 KB, 14 one-warp CTAs per SM.
+template <int K1, int N3P>
+struct SmallSmem {
+  using Blob = BlobLayout<K1, N3P>;
+  alignas(16) float w[Blob::floats];
+  alignas(16) float x[pad_k(K1) * kSmallPanelLd];
+  alignas(8) uint64_t bar;
+};
 using SdfKernelSmem = MlpSmem<kSdfIn, kSdfOutPad>;
+using SdfSmallSmem = SmallSmem<kSdfIn, kSdfOutPad>;
 using ColKernelSmem = MlpSmem<kColIn, kColOutPad>;
 
 }  // namespace knf

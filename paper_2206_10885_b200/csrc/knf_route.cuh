@@ -31,13 +31,14 @@ struct RouteBuffers {
   RouteCounters* ctr; // this pass
   RouteCounters* next_ctr;  // zeroed by scan (may equal nullptr)
   unsigned long long* eval_counter;  // += n_requests per pass (nullable); statistics only
-  int small_tiles;    // cut the last < 49 requests of a cell into tiles of <= 16 (kernels with a small-tile path)
+  int small_tiles;    // 1: cut the last < 49 requests of a cell into tiles of <= 16 (kernels with a small-tile path); 2: every tile <= 16
 };
 
 // How a cell's k requests are cut into tiles: full 64-request tiles, then the remainder r either as one tile
 // (r >= 49, or small tiles off) or as ceil(r / 16) tiles of <= 16 requests.
 constexpr int kSmallTile = 16, kSmallTileMaxRemainder = 48;
 __device__ __forceinline__ int tiles_of_cell(int k, int small_tiles) {
+  if (small_tiles == 2) return (k + kSmallTile - 1) / kSmallTile;
   const int full = k / kTilePts, r = k - full * kTilePts;
   if (r == 0) return full;
   return full + ((small_tiles && r <= kSmallTileMaxRemainder) ? (r + kSmallTile - 1) / kSmallTile : 1);
@@ -205,7 +206,8 @@ static __global__ void route_scatter_kernel(RouteBuffers R, int n_cells) {
     int tb = R.tile_base[c];
     for (int s = 0; s < k;) {
       const int left = k - s;
-      const int take = left >= kTilePts ? kTilePts : ((R.small_tiles && left <= kSmallTileMaxRemainder) ? min(kSmallTile, left) : left);
+      const int take = R.small_tiles == 2 ? min(kSmallTile, left)
+                                          : (left >= kTilePts ? kTilePts : ((R.small_tiles && left <= kSmallTileMaxRemainder) ? min(kSmallTile, left) : left));
       Tile t;
       t.cell = c;
       t.start = start + s;
