@@ -117,6 +117,7 @@ typedef struct {
   int64_t filter_evals;
   int64_t filter_deferred;
   int64_t filter_skipped; /* march steps taken without any evaluation: certified by the cell's Lipschitz bound */
+  int64_t filter_lane_slots; /* 16 x m-tiles the filter kernel computed: filter_evals / this = its tile fill */
   int64_t filter_launches;
   double filter_ms;
 } KnfStats;

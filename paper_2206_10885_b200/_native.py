@@ -91,6 +91,7 @@ class KnfStats(C.Structure):
         ("filter_evals", C.c_int64),
         ("filter_deferred", C.c_int64),
         ("filter_skipped", C.c_int64),
+        ("filter_lane_slots", C.c_int64),
         ("filter_launches", C.c_int64),
         ("filter_ms", C.c_double),
     ]

@@ -242,6 +242,7 @@ int finish_stats(Field& F, cudaStream_t st) {
   F.stats.filter_evals = (int64_t)host[4];
   F.stats.filter_deferred = (int64_t)host[5];
   F.stats.filter_skipped = (int64_t)host[6];
+  F.stats.filter_lane_slots = (int64_t)host[7];
   return 0;
 }
 
@@ -423,7 +424,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     RouteBuffers R = route_buffers(F, cur, nxt, cur);
     R.eval_counter = stat_counter(F, 3);  // requests that went through global routing
     const bool small_only = exact_mode && exact_sparse && F.sparse_small_kernel;
-    R.small_tiles = exact_mode ? (small_only ? 2 : 1) : 0;  // march_warp_kernel has the 16-point path, march_small_kernel only that
+    R.small_tiles = small_only ? 2 : 0;  // dense wavefronts: 64-request tiles for march_warp_kernel; sparse: <= 16 for march_small_kernel
     KNF_TRY(launch_scan_scatter(F, R, (size_t)n, st));
     A.P.blobs = F.sdf_blobs;
     A.P.perm = R.perm;
@@ -460,7 +461,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
         seen_total = (size_t)n_exact + (size_t)n_filter;
       }
       if (n_exact == 0 && n_filter == 0) break;
-      exact_sparse = (size_t)n_exact * 16 < (size_t)n;
+      exact_sparse = (size_t)n_exact * (size_t)F.sparse_div < (size_t)n;
       if (probing && w == 0 && (size_t)n_filter * 8 < (size_t)(n_exact + n_filter)) use_filter = false;  // < 1/8 of the live rays crawl
       if (!use_filter && n_filter == 0) filter_drained = true;
     }

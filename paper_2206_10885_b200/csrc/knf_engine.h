@@ -68,6 +68,7 @@ struct Field {
   uint32_t* sdf_mmah_blobs = nullptr;  // MmaBlobT<2> per cell (fp16 x 2 B fragments); null when a weight exceeds the fp16 range
   bool fp16_ok = false;
   double filter_delta_max = 0.0;       // largest per-cell decision-filter bound (knf_api.cu filter_delta)
+  int sparse_div = 8;                  // a wavefront is sparse when its exact queue holds < n / sparse_div rays (KNF_SPARSE_DIV)
   bool sparse_small_kernel = true;     // exact march: sparse wavefronts by march_small_kernel (KNF_SPARSE_SMALL=0 disables)
   bool filter_skip = true;             // certified (Lipschitz) skipping inside the filter; KNF_FILTER_SKIP=0 disables
   int filter_hint = 0;                 // auto mode: what the previous march on this handle learnt (0 unknown, 1 rays crawl, 2 they do not)

@@ -30,7 +30,7 @@ struct MarchTileArgs {
   int* live_out;            // ... of `next`
   int* live_filter;         // ... of `next_filter`
   int* live_defer;          // ... of `defer`
-  unsigned long long* eval_counter;  // statistics: [0] SDF evaluations, [2] lane slots, [4] filter evaluations, [5] deferred, [6] certified skips
+  unsigned long long* eval_counter;  // statistics: [0] SDF evaluations, [2] lane slots, [4] filter evaluations, [5] deferred, [6] certified skips, [7] filter lane slots
   int max_inner;            // cap on consecutive in-place steps of one tile
   int max_skip;             // filter kernel: 0 disables certified skipping
   double inv_resolution;    // 1 / grid resolution (host-computed)
@@ -187,8 +187,11 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(M
     if (t >= n_tiles) break;
     const Tile tile = P.tiles[t];
     fetch_weights<Blob>(S.w, P.blobs, tile.cell, &S.bar, lane);
+#ifdef KNF_MIXED_TILE_KERNEL
     if (tile.count <= kSmallTilePts) march_exact_tile<true, Smem, kPanelLd>(A, S, tile, lane, parity, evals, slots);
-    else march_exact_tile<false, Smem, kPanelLd>(A, S, tile, lane, parity, evals, slots);
+    else
+#endif
+      march_exact_tile<false, Smem, kPanelLd>(A, S, tile, lane, parity, evals, slots);  // one tile shape per kernel: half the instruction footprint
     __syncwarp();  // every lane is done reading S.w and the panel before the next tile overwrites them
   }
   if (lane == 0 && evals && A.eval_counter) {
@@ -424,6 +427,7 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
       if (FILTER) {
         atomicAdd(A.eval_counter + 5, deferred);
         atomicAdd(A.eval_counter + 6, skipped);
+        atomicAdd(A.eval_counter + 7, slots);
       }
       else atomicAdd(A.eval_counter + 2, slots);
     }

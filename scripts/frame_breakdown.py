@@ -25,6 +25,7 @@ fs.dev.set_profiling(True); fs.dev.reset_stats()
 n = 10
 ms = loop(n)
 s = fs.dev.stats()
+print("filter fill %.3f exact fill %.3f" % (s["filter_evals"] / max(s["filter_lane_slots"], 1), s["sdf_evals"] / max(s["march_lane_slots"], 1)))
 print("frame %.2f ms | exact kernel %.2f ms (%d launches, %.1f M evals) | filter %.2f ms (%d launches, %.1f M evals, %.2f M deferred) | route %.2f ms (%d) | colour %.2f | other %.2f | wavefronts %d launches %d"
       % (ms, s["sdf_mlp_ms"] / n, s["sdf_mlp_launches"] / n, s["sdf_evals"] / n / 1e6, s["filter_ms"] / n, s["filter_launches"] / n, s["filter_evals"] / n / 1e6,
          s["filter_deferred"] / n / 1e6, s["route_ms"] / n, s["route_launches"] / n, s["color_mlp_ms"] / n, s["other_ms"] / n, s["wavefronts"] / n, s["kernel_launches"] / n))

@@ -49,7 +49,7 @@ def test_struct_sizes_match_c_layout():
 
     assert ctypes.sizeof(N.KnfCamera) == 3 * 8 + 9 * 8 + 8 + 4 + 4
     assert ctypes.sizeof(N.KnfSettings) == 24
-    assert ctypes.sizeof(N.KnfStats) == 112 + 5 * 8  # + filter_evals, filter_deferred, filter_skipped, filter_launches, filter_ms
+    assert ctypes.sizeof(N.KnfStats) == 112 + 6 * 8  # + filter_evals, filter_deferred, filter_skipped, filter_lane_slots, filter_launches, filter_ms
     assert ctypes.sizeof(N.KnfFieldDesc) == 8 + 48 + 16 + 8 + 12 * 8
 
 
