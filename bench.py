@@ -325,21 +325,21 @@ def main():
         # what the reference evaluates for the same frames: every crawl step the filter decided or certified counts once
         ref_evals = stats["sdf_evals"] + stats["filter_evals"] - stats["filter_deferred"] + stats["filter_skipped"]
         roof_exact = {
-            "kernel": "march_warp_kernel / mlp_warp_kernel (fused encode + 3-layer SDF MLP as k-ordered fp32 FMA chains + NumPy-exact softplus + sphere-trace step)",
+            "kernel": "march_warp_kernel + march_small_kernel / mlp_warp_kernel (fused encode + 3-layer SDF MLP as k-ordered fp32 FMA chains + NumPy-exact softplus + sphere-trace step)",
             "bound": "fp32", "achieved": exact_tflops, "peak": ffma_peak, "unit": "TFLOP/s", "frac": (exact_tflops / ffma_peak) if exact_tflops else None,
             "peak_source": f"derived: {SM_COUNT} SMs x {FFMA_LANES_PER_SM} FFMA lanes x 2 x sm_max_mhz ({peak_src} MEASURED_PEAKS.json holds HBM and bf16-tensor "
                            "peaks only); measured attainable FP32 rates on this pool: 71.0 TFLOP/s packed FFMA2, 52.0 with one LDS.128 per 16 FFMA2 (profiles/ffma_peak_micro_r1.txt)",
             "evals": int(stats["sdf_evals"]), "launches": int(stats["sdf_mlp_launches"]), "avg_launch_ms": stats["sdf_mlp_ms"] / max(stats["sdf_mlp_launches"], 1),
             "share_of_step": stats["sdf_mlp_ms"] / ms, "tile_fill": stats["sdf_evals"] / max(stats["march_lane_slots"], 1),
-            "note": "after the decision filter only ~4 % of the evaluations reach this kernel, in sparse tiles (tile_fill): achieved counts useful evaluations only",
+            "note": "after the decision filter only ~3 % of the evaluations reach these kernels, mostly in sparse <= 16-request tiles (tile_fill): achieved counts useful evaluations only",
         }
         roof_filter = {
             "kernel": "march_mma_kernel<2, filter> (decision filter: Fourier recurrence + fp16x2 split mma.sync.m16n8k16 layers chained in registers + MUFU softplus "
                       "+ sphere-trace crawl step + certified skipping)",
             "bound": "tensor", "achieved": filter_tflops, "peak": tensor_peak, "unit": "TFLOP/s", "frac": (filter_tflops / tensor_peak) if filter_tflops else None,
-            "traffic": 215.7e6,
-            "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of ONE dense filter launch (1.14 ms under ncu, ~13 M evaluations) from "
-                            "profiles/ncu_r1_filter_v3.summary.txt (ncu --set full); weights (50 MB of fp16 fragments) and ray state are L2-resident, DRAM is 2.3 % busy",
+            "traffic": 206.1e6,
+            "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of ONE dense filter launch (1.06 ms under ncu, ~12 M evaluations) from "
+                            "profiles/ncu_r1_filter_v3.summary.txt (ncu --set full); weights (50 MB of fp16 fragments) and ray state are L2-resident, DRAM is 2 % busy",
             "peak_source": f"{peak_src} MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS, tcgen05 path); mma.sync (HMMA.16816) issue peak measured on this pool: "
                            "553 TFLOP/s (profiles/hmma_split_r1.txt)",
             "algorithmic_flop_per_launch": stats["filter_evals"] * FLOP_PER_SDF_EVAL / max(stats["filter_launches"], 1),

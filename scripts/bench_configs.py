@@ -23,7 +23,7 @@ for name, field in (("random_init_16", f16), ("distilled_4", fd)):
     def orbit():
         for k in range(100):
             surface.render_rows(fs, cameras.orbit_pose(k, 100, 2.5, 0.2, np.deg2rad(40), 800, 800), surface.RenderSettings(), (1, 1, 1), 1, 0, 800, device_out=True)
-    ms = ev_time(orbit, warm=0, it=1)
+    ms = ev_time(orbit, warm=1, it=1)
     out[f"config2_orbit_800x800_100views_{name}"] = {"ms_total": ms, "fps": 100e3 / ms, "mrays_per_s": 100 * 640000 / ms / 1e3}
 # config 4: batched forward sweep
 dev = grid.device_field(f16)
