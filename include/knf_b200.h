@@ -189,6 +189,12 @@ int knf_fourier_encode(const float* x, int64_t n, int32_t L, float* out, int dev
 int knf_softplus(const float* x, int64_t n, float* out, int device, int mem, void* stream);
 int knf_sigmoid(const float* x, int64_t n, float* out, int device, int mem, void* stream);
 
+/* north_star subsystem 2 ("also emits the SDF gradient"): the ANALYTIC gradient of the owning cell's SDF network at each
+ * fp32 point, by forward-mode differentiation through nn.fourier_encode and the softplus layers (no reference
+ * counterpart: grid.grad_fd, grid.py:440-451, is a global finite difference and stays the parity path).  dist (n) may
+ * be NULL; grad is (n,3) fp32. */
+int knf_sdf_gradient(knf_field_t f, const float* pts, int64_t n, float* dist, float* grad, int mem, void* stream);
+
 /* ---- FD normals: grid.py:416-461 ---------------------------------------------------------- */
 /* grid.grad_fd (grid.py:440-451): pts (n,3) f64 -> grad (n,3) f64. */
 int knf_fd_gradient(knf_field_t f, const double* pts, int64_t n, double* grad, int mem, void* stream);

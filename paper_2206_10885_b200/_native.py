@@ -136,6 +136,7 @@ _SIGNATURES = {
     "knf_route": [_P, _P, _I64, _P, _P, _P, _P, _P, _I32, _P],
     "knf_sdf_forward": [_P, _P, _I64, _P, _I32, _P],
     "knf_sdf_values": [_P, _P, _I64, _P, _I32, _P],
+    "knf_sdf_gradient": [_P, _P, _I64, _P, _P, _I32, _P],
     "knf_color_forward": [_P, _P, _P, _P, _P, _I64, _P, _I32, _P],
     "knf_fourier_encode": [_P, _I64, C.c_int32, _P, _I32, _I32, _P],
     "knf_softplus": [_P, _I64, _P, _I32, _I32, _P],

@@ -10,6 +10,7 @@
 
 #include "knf_engine.h"
 #include "knf_mlp.cuh"
+#include "knf_grad.cuh"
 #include "knf_mma.cuh"
 #include "knf_rays.cuh"
 
@@ -864,6 +865,44 @@ int knf_sdf_values(knf_field_t f, const float* pts, int64_t n, float* dist, int 
   float* dd = S.out(dist, (size_t)n);
   if (S.rc) return S.rc;
   KNF_TRY(sdf_forward_device(F, dp, n, nullptr, dd, nullptr, st));
+  return S.finish();
+}
+
+int knf_sdf_gradient(knf_field_t f, const float* pts, int64_t n, float* dist, float* grad, int mem, void* stream) {
+  KNF_TRY(check_field(f));
+  if (n < 0 || (n > 0 && (!pts || !grad))) return fail(KNF_E_INVALID, "bad arguments to knf_sdf_gradient");
+  if (n == 0) return 0;
+  if (n > INT32_MAX / 16) return fail(KNF_E_INVALID, "too many points for one call");
+  Field& F = f->f;
+  std::lock_guard<std::mutex> lk(F.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  KNF_TRY(begin_call(F, st));
+  Stager S(&F, mem, st);
+  const float* dp = S.in(pts, (size_t)n * 3);
+  float* dd = dist ? S.out(dist, (size_t)n) : nullptr;
+  float* dg = S.out(grad, (size_t)n * 3);
+  if (S.rc) return S.rc;
+  KNF_TRY(ensure_requests(F, (size_t)n));
+  RouteBuffers R = route_buffers(F, 2, -1);
+  route_emit_points_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(R, F.geom, dp, (int)n, nullptr);
+  KNF_TRY(launch_scan_scatter(F, R, (size_t)n, st));
+  static bool configured = false;
+  if (!configured) {
+    KNF_CUDA(cudaFuncSetAttribute(sdf_gradient_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(GradSmem)));
+    configured = true;
+  }
+  GradParams G{};
+  G.P.blobs = F.sdf_blobs;
+  G.P.perm = R.perm;
+  G.P.tiles = R.tiles;
+  G.P.ctr = R.ctr;
+  G.P.req_pt = R.req_pt;
+  G.dist = dd;
+  G.grad = dg;
+  const size_t tiles_upper = (size_t)n / kSmallTile + std::min<size_t>((size_t)n, (size_t)F.geom.n_cells) + 1;
+  sdf_gradient_kernel<<<(int)std::min<size_t>(tiles_upper, 148 * 5), 32, sizeof(GradSmem), st>>>(G);
+  F.stats.kernel_launches += 4;
+  KNF_CUDA(cudaGetLastError());
   return S.finish();
 }
 

@@ -487,6 +487,19 @@ def grad_fd(field, x):
     return out[0] if single else out
 
 
+def grad_analytic(field, x, return_distance: bool = False):
+    """Analytic gradient of the owning cell's SDF network at each point (fp32, forward-mode differentiation on the
+    device; include/knf_b200.h knf_sdf_gradient).  Not a reference function: the reference's normals are the global
+    finite differences of ``grad_fd`` / ``normal_batch``, which also see the jumps between neighbouring cells."""
+    dev = device_field(field)
+    a = _Args(dev, x)
+    p = a.inp(x, np.float32, 3)
+    grad = a.out((p.shape[0], 3), np.float32)
+    dist = a.out((p.shape[0],), np.float32)
+    N.check(N.load().knf_sdf_gradient(dev.handle, N.ptr(p), p.shape[0], N.ptr(dist), N.ptr(grad), a.mem, a.stream))
+    return (grad, dist) if return_distance else grad
+
+
 def normal_batch(field, x, eps: float = NORMAL_EPS):
     dev = device_field(field)
     a = _Args(dev, x)

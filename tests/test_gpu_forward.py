@@ -240,3 +240,59 @@ def test_tensor_precision_modes(G, mode):
         dev.set_precision("fp32_chain")
     with pytest.raises(ValueError):
         dev.set_precision(7)
+
+
+def _analytic_gradient_f64(ofield, pts):
+    """float64 forward-mode gradient of the owning cell's SDF network (nn.fourier_encode + two softplus layers)."""
+    spec = ofield.spec
+    cells = oracle.cell_ids(spec, pts.astype(np.float32))
+    W = [w.astype(np.float64) for w in ofield.sdf.W]
+    b = [v.astype(np.float64) for v in ofield.sdf.b]
+    L = spec.pos_octaves
+    out_d, out_g = np.empty(len(pts)), np.empty((len(pts), 3))
+    for i, (x, c) in enumerate(zip(pts.astype(np.float64), cells)):
+        feats, J = [x[0], x[1], x[2]], [np.eye(3)[0], np.eye(3)[1], np.eye(3)[2]]
+        for o in range(L):
+            f = (2.0 ** o) * np.pi
+            for a in range(3):
+                feats.append(np.sin(f * x[a])); J.append(f * np.cos(f * x[a]) * np.eye(3)[a])
+            for a in range(3):
+                feats.append(np.cos(f * x[a])); J.append(-f * np.sin(f * x[a]) * np.eye(3)[a])
+        h, dh = np.array(feats), np.array(J)  # (39,), (39,3)
+        for k in range(2):
+            z = W[k][c] @ h + b[k][c]
+            dz = W[k][c] @ dh
+            sg = 1.0 / (1.0 + np.exp(-z))
+            h, dh = np.log1p(np.exp(-np.abs(z))) + np.maximum(z, 0), sg[:, None] * dz
+        out_d[i] = W[2][c][0] @ h + b[2][c][0]
+        out_g[i] = W[2][c][0] @ dh
+    return out_d, out_g
+
+
+def test_analytic_gradient(G, distilled_field, distilled_oracle):
+    """knf_sdf_gradient (north_star: the fused MLP also emits the SDF gradient): forward-mode analytic gradient of the
+    owning cell's network against a float64 evaluation of the same derivative; its deviation from the reference's
+    global finite-difference normals is REPORTED (the reference renders with FD, and so does the parity path)."""
+    rng = np.random.default_rng(9)
+    for name, field, ofield in (("distilled 4^3", distilled_field, distilled_oracle),
+                                ("random-init 16^3", G.field_init(G.GridConfig(resolution=16), seed=0), None)):
+        if ofield is None:
+            ofield = oracle_from_product(field)
+        pts = rng.uniform(-0.98, 0.98, size=(1500, 3)).astype(np.float32)
+        grad, dist = G.grad_analytic(field, pts, return_distance=True)
+        d64, g64 = _analytic_gradient_f64(ofield, pts)
+        scale = np.abs(g64).max()
+        print(f"{name}: analytic gradient vs float64: max |err| {np.abs(grad - g64).max():.2e} (|grad| up to {scale:.1f}), distance max |err| {np.abs(dist - d64).max():.2e}")
+        assert np.abs(grad - g64).max() <= 2e-5 * max(scale, 1.0)
+        assert np.abs(dist - d64).max() <= 5e-6
+        assert np.allclose(dist, G.sdf_values(field, pts), atol=3e-6)
+        # deviation from the reference's FD normals (grid.normal_batch): reported, and loosely bounded on the smooth field
+        na = grad / np.maximum(np.linalg.norm(grad, axis=1, keepdims=True), 1e-30)
+        nf, ok = G.normal_batch(field, pts.astype(np.float64))
+        dev = np.abs(na - nf)[ok].max(axis=1)
+        print(f"{name}: analytic vs FD normals: median {np.median(dev):.2e}, p99 {np.quantile(dev, 0.99):.2e}, max {dev.max():.2e}")
+        if name.startswith("distilled"):
+            assert np.median(dev) <= 5e-3
+    # ragged / empty
+    assert G.grad_analytic(distilled_field, np.zeros((0, 3), np.float32)).shape == (0, 3)
+    assert G.grad_analytic(distilled_field, pts[:1]).shape == (1, 3)
