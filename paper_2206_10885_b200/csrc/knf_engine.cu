@@ -50,7 +50,7 @@ void DevBuf::release() {
 }
 
 void Workspace::release_all() {
-  DevBuf* all[] = {&req_pt2, &req_cell2, &req_rank2, &req_pt3, &req_cell3, &req_rank3, &cell_count_f, &live2, &live3, &tile_base, &req_pt1, &req_cell1, &req_rank1, &req_pt, &req_cell, &req_rank, &perm, &tiles, &cell_count, &cell_offset, &counters, &t, &t_prev,
+  DevBuf* all[] = {&req_pt2, &req_cell2, &req_rank2, &req_pt3, &req_cell3, &req_rank3, &cell_count_f, &sorted, &live2, &live3, &tile_base, &req_pt1, &req_cell1, &req_rank1, &req_pt, &req_cell, &req_rank, &perm, &tiles, &cell_count, &cell_offset, &counters, &t, &t_prev,
                    &d_prev, &t_conv, &d_conv, &t_hit, &steps, &phase, &hit, &live0, &live1, &hit_list,
                    &hit_count, &sdf_out, &col_v, &col_n, &col_z, &rgb, &origins, &dirs, &t_near, &t_far, &normals64,
                    &colors64, &frame_color, &frame_depth, &frame_normal, &frame_hit};
@@ -119,6 +119,7 @@ int ensure_rays(Field& F, size_t n) {
   KNF_TRY(W.req_pt3.ensure(n * sizeof(float4)));
   KNF_TRY(W.req_cell3.ensure(n * sizeof(int)));
   KNF_TRY(W.req_rank3.ensure(n * sizeof(int)));
+  KNF_TRY(W.sorted.ensure(n * sizeof(float4)));
   KNF_TRY(W.live2.ensure(n * 4));
   KNF_TRY(W.live3.ensure(n * 4));
   {
@@ -155,6 +156,8 @@ RouteBuffers route_buffers(Field& F, int slot, int next_slot, int list) {
   R.next_ctr = next_slot >= 0 ? counters(F, next_slot) : nullptr;
   R.eval_counter = nullptr;
   R.small_tiles = 0;
+  R.sorted = nullptr;
+  R.live = nullptr;
   return R;
 }
 
@@ -404,6 +407,8 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     if (filter_pass) {
       // filter queue of this wavefront: tensor-core predicate; undecided samples join the exact queue below
       RouteBuffers Rf = route_buffers(F, 4 + cur, 4 + nxt, 2 + cur);
+      Rf.sorted = W.sorted.as<float4>();
+      Rf.live = M.live[2 + cur];
       KNF_TRY(launch_scan_scatter(F, Rf, (size_t)n, st));
       MarchTileArgs Af = A;
       Af.P.blobs = reinterpret_cast<const float*>(F.sdf_mmah_blobs);
@@ -411,6 +416,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
       Af.P.tiles = Rf.tiles;
       Af.P.ctr = Rf.ctr;
       Af.P.req_pt = Rf.req_pt;
+      Af.P.sorted = Rf.sorted;
       Af.live_in = M.live[2 + cur];
       Af.max_inner = F.filter_max_inner;
       Af.defer = route_buffers(F, cur, -1, cur);
@@ -423,6 +429,8 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     }
     RouteBuffers R = route_buffers(F, cur, nxt, cur);
     R.eval_counter = stat_counter(F, 3);  // requests that went through global routing
+    R.sorted = W.sorted.as<float4>();
+    R.live = M.live[cur];
     const bool small_only = exact_mode && exact_sparse && F.sparse_small_kernel;
     R.small_tiles = small_only ? 2 : 0;  // dense wavefronts: 64-request tiles for march_warp_kernel; sparse: <= 16 for march_small_kernel
     KNF_TRY(launch_scan_scatter(F, R, (size_t)n, st));
@@ -431,6 +439,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     A.P.tiles = R.tiles;
     A.P.ctr = R.ctr;
     A.P.req_pt = R.req_pt;
+    A.P.sorted = R.sorted;
     A.live_in = M.live[cur];
     {
       ProfScope prof(F, st, SPAN_SDF_MLP);

@@ -40,6 +40,7 @@ struct Workspace {
   DevBuf req_pt, req_cell, req_rank, perm, tiles;
   DevBuf req_pt1, req_cell1, req_rank1;  // second request list: the fused march kernel reads one list while filling the other
   DevBuf req_pt2, req_cell2, req_rank2, req_pt3, req_cell3, req_rank3;  // the decision filter's two request lists
+  DevBuf sorted;                         // march queues: (point, ray) per sorted position
   DevBuf cell_count_f;                   // per-cell request counts of the filter queue
   DevBuf live2, live3;
   DevBuf cell_count, cell_offset, tile_base;

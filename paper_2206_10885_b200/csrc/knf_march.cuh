@@ -72,9 +72,8 @@ __device__ __forceinline__ void march_exact_tile(const MarchTileArgs& A, SmemT& 
     ray[q] = 0;
     px[q] = py[q] = pz[q] = 0.f;
     if (active[q]) {
-      int slot = P.perm[tile.start + col[q]];
-      ray[q] = A.live_in[slot];
-      float4 pt = P.req_pt[slot];
+      const float4 pt = P.sorted[tile.start + col[q]];  // (point, ray id): written by the routing scatter
+      ray[q] = __float_as_int(pt.w);
       px[q] = pt.x; py[q] = pt.y; pz[q] = pt.z;
       ray_load(rr[q], A.M, ray[q]);  // in flight during the first MLP pass
     }
@@ -282,9 +281,8 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
       active[q] = pidx[q] < tile.count;
       px[q] = py[q] = pz[q] = 0.f;
       if (active[q]) {
-        int slot = P.perm[tile.start + pidx[q]];
-        ray[q] = A.live_in[slot];
-        float4 pt = P.req_pt[slot];
+        const float4 pt = P.sorted[tile.start + pidx[q]];  // (point, ray id): written by the routing scatter
+        ray[q] = __float_as_int(pt.w);
         px[q] = pt.x; py[q] = pt.y; pz[q] = pt.z;
         ray_load_scalars(rr[q], A.M, ray[q]);  // in flight during the first pass
 #pragma unroll

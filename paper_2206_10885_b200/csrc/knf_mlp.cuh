@@ -44,6 +44,7 @@ struct MlpParams {
   RouteCounters* ctr;          // n_tiles, tile_cursor
   // SDF inputs
   const float4* req_pt;        // request slot -> fp32 point
+  const float4* sorted;        // march kernels: sorted position -> (point, ray id bits in .w)
   // colour inputs (request slot -> row)
   const float* col_v;          // (n,3) fp32 view dirs
   const float* col_n;          // (n,3) fp32 normals

@@ -31,6 +31,8 @@ struct RouteBuffers {
   RouteCounters* ctr; // this pass
   RouteCounters* next_ctr;  // zeroed by scan (may equal nullptr)
   unsigned long long* eval_counter;  // += n_requests per pass (nullable); statistics only
+  float4* sorted;     // march queues: sorted position -> (point, ray id in .w): one coalesced load per tile point (nullable)
+  const int* live;    // march queues: request slot -> ray id (read by scatter when `sorted` is set)
   int small_tiles;    // 1: cut the last < 49 requests of a cell into tiles of <= 16 (kernels with a small-tile path); 2: every tile <= 16
 };
 
@@ -199,7 +201,16 @@ static __global__ void route_scatter_kernel(RouteBuffers R, int n_cells) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   for (int s = gid; s < n; s += stride) {
     const int c = R.req_cell[s];  // -1: a slot its producer left empty (knf_volume.cu)
-    if (c >= 0) R.perm[R.cell_offset[c] + R.req_rank[s]] = s;
+    if (c >= 0) {
+      const int pos = R.cell_offset[c] + R.req_rank[s];
+      if (R.sorted) {  // march queues: the tile kernels read (point, ray) straight from the sorted position
+        float4 v = R.req_pt[s];
+        v.w = __int_as_float(R.live[s]);
+        R.sorted[pos] = v;
+      } else {
+        R.perm[pos] = s;
+      }
+    }
   }
   for (int c = gid; c < n_cells; c += stride) {
     const int start = R.cell_offset[c], k = R.cell_offset[c + 1] - start;
