@@ -262,7 +262,7 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
   const int n_tiles = P.ctr->n_tiles;
   const uint32_t* blobs = reinterpret_cast<const uint32_t*>(P.blobs);
   uint32_t parity = 0;
-  unsigned long long evals = 0, slots = 0, deferred = 0, skipped = 0;
+  unsigned evals = 0, slots = 0, deferred = 0, skipped = 0;  // per warp and launch: far below 2^32
 
   for (;;) {
     const int tix = next_tile(P.ctr, lane);
@@ -307,6 +307,7 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
     int n_active = tile.count;
     const float* W3d = reinterpret_cast<const float*>(S.w + Blob::w3d);  // output-layer column 0
     double safe_below = 0.0;
+    float safe_below_f = 0.f;  // safe_below rounded down
     float lip[3] = {0.f, 0.f, 0.f};
 
     for (int inner = 0;; inner++) {
@@ -324,6 +325,7 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
         parity ^= 1;
         if (FILTER) {
           safe_below = -(A.M.eps + (double)reinterpret_cast<const float*>(S.w + Blob::b3)[kFilterDeltaSlot]);
+          safe_below_f = __double2float_rd(safe_below);
 #pragma unroll
           for (int a = 0; a < 3; a++) lip[a] = reinterpret_cast<const float*>(S.w + Blob::b3)[kFilterLipSlot + a];
         }
@@ -339,7 +341,7 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
         if (m == t) dist = d;
         slots += 16;
       }
-      evals += (lane == 0) ? (unsigned long long)n_active : 0ull;
+      evals += (lane == 0) ? (unsigned)n_active : 0u;
       if (inner == 0) cp_async_wait_all();  // the lane's own origin / direction slots
 
       int code[2], cell[2];
@@ -359,7 +361,8 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
             // |d(p) - d(p0)| <= sum_a L_a |p_a - p0_a| inside the cell (L_a: proven per-axis Lipschitz bounds of the cell's
             // network), so every sample whose bound stays below `room` still has an exact distance below -eps: the
             // reference's evaluation there can only say "keep crawling", and its step is taken without evaluating.
-            const double room = (FILTER && A.max_skip > 0) ? safe_below - (double)(q ? dist.y : dist.x) : 0.0;
+            // (fp32, rounded towards less room: the fp64 pipe is the scarce one in this kernel)
+            const float room = (FILTER && A.max_skip > 0) ? __fmul_rd(__fsub_rd(safe_below_f, q ? dist.y : dist.x), 0.99999f) : 0.0f;
             for (;;) {
               px[q] = __double2float_rn(S.od[0][32 * q + lane] + t_next * S.od[3][32 * q + lane]);
               py[q] = __double2float_rn(S.od[1][32 * q + lane] + t_next * S.od[4][32 * q + lane]);
@@ -368,9 +371,9 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
                                        pz[q] > in_lo[2] && pz[q] < in_hi[2];
               cell[q] = well_inside ? tile.cell : cell_of_slow(px[q], py[q], pz[q], A.G.lo[0], A.G.lo[1], A.G.lo[2], A.G.hi[0], A.G.hi[1], A.G.hi[2], A.G.resolution);
               if (!FILTER || !well_inside) break;
-              // (+ 1e-6 per axis: the fp32 roundings of the two points; * 1.00001: the fp32 arithmetic of this line)
+              // (+ 1e-6 per axis: the fp32 roundings of the two points; the 0.99999 on `room` covers the fp32 arithmetic here)
               const float rise = lip[0] * (fabsf(px[q] - x0) + 1e-6f) + lip[1] * (fabsf(py[q] - y0) + 1e-6f) + lip[2] * (fabsf(pz[q] - z0) + 1e-6f);
-              if (!((double)rise * 1.00001 < room)) break;
+              if (!(rise < room)) break;
               // the reference's march step at t_next (surface.py:217-223) with max(d, eps/2) = eps/2
               rr[q].steps += 1;
               rr[q].t_prev = rr[q].t;
@@ -398,7 +401,7 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
         if (FILTER) {
           march_emit(A.next_filter, A.live_filter, code[q] == STEP_FILTER && leaves, ray[q], rr[q], A.M, px[q], py[q], pz[q], cell[q]);
           march_emit(A.defer, A.live_defer, code[q] == STEP_EXACT, ray[q], rr[q], A.M, px[q], py[q], pz[q], cell[q]);
-          deferred += (code[q] == STEP_EXACT) ? 1ull : 0ull;
+          deferred += (code[q] == STEP_EXACT) ? 1u : 0u;
         } else {
           march_emit(A.next, A.live_out, code[q] == STEP_EXACT && leaves, ray[q], rr[q], A.M, px[q], py[q], pz[q], cell[q]);
           march_emit(A.next_filter, A.live_filter, code[q] == STEP_FILTER, ray[q], rr[q], A.M, px[q], py[q], pz[q], cell[q]);
@@ -421,13 +424,13 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
       }
     }
     if (lane == 0 && evals) {
-      atomicAdd(A.eval_counter + (FILTER ? 4 : 0), evals);
+      atomicAdd(A.eval_counter + (FILTER ? 4 : 0), (unsigned long long)evals);
       if (FILTER) {
-        atomicAdd(A.eval_counter + 5, deferred);
-        atomicAdd(A.eval_counter + 6, skipped);
-        atomicAdd(A.eval_counter + 7, slots);
+        atomicAdd(A.eval_counter + 5, (unsigned long long)deferred);
+        atomicAdd(A.eval_counter + 6, (unsigned long long)skipped);
+        atomicAdd(A.eval_counter + 7, (unsigned long long)slots);
       }
-      else atomicAdd(A.eval_counter + 2, slots);
+      else atomicAdd(A.eval_counter + 2, (unsigned long long)slots);
     }
   }
 }
