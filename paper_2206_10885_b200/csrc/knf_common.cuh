@@ -112,6 +112,34 @@ __device__ __forceinline__ void np_sincosf(float x, float& s_out, float& c_out) 
   c_out = (ic & 2) ? -cv : cv;
 }
 
+// Two np_sincosf evaluations in one packed (f32x2) instruction stream: identical operations per component, so identical
+// bits; used by the tensor tile kernels, where a lane encodes one axis of two rows.
+__device__ __forceinline__ void np_sincosf2(float2 x, float2& s_out, float2& c_out) {
+#define KNF_P2(v) make_float2(v, v)
+  const float2 magic = KNF_P2(0x1.8p+23f);
+  float2 q = __fadd2_rn(__ffma2_rn(x, KNF_P2(0x1.45f306p-1f), magic), KNF_P2(-0x1.8p+23f));
+  float2 r = __ffma2_rn(q, KNF_P2(-0x1.921fb0p+00f), x);
+  r = __ffma2_rn(q, KNF_P2(-0x1.5110b4p-22f), r);
+  r = __ffma2_rn(q, KNF_P2(-0x1.846988p-48f), r);
+  const float2 r2 = __fmul2_rn(r, r);
+  float2 pc = __ffma2_rn(KNF_P2(0x1.98e616p-16f), r2, KNF_P2(-0x1.6c06dcp-10f));
+  pc = __ffma2_rn(pc, r2, KNF_P2(0x1.55553cp-05f));
+  pc = __ffma2_rn(pc, r2, KNF_P2(-0x1.000000p-01f));
+  pc = __ffma2_rn(pc, r2, KNF_P2(0x1.000000p+00f));
+  float2 ps = __ffma2_rn(KNF_P2(0x1.7d3bbcp-19f), r2, KNF_P2(-0x1.a06bbap-13f));
+  ps = __ffma2_rn(ps, r2, KNF_P2(0x1.11119ap-07f));
+  ps = __ffma2_rn(ps, r2, KNF_P2(-0x1.555556p-03f));
+  ps = __fmul2_rn(ps, r2);
+  ps = __ffma2_rn(ps, r, r);
+#undef KNF_P2
+  const int iq0 = (int)q.x, iq1 = (int)q.y;
+  const float sv0 = (iq0 & 1) ? pc.x : ps.x, sv1 = (iq1 & 1) ? pc.y : ps.y;
+  s_out = make_float2((iq0 & 2) ? -sv0 : sv0, (iq1 & 2) ? -sv1 : sv1);
+  const int ic0 = iq0 + 1, ic1 = iq1 + 1;
+  const float cv0 = (ic0 & 1) ? pc.x : ps.x, cv1 = (ic1 & 1) ? pc.y : ps.y;
+  c_out = make_float2((ic0 & 2) ? -cv0 : cv0, (ic1 & 2) ? -cv1 : cv1);
+}
+
 // np.exp on float32 (loops_exponent_log): Cody-Waite by ln2, rational P5/Q2, scalef.
 __device__ __forceinline__ float np_expf(float x) {
   const float magic = 0x1.8p+23f;

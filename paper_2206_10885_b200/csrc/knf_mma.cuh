@@ -152,7 +152,7 @@ __device__ __forceinline__ void mma_layer(const APieces<P> (&A)[KT], const uint2
 #pragma unroll
   for (int nt = 0; nt < 4; nt++)
 #pragma unroll
-    for (int i = 0; i < 4; i++) small[nt][i] = big[nt][i] = 0.0f;
+    for (int i = 0; i < 4; i++) small[nt][i] = 0.0f;  // `big` arrives holding its initial value (zero, or the bias)
 #pragma unroll
   for (int kt = 0; kt < KT; kt++) {
     uint2 w[4][P];
@@ -186,21 +186,36 @@ __device__ __forceinline__ void mma_layer(const APieces<P> (&A)[KT], const uint2
 }
 
 // h = softplus(big + small [/ 2^11] + bias) on the accumulator fragments: eight independent packed evaluations in flight.
+// The filter (FAST) starts the big accumulator at the bias instead of adding it afterwards (one packed add less per
+// pair; the sum order differs from the other modes by design -- only the proven bound matters there).
+template <bool FAST>
+__device__ __forceinline__ void init_big(float (&big)[4][4], const float* __restrict__ bias, int t) {
+#pragma unroll
+  for (int nt = 0; nt < 4; nt++) {
+    const float2 b = FAST ? *reinterpret_cast<const float2*>(bias + 8 * nt + 2 * t) : make_float2(0.0f, 0.0f);
+    big[nt][0] = b.x; big[nt][1] = b.y; big[nt][2] = b.x; big[nt][3] = b.y;
+  }
+}
+
 template <int P, bool FAST>
 __device__ __forceinline__ void finish_hidden(const float (&small)[4][4], const float (&big)[4][4], const float* __restrict__ bias,
                                               int t, float (&h)[4][4]) {
   float2 r[8];
 #pragma unroll
   for (int nt = 0; nt < 4; nt++) {
-    const float2 b = *reinterpret_cast<const float2*>(bias + 8 * nt + 2 * t);
+    const float2 b = FAST ? make_float2(0.0f, 0.0f) : *reinterpret_cast<const float2*>(bias + 8 * nt + 2 * t);
 #pragma unroll
     for (int hh = 0; hh < 2; hh++) {
       const float2 bg = make_float2(big[nt][2 * hh], big[nt][2 * hh + 1]), sm = make_float2(small[nt][2 * hh], small[nt][2 * hh + 1]);
       const float2 z = (P == 3) ? __fadd2_rn(bg, sm) : __ffma2_rn(sm, make_float2(1.0f / kHalfPieceScale, 1.0f / kHalfPieceScale), bg);
-      r[2 * nt + hh] = __fadd2_rn(z, b);
+      r[2 * nt + hh] = FAST ? z : __fadd2_rn(z, b);
     }
   }
-  if (FAST) softplus_fast_f2xN<8>(r);
+#ifndef KNF_FILTER_SOFTPLUS
+#define KNF_FILTER_SOFTPLUS 0  // 0: MUFU ex2 + lg2 (XU pipe), 1: the packed polynomial softplus_f2xN (FMA pipe; |err| 5e-7)
+#endif
+  if (FAST && KNF_FILTER_SOFTPLUS == 0) softplus_fast_f2xN<8>(r);
+  else if (FAST) softplus_f2xN<8>(r);
   else softplus_tile<8>(r);
 #pragma unroll
   for (int nt = 0; nt < 4; nt++) {
@@ -220,8 +235,7 @@ __device__ __forceinline__ void mma_encode(const SmemT& S, int m, int lane, floa
     const float2 c = make_float2(S.pts[t][p0], S.pts[t][p0 + 8]);
     const float2 a = __fmul2_rn(make_float2(pi_f, pi_f), c);
     float2 s, co;
-    np_sincosf(a.x, s.x, co.x);
-    np_sincosf(a.y, s.y, co.y);
+    np_sincosf2(a, s, co);
 #pragma unroll
     for (int o = 0; o < kSdfFreqs; o++) {
       v[2 * o] = s;
@@ -256,6 +270,7 @@ __device__ __forceinline__ void mma_hidden_from(const SmemT& S, const float2 (&v
     for (int kt = 0; kt < Blob::kt1; kt++)
       make_a<P>(A[kt], make_float2(v[4 * kt].x, v[4 * kt + 1].x), make_float2(v[4 * kt].y, v[4 * kt + 1].y),
                 make_float2(v[4 * kt + 2].x, v[4 * kt + 3].x), make_float2(v[4 * kt + 2].y, v[4 * kt + 3].y));
+    init_big<FAST>(big, reinterpret_cast<const float*>(S.w + Blob::b1), t);
     mma_layer<P, Blob::kt1>(A, reinterpret_cast<const uint2*>(S.w + Blob::frag1), lane, small, big);
   }
   finish_hidden<P, FAST>(small, big, reinterpret_cast<const float*>(S.w + Blob::b1), t, h1);
@@ -266,6 +281,7 @@ __device__ __forceinline__ void mma_hidden_from(const SmemT& S, const float2 (&v
     for (int kt = 0; kt < Blob::kt2; kt++)
       make_a<P>(A[kt], make_float2(h1[2 * kt][0], h1[2 * kt][1]), make_float2(h1[2 * kt][2], h1[2 * kt][3]),
                 make_float2(h1[2 * kt + 1][0], h1[2 * kt + 1][1]), make_float2(h1[2 * kt + 1][2], h1[2 * kt + 1][3]));
+    init_big<FAST>(big, reinterpret_cast<const float*>(S.w + Blob::b2), t);
     mma_layer<P, Blob::kt2>(A, reinterpret_cast<const uint2*>(S.w + Blob::frag2), lane, small, big);
   }
   finish_hidden<P, FAST>(small, big, reinterpret_cast<const float*>(S.w + Blob::b2), t, h2);
