@@ -337,8 +337,8 @@ def main():
             "kernel": "march_mma_kernel<2, filter> (decision filter: Fourier recurrence + fp16x2 split mma.sync.m16n8k16 layers chained in registers + MUFU softplus "
                       "+ sphere-trace crawl step + certified skipping)",
             "bound": "tensor", "achieved": filter_tflops, "peak": tensor_peak, "unit": "TFLOP/s", "frac": (filter_tflops / tensor_peak) if filter_tflops else None,
-            "traffic": 206.1e6,
-            "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of ONE dense filter launch (1.06 ms under ncu, ~12 M evaluations) from "
+            "traffic": 195.3e6,
+            "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of ONE dense filter launch (1.00 ms under ncu, ~12 M evaluations) from "
                             "profiles/ncu_r1_filter_v3.summary.txt (ncu --set full); weights (50 MB of fp16 fragments) and ray state are L2-resident, DRAM is 2 % busy",
             "peak_source": f"{peak_src} MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS, tcgen05 path); mma.sync (HMMA.16816) issue peak measured on this pool: "
                            "553 TFLOP/s (profiles/hmma_split_r1.txt)",
