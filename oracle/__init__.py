@@ -19,6 +19,12 @@ holds no stored golden vectors of its own; its known-answer tests for the path
 (cell corners, ray/AABB cases, furnace exactness -- SURVEY.md section 8c) are
 re-run against this oracle in ``tests/test_oracle_known_answers.py``.
 
+One piece is C: ``oracle/np_softplus.c`` restates, operation for operation, how NumPy 2.3 evaluates the float32
+softplus of nn.py:26-33 on an AVX-512 host (np.exp's source loop + Intel SVML's log1p, a third-party routine pinned to
+the installed numpy binary); ``tests/test_oracle_golden.py::test_softplus_restatement_bit_exact`` checks it against
+NumPy itself and against the reference-generated golden vector.  It documents the arithmetic the device softplus
+reproduces; like everything here it is only ever run by the tests.
+
 Arithmetic note: like the reference, the oracle's matrix products go through
 NumPy -> OpenBLAS ``sgemm`` and its transcendentals through NumPy's SIMD loops,
 so last-ulp results depend on the host CPU and on how many points share a cell

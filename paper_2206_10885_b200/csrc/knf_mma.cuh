@@ -24,8 +24,12 @@
 // lane runs nn.fourier_encode's recurrence for one axis of its eight rows.  Shared memory holds only
 // the cell's weight fragments (one TMA bulk copy) and a 64 x 3 coordinate exchange.
 //
-// Work per 64-point pass and warp: 480 HMMA (tensor pipe) + ~64 packed softplus + ~80 splits (FMA /
-// ALU pipes) instead of 2336 FFMA2 + 64 packed softplus.
+// Work per 64-point pass and warp: 480 HMMA (bf16 x 3) or 240 (fp16 x 2) on the tensor pipe + 64 packed softplus +
+// ~80 operand splits (FMA / ALU pipes) instead of 2336 FFMA2 + 64 packed softplus.
+//
+// Three users: sdf_mma_kernel (batched forward in the KNF_PRECISION_TENSOR_* modes), march_mma_kernel<P, false>
+// (the march in those modes) and march_mma_kernel<2, true> -- the DECISION FILTER of the exact mode (knf_march.cuh),
+// which is where the default configuration spends most of its time.
 #pragma once
 
 #include "knf_common.cuh"
@@ -51,9 +55,9 @@ struct MmaBlobT {
   static constexpr int b2 = b1 + kHidden;
   static constexpr int w3d = b2 + kHidden;
   static constexpr int b3 = w3d + kHidden;
-  static constexpr int march_words = b3 + kSdfOutPad + 4;  // + 4 words of filter constants  // what a march kernel needs: P = 3: 2956 (11824 B... see bytes), P = 2: 2668 (10672 B)
+  static constexpr int march_words = b3 + kSdfOutPad + 4;  // + 4 words of filter constants; P = 3: 3952 (15808 B), P = 2: 2672 (10688 B)
   static constexpr int w3 = march_words;
-  static constexpr int words = w3 + kHidden * kSdfOutPad;  // P = 3: 4332 (17328 B); P = 2: 3052 (12208 B)
+  static constexpr int words = w3 + kHidden * kSdfOutPad;  // P = 3: 4336 (17344 B); P = 2: 3056 (12224 B)
   static constexpr int bytes = words * 4;
   static constexpr int march_bytes = march_words * 4;
   static_assert(bytes % 16 == 0 && march_bytes % 16 == 0, "blob (parts) must be multiples of 16 B for cp.async.bulk");
