@@ -359,6 +359,7 @@ def main():
             "mrays_per_s": fps * W * H / 1e6,
             "sdf_evals_per_s": ref_evals * world / (ms / 1e3),
             "sdf_evals_per_ray": ref_evals / max(stats["rays"], 1),
+            "sdf_evals_executed_per_s": (stats["sdf_evals"] + stats["filter_evals"]) * world / (ms / 1e3),  # network evaluations actually run (exact + filter)
             "sdf_evals_breakdown": {"exact_fp32_chain": int(stats["sdf_evals"]), "filter_tensor": int(stats["filter_evals"]),
                                     "filter_undecided_re_evaluated": int(stats["filter_deferred"]), "certified_without_evaluation": int(stats["filter_skipped"]),
                                     "note": "sdf_evals_per_s / per_ray count what the reference evaluates for these frames (exact + filter - undecided + certified)"},
