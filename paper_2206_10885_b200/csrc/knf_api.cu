@@ -420,6 +420,8 @@ int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
   if (const char* env = std::getenv("KNF_FILTER_SKIP")) F.filter_skip = std::atoi(env) != 0;
   if (const char* env = std::getenv("KNF_SPARSE_SMALL")) F.sparse_small_kernel = std::atoi(env) != 0;
   if (const char* env = std::getenv("KNF_SPARSE_DIV")) F.sparse_div = std::max(1, std::atoi(env));
+  if (const char* env = std::getenv("KNF_SPARSE_INNER")) F.sparse_max_inner = std::max(1, std::atoi(env));
+  if (const char* env = std::getenv("KNF_SPARSE_KEEP")) F.sparse_keep_div = std::max(1, std::atoi(env));
   if (const char* env = std::getenv("KNF_FILTER")) {
     const std::string v(env);
     if (v == "off" || v == "0") F.filter_mode = KNF_FILTER_OFF;

@@ -450,6 +450,10 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
         A.P.blobs = reinterpret_cast<const float*>(F.sdf_mmah_blobs);
         march_mma_kernel<2, false><<<mlp_grid(F, (size_t)n, march_ctas_per_sm<2>()), 32, sizeof(MmaMarchSmemT<2>), st>>>(A);
       } else if (small_only) {
+        // sparse wavefront: few tiles, the GPU is far from full -- a ray that stays in its cell keeps stepping there
+        // rather than paying another routing round trip (the long tail of a frame is a chain of such round trips)
+        A.max_inner = F.sparse_max_inner;
+        A.keep_div = F.sparse_keep_div;
         march_small_kernel<<<mlp_grid(F, (size_t)n, kSmallCtasPerSm), 32, sizeof(SdfSmallSmem), st>>>(A);
       } else {
         march_warp_kernel<<<mlp_grid(F, (size_t)n), 32, sizeof(SdfKernelSmem), st>>>(A);

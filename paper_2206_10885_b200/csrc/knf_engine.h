@@ -69,6 +69,8 @@ struct Field {
   uint32_t* sdf_mmah_blobs = nullptr;  // MmaBlobT<2> per cell (fp16 x 2 B fragments); null when a weight exceeds the fp16 range
   bool fp16_ok = false;
   double filter_delta_max = 0.0;       // largest per-cell decision-filter bound (knf_api.cu filter_delta)
+  int sparse_max_inner = 8;            // residency cap and keep rule of sparse exact wavefronts (KNF_SPARSE_INNER / KNF_SPARSE_KEEP)
+  int sparse_keep_div = 2;   // measured: (16, 4) gains 3 % on the distilled frame and loses 1.3 % on the random-init one; (32, 8) and up lose more
   int sparse_div = 8;                  // a wavefront is sparse when its exact queue holds < n / sparse_div rays (KNF_SPARSE_DIV)
   bool sparse_small_kernel = true;     // exact march: sparse wavefronts by march_small_kernel (KNF_SPARSE_SMALL=0 disables)
   bool filter_skip = true;             // certified (Lipschitz) skipping inside the filter; KNF_FILTER_SKIP=0 disables

@@ -33,6 +33,7 @@ struct MarchTileArgs {
   unsigned long long* eval_counter;  // statistics: [0] SDF evaluations, [2] lane slots, [4] filter evaluations, [5] deferred, [6] certified skips, [7] filter lane slots
   int max_inner;            // cap on consecutive in-place steps of one tile
   int max_skip;             // filter kernel: 0 disables certified skipping
+  int keep_div;             // a tile keeps stepping in place while n_stay * keep_div >= its size (2 = half; 0 is read as 2)
   double inv_resolution;    // 1 / grid resolution (host-computed)
   double crawl_below;       // exact kernels: a march step from a distance below this continues in the filter queue (-inf: never)
 };
@@ -151,7 +152,7 @@ __device__ __forceinline__ void march_exact_tile(const MarchTileArgs& A, SmemT& 
       n_stay += __popc(__ballot_sync(0xffffffffu, stay[q]));
     }
     // keep stepping in place while at least half of the tile's rays are still here
-    const bool cont = n_stay > 0 && 2 * n_stay >= tile.count && inner + 1 < A.max_inner;
+    const bool cont = n_stay > 0 && (A.keep_div > 0 ? A.keep_div : 2) * n_stay >= tile.count && inner + 1 < A.max_inner;
 #pragma unroll
     for (int q = 0; q < NQ; q++) {
       march_emit(A.next, A.live_out, code[q] == STEP_EXACT && !(cont && stay[q]), ray[q], rr[q], A.M, px[q], py[q], pz[q], cell[q]);
@@ -394,7 +395,7 @@ static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_
         stay[q] = code[q] == (FILTER ? STEP_FILTER : STEP_EXACT) && cell[q] == tile.cell;
       }
       const int n_stay = __popc(__ballot_sync(0xffffffffu, stay[0])) + __popc(__ballot_sync(0xffffffffu, stay[1]));
-      const bool cont = n_stay > 0 && 2 * n_stay >= tile.count && inner + 1 < A.max_inner;
+      const bool cont = n_stay > 0 && (A.keep_div > 0 ? A.keep_div : 2) * n_stay >= tile.count && inner + 1 < A.max_inner;
 #pragma unroll
       for (int q = 0; q < 2; q++) {
         const bool leaves = !(cont && stay[q]);

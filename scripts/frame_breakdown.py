@@ -6,8 +6,13 @@ import numpy as np, torch
 from paper_2206_10885_b200 import grid, surface
 from bench import orbit_view
 W, H = 1920, 1080
-fs = surface.FieldSurface(grid.field_init(grid.GridConfig(resolution=16), seed=0))
-for a in sys.argv[1:]:
+args = [a for a in sys.argv[1:] if a != "distilled"]
+if "distilled" in sys.argv[1:]:
+    from paper_2206_10885_b200.modelio import load_model
+    fs = surface.FieldSurface(load_model(os.path.join(ROOT, "tests", "golden", "sphere_r4_distilled.knf")))
+else:
+    fs = surface.FieldSurface(grid.field_init(grid.GridConfig(resolution=16), seed=0))
+for a in args:
     k, v = a.split("=")
     getattr(fs.dev, "set_" + k)(v)
 dev = torch.device("cuda", 0)
