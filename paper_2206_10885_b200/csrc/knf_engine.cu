@@ -389,6 +389,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
   // host learns by polling the request counts.
   F.prof_chain = true;  // spans inside the loop are back to back on `st`: one shared event between neighbours
   F.prof_last_end = (size_t)-1;
+  size_t live_upper = (size_t)n;  // upper bound on the size of any queue from here on: sizes the routing and tile grids
   for (int w = 0; w <= s.max_steps + 2; w++) {
     const int cur = w & 1, nxt = cur ^ 1;
     const bool filter_pass = exact_mode && F.fp16_ok && F.filter_mode != 0 && !filter_drained && w > 0;
@@ -409,7 +410,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
       RouteBuffers Rf = route_buffers(F, 4 + cur, 4 + nxt, 2 + cur);
       Rf.sorted = W.sorted.as<float4>();
       Rf.live = M.live[2 + cur];
-      KNF_TRY(launch_scan_scatter(F, Rf, (size_t)n, st));
+      KNF_TRY(launch_scan_scatter(F, Rf, live_upper, st));
       MarchTileArgs Af = A;
       Af.P.blobs = reinterpret_cast<const float*>(F.sdf_mmah_blobs);
       Af.P.perm = Rf.perm;
@@ -423,7 +424,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
       Af.live_defer = M.live[cur];
       {
         ProfScope prof(F, st, SPAN_FILTER);
-        march_mma_kernel<2, true><<<mlp_grid(F, (size_t)n, march_ctas_per_sm<2>()), 32, sizeof(MmaMarchSmemT<2>), st>>>(Af);
+        march_mma_kernel<2, true><<<mlp_grid(F, live_upper, march_ctas_per_sm<2>()), 32, sizeof(MmaMarchSmemT<2>), st>>>(Af);
       }
       F.stats.kernel_launches += 1;
     }
@@ -433,7 +434,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     R.live = M.live[cur];
     const bool small_only = exact_mode && exact_sparse && F.sparse_small_kernel;
     R.small_tiles = small_only ? 2 : 0;  // dense wavefronts: 64-request tiles for march_warp_kernel; sparse: <= 16 for march_small_kernel
-    KNF_TRY(launch_scan_scatter(F, R, (size_t)n, st));
+    KNF_TRY(launch_scan_scatter(F, R, live_upper, st));
     A.P.blobs = F.sdf_blobs;
     A.P.perm = R.perm;
     A.P.tiles = R.tiles;
@@ -445,18 +446,18 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
       ProfScope prof(F, st, SPAN_SDF_MLP);
       if (F.precision == KNF_PRECISION_TENSOR_BF16X3) {
         A.P.blobs = reinterpret_cast<const float*>(F.sdf_mma_blobs);
-        march_mma_kernel<3, false><<<mlp_grid(F, (size_t)n, march_ctas_per_sm<3>()), 32, sizeof(MmaMarchSmemT<3>), st>>>(A);
+        march_mma_kernel<3, false><<<mlp_grid(F, live_upper, march_ctas_per_sm<3>()), 32, sizeof(MmaMarchSmemT<3>), st>>>(A);
       } else if (F.precision == KNF_PRECISION_TENSOR_FP16X2) {
         A.P.blobs = reinterpret_cast<const float*>(F.sdf_mmah_blobs);
-        march_mma_kernel<2, false><<<mlp_grid(F, (size_t)n, march_ctas_per_sm<2>()), 32, sizeof(MmaMarchSmemT<2>), st>>>(A);
+        march_mma_kernel<2, false><<<mlp_grid(F, live_upper, march_ctas_per_sm<2>()), 32, sizeof(MmaMarchSmemT<2>), st>>>(A);
       } else if (small_only) {
         // sparse wavefront: few tiles, the GPU is far from full -- a ray that stays in its cell keeps stepping there
         // rather than paying another routing round trip (the long tail of a frame is a chain of such round trips)
         A.max_inner = F.sparse_max_inner;
         A.keep_div = F.sparse_keep_div;
-        march_small_kernel<<<mlp_grid(F, (size_t)n, kSmallCtasPerSm), 32, sizeof(SdfSmallSmem), st>>>(A);
+        march_small_kernel<<<mlp_grid(F, live_upper, kSmallCtasPerSm), 32, sizeof(SdfSmallSmem), st>>>(A);
       } else {
-        march_warp_kernel<<<mlp_grid(F, (size_t)n), 32, sizeof(SdfKernelSmem), st>>>(A);
+        march_warp_kernel<<<mlp_grid(F, live_upper), 32, sizeof(SdfKernelSmem), st>>>(A);
       }
     }
     F.stats.kernel_launches += 1;
@@ -475,6 +476,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
       }
       if (n_exact == 0 && n_filter == 0) break;
       exact_sparse = (size_t)n_exact * (size_t)F.sparse_div < (size_t)n;
+      live_upper = std::max<size_t>((size_t)n_exact + (size_t)n_filter, 1);  // rays only retire: an upper bound for every later queue
       if (probing && w == 0 && (size_t)n_filter * 8 < (size_t)(n_exact + n_filter)) use_filter = false;  // < 1/8 of the live rays crawl
       if (!use_filter && n_filter == 0) filter_drained = true;
     }
