@@ -212,21 +212,44 @@ static __global__ void route_scatter_kernel(RouteBuffers R, int n_cells) {
       }
     }
   }
-  for (int c = gid; c < n_cells; c += stride) {
-    const int start = R.cell_offset[c], k = R.cell_offset[c + 1] - start;
-    int tb = R.tile_base[c];
-    for (int s = 0; s < k;) {
-      const int left = k - s;
-      const int take = R.small_tiles == 2 ? min(kSmallTile, left)
-                                          : (left >= kTilePts ? kTilePts : ((R.small_tiles && left <= kSmallTileMaxRemainder) ? min(kSmallTile, left) : left));
-      Tile t;
-      t.cell = c;
-      t.start = start + s;
-      t.count = take;
-      t.pad = 0;
-      R.tiles[tb++] = t;
-      s += take;
+  // tile descriptors, one thread per TILE (a cell of a coarse grid can own thousands): the tile's cell is found by
+  // bisection over the per-cell tile bases the scan wrote
+  const int n_tiles = R.ctr->n_tiles;
+  for (int ti = gid; ti < n_tiles; ti += stride) {
+    int lo = 0, hi = n_cells;  // invariant: tile_base[lo] <= ti < tile_base[hi]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (R.tile_base[mid] <= ti) lo = mid;
+      else hi = mid;
     }
+    const int c = lo, j = ti - R.tile_base[c];
+    const int start = R.cell_offset[c], k = R.cell_offset[c + 1] - start;
+    int off, take;
+    if (R.small_tiles == 2) {
+      off = j * kSmallTile;
+      take = min(kSmallTile, k - off);
+    } else {
+      const int full = k / kTilePts;
+      if (j < full) {
+        off = j * kTilePts;
+        take = kTilePts;
+      } else {
+        const int r = k - full * kTilePts, jr = j - full;
+        if (R.small_tiles && r <= kSmallTileMaxRemainder) {
+          off = full * kTilePts + jr * kSmallTile;
+          take = min(kSmallTile, k - off);
+        } else {
+          off = full * kTilePts;
+          take = r;
+        }
+      }
+    }
+    Tile t;
+    t.cell = c;
+    t.start = start + off;
+    t.count = take;
+    t.pad = 0;
+    R.tiles[ti] = t;
   }
 }
 
