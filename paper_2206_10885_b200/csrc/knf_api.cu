@@ -419,6 +419,8 @@ int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
   if (F.precision == KNF_PRECISION_TENSOR_FP16X2 && !F.fp16_ok) F.precision = KNF_PRECISION_TENSOR_BF16X3;
   if (const char* env = std::getenv("KNF_FILTER_SKIP")) F.filter_skip = std::atoi(env) != 0;
   if (const char* env = std::getenv("KNF_SPARSE_SMALL")) F.sparse_small_kernel = std::atoi(env) != 0;
+  if (const char* env = std::getenv("KNF_FILTER_KEEP")) F.filter_keep_div = std::max(1, std::atoi(env));
+  if (const char* env = std::getenv("KNF_FILTER_INNER")) F.filter_max_inner = std::max(1, std::atoi(env));
   if (const char* env = std::getenv("KNF_SPARSE_DIV")) F.sparse_div = std::max(1, std::atoi(env));
   if (const char* env = std::getenv("KNF_SPARSE_INNER")) F.sparse_max_inner = std::max(1, std::atoi(env));
   if (const char* env = std::getenv("KNF_SPARSE_KEEP")) F.sparse_keep_div = std::max(1, std::atoi(env));

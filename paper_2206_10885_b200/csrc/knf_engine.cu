@@ -420,6 +420,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
       Af.P.sorted = Rf.sorted;
       Af.live_in = M.live[2 + cur];
       Af.max_inner = F.filter_max_inner;
+      Af.keep_div = F.filter_keep_div;
       Af.defer = route_buffers(F, cur, -1, cur);
       Af.live_defer = M.live[cur];
       {

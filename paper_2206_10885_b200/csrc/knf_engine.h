@@ -95,6 +95,7 @@ struct Field {
   bool prof_chain = false;            // set by the march loop
   int* host_poll = nullptr;  // pinned; early-out polling of the march loop
   int march_max_inner = 8;    // tile-residency cap (steps in place per tile visit), exact / tensor march kernels
+  int filter_keep_div = 2;    // the filter keeps stepping a tile in place while n_stay * this >= its size (KNF_FILTER_KEEP)
   int filter_max_inner = 12;  // ... of the decision-filter kernel (measured optimum: 8 -> 15.97 ms, 12 -> 15.80, 16 -> 16.06)
 };
 
