@@ -249,7 +249,12 @@ static __global__ void __launch_bounds__(32, kSmallCtasPerSm) march_small_kernel
 //   converges after filtered steps re-evaluates d_prev exactly first (PH_RECHECK).  Results are bit-identical to
 //   running the exact kernel on every sample (tests/test_gpu_march.py::test_decision_filter_is_exact).
 template <int PC, bool FILTER>
-static __global__ void __launch_bounds__(32, march_ctas_per_sm<PC>()) march_mma_kernel(MarchTileArgs A) {
+// A plain register cap instead of __launch_bounds__(32, n): with the latter ptxas squeezed the filter into 128 registers
+// (spills) although 14 one-warp CTAs leave room for 146; measured 8.2 ms vs 8.6-8.9 ms of filter time per frame.
+#ifndef KNF_MARCH_MMA_MAXNREG
+#define KNF_MARCH_MMA_MAXNREG 144
+#endif
+static __global__ void __maxnreg__(KNF_MARCH_MMA_MAXNREG) march_mma_kernel(MarchTileArgs A) {
   using Blob = MmaBlobT<PC>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   MmaMarchSmemT<PC>& S = *reinterpret_cast<MmaMarchSmemT<PC>*>(smem_raw);
