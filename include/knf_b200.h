@@ -150,7 +150,8 @@ int knf_field_get_precision(knf_field_t f);
 /* Decision filter of surface.march_rays in KNF_PRECISION_FP32_CHAIN mode (surface.py:185-223).  A ray inside a
  * negative region advances by the fixed step scale * eps / 2 and the reference consults the distance there only
  * as the predicate d < -eps (plus, once, as d_prev of the secant step).  With the filter on, those predicates are
- * answered by a tensor-core evaluation with a proven per-cell error bound; every sample it cannot decide, and
+ * answered by a tensor-core evaluation with a per-cell error bound (forward error analysis over the cell's
+ * weights with a measured model of the tensor-core accumulation); every sample it cannot decide, and
  * every value the reference uses as a number, is evaluated by the exact fp32 chain kernel.  Results are
  * bit-identical to filter off.  KNF_FILTER_AUTO probes the first wavefront and switches the filter off when fewer
  * than 1/8 of the live rays are in a negative region (always the case on a real surface).  Environment variable
@@ -159,6 +160,9 @@ enum { KNF_FILTER_OFF = 0, KNF_FILTER_ON = 1, KNF_FILTER_AUTO = 2 };
 int knf_field_set_filter(knf_field_t f, int mode);
 /* largest per-cell bound |filter distance - exact distance| the field was packed with (for reports) */
 double knf_field_filter_delta(knf_field_t f);
+/* number of cells the filter is switched off for (bound = +inf): cells whose hidden activations could leave the
+ * fp16 range of the tensor-core operand pieces (very large weights); their samples all go to the exact kernel */
+int knf_field_filter_cells_off(knf_field_t f);
 
 /* ---- routing: grid.py:176-213 ------------------------------------------------------------ */
 /* grid.cell_index_flat (grid.py:182-185) on fp32 points (fp64 arithmetic, bit-exact). */

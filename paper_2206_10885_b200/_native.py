@@ -131,6 +131,7 @@ _SIGNATURES = {
     "knf_field_get_precision": [_P],
     "knf_field_set_filter": [_P, _I32],
     "knf_field_filter_delta": [_P],
+    "knf_field_filter_cells_off": [_P],
     "knf_cell_index": [_P, _P, _I64, _P, _I32, _P],
     "knf_cell_index_f64": [_P, _P, _I64, _P, _I32, _P],
     "knf_route": [_P, _P, _I64, _P, _P, _P, _P, _P, _I32, _P],

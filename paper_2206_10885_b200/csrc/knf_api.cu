@@ -187,6 +187,7 @@ static inline void split_fp16x2(float w, uint16_t p[2]) {
 //   * the exact kernel's own distance to real arithmetic: fp32 FMA chains of <= 48 terms, gamma_48 < 2^-18;
 //   * softplus is 1-Lipschitz; the fast softplus adds kFastSoftplusErr + 2^-22 y, NumPy's adds <= 2^-22 y.
 // Inputs are bounded by 1 (sin / cos) and by the box (raw coordinates).
+constexpr double kFp16Safe = 60000.0;  // below the largest finite fp16 (65504) with room for the rounding of a piece
 static double filter_delta(int pieces, const float* w1, const float* b1, const float* w2, const float* b2, const float* w3,
                            const float* b3, double x_raw) {
   const double e_rep = pieces == 2 ? 3.1 * std::ldexp(1.0, -22) : 0.0;
@@ -216,7 +217,13 @@ static double filter_delta(int pieces, const float* w1, const float* b1, const f
     s += a * H2[k];
     err += a * eh2[k];
   }
-  return 1.05 * (err + std::ldexp(1.0, -17) * s) + 1e-6;
+  // fp16 operand pieces: a hidden activation (bounded by H1 / H2) or a first-layer input beyond the fp16 range turns
+  // into inf inside the tensor-core evaluation and the analysis above says nothing: no bound for this cell.
+  double h_max = x_raw;
+  for (int n = 0; n < kHidden; n++) h_max = std::max(h_max, std::max(H1[n], H2[n]));
+  if (pieces == 2 && !(h_max < kFp16Safe)) return INFINITY;
+  const double delta = 1.05 * (err + std::ldexp(1.0, -17) * s) + 1e-6;
+  return std::isfinite(delta) ? delta : INFINITY;
 }
 
 // Proven Lipschitz bound of one cell's distance network d(x) = w3 . softplus(W2 softplus(W1 enc(x) + b1) + b2) + b3:
@@ -284,7 +291,7 @@ static void lipschitz_bound(const float* w1, const float* w2, const float* w3, d
 
 template <int P>
 void pack_sdf_mma(int n_cells, const float* const w[3], const float* const b[3], double x_raw, std::vector<uint32_t>& out,
-                  double* delta_max) {
+                  double* delta_max, int* cells_off = nullptr) {
   using Blob = MmaBlobT<P>;
   out.assign((size_t)n_cells * Blob::words, 0u);
   for (int c = 0; c < n_cells; c++) {
@@ -331,9 +338,11 @@ void pack_sdf_mma(int n_cells, const float* const w[3], const float* const b[3],
     std::memcpy(blob + Blob::w3d, w3, kHidden * sizeof(float));  // row 0 of (9, 32): the distance output
     std::memcpy(blob + Blob::b3, b[2] + (size_t)c * kSdfOut, kSdfOut * sizeof(float));
     const double delta = filter_delta(P, w1, b[0] + (size_t)c * kHidden, w2, b[1] + (size_t)c * kHidden, w3, b[2] + (size_t)c * kSdfOut, x_raw);
-    const float delta_f = std::nextafter((float)delta, INFINITY);
+    // delta = +inf switches the filter off for this cell: -(eps + inf) = -inf, no distance is ever below it
+    const float delta_f = delta < 1e30 ? std::nextafter((float)delta, INFINITY) : INFINITY;
     std::memcpy(blob + Blob::b3 + kFilterDeltaSlot, &delta_f, sizeof(float));
-    if (delta_max) *delta_max = std::max(*delta_max, (double)delta_f);
+    if (delta_max && std::isfinite(delta_f)) *delta_max = std::max(*delta_max, (double)delta_f);
+    if (cells_off && !std::isfinite(delta_f)) *cells_off += 1;
     double lip[3];
     lipschitz_bound(w1, w2, w3, lip);
     for (int a = 0; a < 3; a++) {
@@ -403,7 +412,12 @@ int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
     for (size_t i = 0; i < n2 && F.fp16_ok; i++) F.fp16_ok = std::fabs(d->sdf_w[1][i]) < 60000.0f;
     if (F.fp16_ok) {
       F.filter_delta_max = 0.0;
-      pack_sdf_mma<2>(F.geom.n_cells, d->sdf_w, d->sdf_b, x_raw, frags, &F.filter_delta_max);
+      F.filter_x_raw = (float)x_raw;
+      F.filter_cells_off = 0;
+      pack_sdf_mma<2>(F.geom.n_cells, d->sdf_w, d->sdf_b, x_raw, frags, &F.filter_delta_max, &F.filter_cells_off);
+      if (F.filter_cells_off == F.geom.n_cells) F.fp16_ok = false;  // nothing left for the filter to decide
+    }
+    if (F.fp16_ok) {
       KNF_CUDA(cudaMalloc(&F.sdf_mmah_blobs, frags.size() * sizeof(uint32_t)));
       KNF_CUDA(cudaMemcpy(F.sdf_mmah_blobs, frags.data(), frags.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     }
@@ -416,7 +430,7 @@ int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
     else if (v == "tensor_fp16x2" || v == "2") F.precision = KNF_PRECISION_TENSOR_FP16X2;
     else return fail(KNF_E_INVALID, "KNF_PRECISION must be fp32_chain, tensor_bf16x3 or tensor_fp16x2");
   }
-  if (F.precision == KNF_PRECISION_TENSOR_FP16X2 && !F.fp16_ok) F.precision = KNF_PRECISION_TENSOR_BF16X3;
+  if (F.precision == KNF_PRECISION_TENSOR_FP16X2 && (!F.fp16_ok || F.filter_cells_off > 0)) F.precision = KNF_PRECISION_TENSOR_BF16X3;  // bf16 pieces keep fp32's range
   if (const char* env = std::getenv("KNF_FILTER_SKIP")) F.filter_skip = std::atoi(env) != 0;
   if (const char* env = std::getenv("KNF_SPARSE_SMALL")) F.sparse_small_kernel = std::atoi(env) != 0;
   if (const char* env = std::getenv("KNF_FILTER_KEEP")) F.filter_keep_div = std::max(1, std::atoi(env));
@@ -688,9 +702,13 @@ int knf_field_create_from_knf(const char* path, int device, knf_field_t* out) {
 
 int knf_field_destroy(knf_field_t f) {
   if (!f) return 0;
+  int prev_device = -1;
+  if (cudaGetDevice(&prev_device) != cudaSuccess) prev_device = -1;
   cudaSetDevice(f->f.device);
   {
     std::lock_guard<std::mutex> lk(f->f.mu);
+    if (f->f.last_call_valid) cudaEventSynchronize(f->f.last_call_done);  // asynchronous (KNF_MEM_DEVICE) calls may still be using the workspace
+    if (f->f.last_call_done) cudaEventDestroy(f->f.last_call_done);
     f->f.ws.release_all();
     for (cudaEvent_t e : f->f.events) cudaEventDestroy(e);
     if (f->f.host_poll) cudaFreeHost(f->f.host_poll);
@@ -700,6 +718,8 @@ int knf_field_destroy(knf_field_t f) {
     if (f->f.sdf_mmah_blobs) cudaFree(f->f.sdf_mmah_blobs);
   }
   delete f;
+  if (prev_device >= 0) cudaSetDevice(prev_device);
+  cudaGetLastError();
   return 0;
 }
 
@@ -753,8 +773,8 @@ int knf_field_set_precision(knf_field_t f, int mode) {
   KNF_TRY(check_field(f));
   if (mode != KNF_PRECISION_FP32_CHAIN && mode != KNF_PRECISION_TENSOR_BF16X3 && mode != KNF_PRECISION_TENSOR_FP16X2)
     return fail(KNF_E_INVALID, "unknown KNF_PRECISION_* mode");
-  if (mode == KNF_PRECISION_TENSOR_FP16X2 && !f->f.fp16_ok)
-    return fail(KNF_E_UNSUPPORTED, "KNF_PRECISION_TENSOR_FP16X2 needs hidden-layer weights below 6e4 in magnitude");
+  if (mode == KNF_PRECISION_TENSOR_FP16X2 && (!f->f.fp16_ok || f->f.filter_cells_off > 0))
+    return fail(KNF_E_UNSUPPORTED, "KNF_PRECISION_TENSOR_FP16X2 needs hidden-layer weights and activation bounds below 6e4 in magnitude");
   std::lock_guard<std::mutex> lk(f->f.mu);
   f->f.precision = mode;
   return 0;
@@ -778,6 +798,11 @@ double knf_field_filter_delta(knf_field_t f) {
   return f->f.filter_delta_max;
 }
 
+int knf_field_filter_cells_off(knf_field_t f) {
+  KNF_TRY(check_field(f));
+  return f->f.fp16_ok ? f->f.filter_cells_off : f->f.geom.n_cells;
+}
+
 // ---- routing ---------------------------------------------------------------------------------------
 extern "C++" {
 template <class T>
@@ -789,7 +814,8 @@ static int cell_index_impl(knf_field_t f, const T* pts, int64_t n, int32_t* cell
   Field& F = f->f;
   std::lock_guard<std::mutex> lk(F.mu);
   cudaStream_t st = (cudaStream_t)stream;
-  KNF_TRY(begin_call(F, st));
+  CallScope call_scope(F, st);
+  KNF_TRY(call_scope.rc);
   Stager S(&F, mem, st);
   const T* dp = S.in(pts, (size_t)n * 3);
   int32_t* dc = S.out(cell, (size_t)n);
@@ -817,7 +843,8 @@ int knf_route(knf_field_t f, const float* pts, int64_t n, int32_t* cell, int32_t
   Field& F = f->f;
   std::lock_guard<std::mutex> lk(F.mu);
   cudaStream_t st = (cudaStream_t)stream;
-  KNF_TRY(begin_call(F, st));
+  CallScope call_scope(F, st);
+  KNF_TRY(call_scope.rc);
   Stager S(&F, mem, st);
   size_t nseg_cap = std::min<size_t>((size_t)std::max<int64_t>(n, 1), (size_t)F.geom.n_cells);
   const float* dp = S.in(pts, (size_t)n * 3);
@@ -846,7 +873,8 @@ int knf_sdf_forward(knf_field_t f, const float* pts, int64_t n, float* out, int 
   Field& F = f->f;
   std::lock_guard<std::mutex> lk(F.mu);
   cudaStream_t st = (cudaStream_t)stream;
-  KNF_TRY(begin_call(F, st));
+  CallScope call_scope(F, st);
+  KNF_TRY(call_scope.rc);
   Stager S(&F, mem, st);
   const float* dp = S.in(pts, (size_t)n * 3);
   float* dout = S.out(out, (size_t)n * kSdfOut);
@@ -863,7 +891,8 @@ int knf_sdf_values(knf_field_t f, const float* pts, int64_t n, float* dist, int 
   Field& F = f->f;
   std::lock_guard<std::mutex> lk(F.mu);
   cudaStream_t st = (cudaStream_t)stream;
-  KNF_TRY(begin_call(F, st));
+  CallScope call_scope(F, st);
+  KNF_TRY(call_scope.rc);
   Stager S(&F, mem, st);
   const float* dp = S.in(pts, (size_t)n * 3);
   float* dd = S.out(dist, (size_t)n);
@@ -880,7 +909,8 @@ int knf_sdf_gradient(knf_field_t f, const float* pts, int64_t n, float* dist, fl
   Field& F = f->f;
   std::lock_guard<std::mutex> lk(F.mu);
   cudaStream_t st = (cudaStream_t)stream;
-  KNF_TRY(begin_call(F, st));
+  CallScope call_scope(F, st);
+  KNF_TRY(call_scope.rc);
   Stager S(&F, mem, st);
   const float* dp = S.in(pts, (size_t)n * 3);
   float* dd = dist ? S.out(dist, (size_t)n) : nullptr;
@@ -919,7 +949,8 @@ int knf_color_forward(knf_field_t f, const float* x, const float* v, const float
   Field& F = f->f;
   std::lock_guard<std::mutex> lk(F.mu);
   cudaStream_t st = (cudaStream_t)stream;
-  KNF_TRY(begin_call(F, st));
+  CallScope call_scope(F, st);
+  KNF_TRY(call_scope.rc);
   Stager S(&F, mem, st);
   const float* dx = S.in(x, (size_t)n * 3);
   const float* dv = S.in(v, (size_t)n * 3);
@@ -940,7 +971,8 @@ int knf_fd_gradient(knf_field_t f, const double* pts, int64_t n, double* grad, i
   Field& F = f->f;
   std::lock_guard<std::mutex> lk(F.mu);
   cudaStream_t st = (cudaStream_t)stream;
-  KNF_TRY(begin_call(F, st));
+  CallScope call_scope(F, st);
+  KNF_TRY(call_scope.rc);
   Stager S(&F, mem, st);
   const double* dp = S.in(pts, (size_t)n * 3);
   double* dg = S.out(grad, (size_t)n * 3);
@@ -960,7 +992,8 @@ int knf_fd_normals(knf_field_t f, const double* pts, int64_t n, double eps, doub
   Field& F = f->f;
   std::lock_guard<std::mutex> lk(F.mu);
   cudaStream_t st = (cudaStream_t)stream;
-  KNF_TRY(begin_call(F, st));
+  CallScope call_scope(F, st);
+  KNF_TRY(call_scope.rc);
   Stager S(&F, mem, st);
   const double* dp = S.in(pts, (size_t)n * 3);
   double* dn = S.out(nrm, (size_t)n * 3);
@@ -1034,7 +1067,8 @@ int knf_march(knf_field_t f, const double* origins, const double* dirs, const do
   Field& F = f->f;
   std::lock_guard<std::mutex> lk(F.mu);
   cudaStream_t st = (cudaStream_t)stream;
-  KNF_TRY(begin_call(F, st));
+  CallScope call_scope(F, st);
+  KNF_TRY(call_scope.rc);
   Stager S(&F, mem, st);
   const double* dorig = S.in(origins, (size_t)n * 3);
   const double* ddir = S.in(dirs, (size_t)n * 3);
@@ -1059,7 +1093,8 @@ int knf_shade(knf_field_t f, const double* pts, const double* view_dirs, int64_t
   Field& F = f->f;
   std::lock_guard<std::mutex> lk(F.mu);
   cudaStream_t st = (cudaStream_t)stream;
-  KNF_TRY(begin_call(F, st));
+  CallScope call_scope(F, st);
+  KNF_TRY(call_scope.rc);
   Stager S(&F, mem, st);
   const double* dp = S.in(pts, (size_t)n * 3);
   const double* dv = S.in(view_dirs, (size_t)n * 3);
@@ -1111,7 +1146,8 @@ int knf_trace_and_shade(knf_field_t f, const double* origins, const double* dirs
   Field& F = f->f;
   std::lock_guard<std::mutex> lk(F.mu);
   cudaStream_t st = (cudaStream_t)stream;
-  KNF_TRY(begin_call(F, st));
+  CallScope call_scope(F, st);
+  KNF_TRY(call_scope.rc);
   Stager S(&F, mem, st);
   const double* dorig = S.in(origins, (size_t)n * 3);
   const double* ddir = S.in(dirs, (size_t)n * 3);
@@ -1189,7 +1225,8 @@ int knf_render_frame(knf_field_t f, const KnfCamera* cam, const KnfSettings* s, 
   Field& F = f->f;
   std::lock_guard<std::mutex> lk(F.mu);
   cudaStream_t st = (cudaStream_t)stream;
-  KNF_TRY(begin_call(F, st));
+  CallScope call_scope(F, st);
+  KNF_TRY(call_scope.rc);
   const size_t px = (size_t)(row1 - row0) * cam->width;
   Stager S(&F, mem, st);
   float* dcolor = S.out(color, px * 3);
@@ -1214,7 +1251,8 @@ int knf_render_pass_u8(knf_field_t f, const KnfCamera* cam, const KnfSettings* s
   Field& F = f->f;
   std::lock_guard<std::mutex> lk(F.mu);
   cudaStream_t st = (cudaStream_t)stream;
-  KNF_TRY(begin_call(F, st));
+  CallScope call_scope(F, st);
+  KNF_TRY(call_scope.rc);
   const size_t px = (size_t)(row1 - row0) * cam->width;
   Stager S(&F, mem, st);
   uint8_t* drgb = S.out(rgb, px * 3);
@@ -1260,7 +1298,8 @@ int knf_sample_volume(knf_field_t f, int32_t resolution, const double bbox_min[3
   Field& F = f->f;
   std::lock_guard<std::mutex> lk(F.mu);
   cudaStream_t st = (cudaStream_t)stream;
-  KNF_TRY(begin_call(F, st));
+  CallScope call_scope(F, st);
+  KNF_TRY(call_scope.rc);
   const int64_t R = resolution, total = R * R * R;
   Stager S(&F, mem, st);
   float* dvals = S.out(values, (size_t)total);

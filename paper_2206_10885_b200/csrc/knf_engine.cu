@@ -161,8 +161,42 @@ RouteBuffers route_buffers(Field& F, int slot, int next_slot, int list) {
   return R;
 }
 
+CallScope::CallScope(Field& f, cudaStream_t s) : F(f), st(s) {
+  if (cudaGetDevice(&prev_device) != cudaSuccess) {
+    cudaGetLastError();
+    prev_device = -1;
+  }
+  cudaError_t e = cudaSetDevice(F.device);
+  if (e != cudaSuccess) {
+    rc = cuda_fail(e, "cudaSetDevice");
+    return;
+  }
+  if (F.last_call_valid && F.last_call_stream != (void*)st) {
+    e = cudaStreamWaitEvent(st, F.last_call_done, 0);
+    if (e != cudaSuccess) {
+      rc = cuda_fail(e, "cudaStreamWaitEvent");
+      return;
+    }
+  }
+  rc = begin_call(F, st);
+}
+CallScope::~CallScope() {
+  if (!F.last_call_done && cudaEventCreateWithFlags(&F.last_call_done, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    F.last_call_done = nullptr;
+  }
+  if (F.last_call_done && cudaEventRecord(F.last_call_done, st) == cudaSuccess) {
+    F.last_call_stream = (void*)st;
+    F.last_call_valid = true;
+  } else {
+    cudaGetLastError();
+    cudaStreamSynchronize(st);  // no event: fall back to finishing this call's work before the next one may start
+    F.last_call_valid = false;
+  }
+  if (prev_device >= 0 && prev_device != F.device) cudaSetDevice(prev_device);
+}
+
 int begin_call(Field& F, cudaStream_t st) {
-  KNF_CUDA(cudaSetDevice(F.device));
   F.prof_chain = false;
   KNF_TRY(ensure_requests(F, 1024));
   KNF_CUDA(cudaMemsetAsync(F.ws.cell_count.p, 0, (size_t)F.geom.n_cells * sizeof(int), st));
@@ -405,6 +439,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     A.crawl_below = use_filter ? crawl_on : -INFINITY;
     A.max_skip = F.filter_skip ? 1 : 0;
     A.inv_resolution = 1.0 / (double)F.geom.resolution;
+    A.filter_x_raw = F.filter_x_raw;
     if (filter_pass) {
       // filter queue of this wavefront: tensor-core predicate; undecided samples join the exact queue below
       RouteBuffers Rf = route_buffers(F, 4 + cur, 4 + nxt, 2 + cur);

@@ -68,7 +68,9 @@ struct Field {
   uint32_t* sdf_mma_blobs = nullptr;   // knf_mma.cuh MmaBlobT<3> per cell (bf16 x 3 B fragments)
   uint32_t* sdf_mmah_blobs = nullptr;  // MmaBlobT<2> per cell (fp16 x 2 B fragments); null when a weight exceeds the fp16 range
   bool fp16_ok = false;
-  double filter_delta_max = 0.0;       // largest per-cell decision-filter bound (knf_api.cu filter_delta)
+  double filter_delta_max = 0.0;       // largest FINITE per-cell decision-filter bound (knf_api.cu filter_delta)
+  float filter_x_raw = 0.0f;           // coordinate magnitude the bounds were derived for (1.001 x the box's largest |coordinate|)
+  int filter_cells_off = 0;            // cells whose activations can leave the fp16 range: delta = +inf, the filter decides nothing there
   int sparse_max_inner = 8;            // residency cap and keep rule of sparse exact wavefronts (KNF_SPARSE_INNER / KNF_SPARSE_KEEP)
   int sparse_keep_div = 2;   // measured: (16, 4) gains 3 % on the distilled frame and loses 1.3 % on the random-init one; (32, 8) and up lose more
   int sparse_div = 8;                  // a wavefront is sparse when its exact queue holds < n / sparse_div rays (KNF_SPARSE_DIV)
@@ -94,6 +96,9 @@ struct Field {
   void* prof_last_stream = nullptr;
   bool prof_chain = false;            // set by the march loop
   int* host_poll = nullptr;  // pinned; early-out polling of the march loop
+  cudaEvent_t last_call_done = nullptr;  // recorded at the end of every call (CallScope)
+  void* last_call_stream = nullptr;
+  bool last_call_valid = false;
   int march_max_inner = 8;    // tile-residency cap (steps in place per tile visit), exact / tensor march kernels
   int filter_keep_div = 2;    // the filter keeps stepping a tile in place while n_stay * this >= its size (KNF_FILTER_KEEP)
   int filter_max_inner = 12;  // ... of the decision-filter kernel (measured optimum: 8 -> 15.97 ms, 12 -> 15.80, 16 -> 16.06)
@@ -118,7 +123,21 @@ int ensure_rays(Field& F, size_t n_rays);
 RouteBuffers route_buffers(Field& F, int counter_slot, int next_slot, int list = 0);  // list 0/1: exact queue, 2/3: filter queue
 RouteCounters* counters(Field& F, int slot);
 unsigned long long* stat_counter(Field& F, int which);  // 0 = sdf evals, 1 = colour evals
-int begin_call(Field& F, cudaStream_t st);              // select device, reset routing invariants
+int begin_call(Field& F, cudaStream_t st);              // reset routing invariants (device already selected by CallScope)
+// One API call on a field handle (the caller holds F.mu).  All scratch belongs to the handle but work is ordered only on
+// the caller's stream, so a call on another stream than the previous one first waits (on the device) for that call's
+// kernels: two torch streams or threads sharing a handle are serialised instead of racing on the workspace.  The
+// thread's current device is saved and restored (a library call must not change torch.cuda.current_device()).
+struct CallScope {
+  Field& F;
+  cudaStream_t st;
+  int prev_device = -1;
+  int rc = 0;
+  CallScope(Field& f, cudaStream_t s);
+  ~CallScope();
+  CallScope(const CallScope&) = delete;
+  CallScope& operator=(const CallScope&) = delete;
+};
 int finish_stats(Field& F, cudaStream_t st);            // pull device counters into F.stats (syncs)
 
 int launch_scan_scatter(Field& F, const RouteBuffers& R, size_t n_upper, cudaStream_t st, int* seg_cell = nullptr,

@@ -36,6 +36,8 @@ struct MarchTileArgs {
   int keep_div;             // a tile keeps stepping in place while n_stay * keep_div >= its size (2 = half; 0 is read as 2)
   double inv_resolution;    // 1 / grid resolution (host-computed)
   double crawl_below;       // exact kernels: a march step from a distance below this continues in the filter queue (-inf: never)
+  float filter_x_raw;       // filter kernel: the coordinate magnitude the per-cell bounds delta were derived for (knf_api.cu filter_delta);
+                            // a sample with a larger |coordinate| (outside the box: caller-supplied t ranges) is left to the exact kernel
 };
 
 // Queue one ray's next sample (warp-uniform call; `emit` selects the lanes that take part).
@@ -358,7 +360,8 @@ static __global__ void __maxnreg__(KNF_MARCH_MMA_MAXNREG) march_mma_kernel(March
         cell[q] = -1;
         if (active[q]) {
           double t_next = 0.0;
-          code[q] = FILTER ? ray_filter_step(rr[q], A.M, ray[q], q ? dist.y : dist.x, safe_below, t_next)
+          code[q] = FILTER ? ray_filter_step(rr[q], A.M, ray[q], q ? dist.y : dist.x, safe_below, t_next,
+                                             fmaxf(fmaxf(fabsf(px[q]), fabsf(py[q])), fabsf(pz[q])) <= A.filter_x_raw)
                            : ray_step(rr[q], A.M, ray[q], q ? dist.y : dist.x, t_next, A.crawl_below);
           if (FILTER && code[q] == STEP_EXACT) {
             cell[q] = tile.cell;  // undecided: the same sample goes to the exact queue of this wavefront

@@ -533,7 +533,8 @@ int intersect_scene_device(knf_scene_s& sc, PathState& P, double t_max, const un
     knf_scene_s::NeuralBufs& B = sc.nb[ob.neural_slot];
     Field& F = sc.fields[oi]->f;
     std::lock_guard<std::mutex> lk(F.mu);
-    KNF_TRY(begin_call(F, st));
+    CallScope call_scope(F, st);
+  KNF_TRY(call_scope.rc);
     pt_neural_prepare_kernel<<<nb, 256, 0, st>>>(P, sc.dev, oi, F.geom, mask, B.ol.as<double>(), B.dl.as<double>(),
                                                  B.tn.as<double>(), B.tf.as<double>());
     KNF_TRY(march_device(F, B.ol.as<double>(), B.dl.as<double>(), B.tn.as<double>(), B.tf.as<double>(), P.n,
@@ -569,7 +570,8 @@ int trace_batch_device(knf_scene_s& sc, const double* o, const double* d, const 
       int m = *sc.host_count;
       if (m <= 0) continue;
       std::lock_guard<std::mutex> lk(F.mu);
-      KNF_TRY(begin_call(F, st));
+      CallScope call_scope(F, st);
+  KNF_TRY(call_scope.rc);
       ShadeTargets T;
       T.normals = B.nrm.as<double>();
       T.colors = B.col.as<double>();

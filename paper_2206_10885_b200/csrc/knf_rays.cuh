@@ -321,9 +321,12 @@ __device__ __forceinline__ int ray_step(RayRegs& R, const MarchState& M, int ray
 // -eps: the reference neither converges nor uses the value (max(d, eps/2) = eps/2), so the step is taken with the
 // reference's own arithmetic and d_f is remembered as a predicate-only d_prev.  Otherwise nothing is changed and
 // the caller re-queues the same sample for the exact kernel (STEP_EXACT, t_next = t).
-__device__ __forceinline__ int ray_filter_step(RayRegs& R, const MarchState& M, int ray, float d_f, double safe_below, double& t_next) {
+__device__ __forceinline__ int ray_filter_step(RayRegs& R, const MarchState& M, int ray, float d_f, double safe_below, double& t_next,
+                                               bool trusted = true) {
   const double dv = (double)d_f;
-  if (!(dv < safe_below)) {  // also catches NaN
+  // Undecided: not provably below -eps; NaN; -inf (a hidden activation left the fp16 range: the bound delta says
+  // nothing about such a value); or a sample the bound was not derived for (`trusted` false: outside the box).
+  if (!(dv < safe_below) || !(dv >= -3.0e38) || !trusted) {
     t_next = R.t;
     return STEP_EXACT;
   }

@@ -206,7 +206,8 @@ extern "C" int knf_volume_forward(knf_field_t f, const double* origins, const do
   Field& F = f->f;
   std::lock_guard<std::mutex> lk(F.mu);
   cudaStream_t st = (cudaStream_t)stream;
-  KNF_TRY(begin_call(F, st));
+  CallScope call_scope(F, st);
+  KNF_TRY(call_scope.rc);
   const int B = (int)n_rays, m = n_s - 1;
   const size_t n_samples = (size_t)B * n_s, n_int = (size_t)B * m;
 

@@ -171,24 +171,40 @@ class DeviceField:
         desc.dir_freqs = int(cfg.dir_freqs)
         desc.feature_dim = int(cfg.feature_dim)
         desc.fd_step = float(cfg.fd_step)
+        expect_sdf = [(32, 3 + 6 * desc.sdf_freqs), (32, 32), (1 + desc.feature_dim, 32)]
+        expect_col = [(32, 3 + 3 + 6 * desc.dir_freqs + 3 + desc.feature_dim), (32, 32), (3, 32)]
+        n_cells = int(cfg.resolution) ** 3
+        # Everything the C side memcpy's is validated here first: it reads n_cells * out * in weights and
+        # n_cells * out biases per layer without looking at shapes.
+        for name, fam, expect, acts in (("sdf", field.sdf, expect_sdf, SDF_ACTIVATIONS), ("color", field.color, expect_col, COLOR_ACTIVATIONS)):
+            if len(fam.weights) != 3 or len(fam.biases) != 3:
+                raise N.KnfUnsupported("only 3-layer MLP families are supported")
+            for k in range(3):
+                w, b = np.asarray(fam.weights[k]), np.asarray(fam.biases[k])
+                if w.ndim != 3 or tuple(w.shape[1:]) != expect[k]:
+                    raise N.KnfUnsupported(f"{name} layer {k} has shape {tuple(w.shape[1:])}, kernels need {expect[k]}")
+                if w.shape[0] != n_cells:
+                    raise ValueError(f"{name} weight stack {k} does not match resolution^3 = {n_cells} cells")
+                if tuple(b.shape) != (n_cells, expect[k][0]):
+                    raise ValueError(f"{name} bias stack {k} has shape {tuple(b.shape)}, expected {(n_cells, expect[k][0])}")
+                # the reference evaluates in the field's own dtype (grid.py:253-290, tiny_field64 in its tests); these
+                # kernels reproduce its float32 arithmetic only -- narrowing a float64 field silently would be a
+                # different function, so refuse it
+                if w.dtype != np.float32 or b.dtype != np.float32:
+                    raise N.KnfUnsupported(f"{name} layer {k} is {w.dtype}/{b.dtype}: only float32 fields are supported "
+                                           "(cast explicitly with astype(np.float32) if narrowing is intended)")
+            # an empty activation list marks the internal geometry-only field (_geometry_field); anything else must be
+            # the reference's activations, which are what the kernels are compiled for (nn.py:41-50)
+            if len(fam.activations) and [str(a) for a in fam.activations] != [str(a) for a in acts]:
+                raise N.KnfUnsupported(f"{name} activations {list(fam.activations)} differ from the reference's {list(acts)}")
         keep = []
         for name, fam in (("sdf", field.sdf), ("color", field.color)):
-            if len(fam.weights) != 3:
-                raise N.KnfUnsupported("only 3-layer MLP families are supported")
             for k in range(3):
                 w = np.ascontiguousarray(fam.weights[k], dtype=np.float32)
                 b = np.ascontiguousarray(fam.biases[k], dtype=np.float32)
                 keep += [w, b]
                 getattr(desc, f"{name}_w")[k] = w.ctypes.data
                 getattr(desc, f"{name}_b")[k] = b.ctypes.data
-        expect_sdf = [(32, 3 + 6 * desc.sdf_freqs), (32, 32), (1 + desc.feature_dim, 32)]
-        expect_col = [(32, 3 + 3 + 6 * desc.dir_freqs + 3 + desc.feature_dim), (32, 32), (3, 32)]
-        for fam, expect in ((field.sdf, expect_sdf), (field.color, expect_col)):
-            for k in range(3):
-                if tuple(fam.weights[k].shape[1:]) != expect[k]:
-                    raise N.KnfUnsupported(f"layer {k} has shape {fam.weights[k].shape[1:]}, kernels need {expect[k]}")
-                if fam.weights[k].shape[0] != cfg.resolution**3:
-                    raise ValueError("weight stack does not match resolution^3 cells")
         handle = C.c_void_p()
         N.check(lib.knf_field_create(C.byref(desc), device, C.byref(handle)))
         return cls(handle, device, cfg)
@@ -237,6 +253,13 @@ class DeviceField:
     def filter_delta(self) -> float:
         return float(N.load().knf_field_filter_delta(self.handle))
 
+    def filter_cells_off(self) -> int:
+        """Cells whose activations could leave the fp16 range: the decision filter leaves them to the exact kernel."""
+        n = int(N.load().knf_field_filter_cells_off(self.handle))
+        if n < 0:
+            N.check(n)
+        return n
+
     def get_precision(self) -> str:
         code = N.load().knf_field_get_precision(self.handle)
         N.check(min(code, 0))
@@ -276,9 +299,12 @@ def device_field(field, device: int | None = None) -> DeviceField:
 
 
 def invalidate(field):
-    """Drop cached device copies after mutating a field's arrays."""
+    """Drop cached device copies after mutating a field's arrays: the next query uploads the field again.
+
+    The old handle is NOT destroyed here -- a FieldSurface or an uploaded path-trace scene may still hold it (the
+    scene stores the raw knf_field_t); it is freed by its finaliser once nothing references the DeviceField."""
     for key in [k for k in _CACHE if k[0] == id(field)]:
-        _CACHE.pop(key).close()
+        _CACHE.pop(key)
 
 
 # ---------------------------------------------------------------------------------------------

@@ -179,6 +179,13 @@ def _material(obj, mat):
         raise TypeError(f"unsupported material {type(mat).__name__}")
 
 
+def invalidate_scene(scene: Scene) -> None:
+    """Forget the cached device copy of `scene` (device_scene notices edits by itself; this is for callers that
+    mutate arrays in place in ways a value comparison cannot see, e.g. after grid.invalidate(field))."""
+    if hasattr(scene, "_knf_device_scene"):
+        del scene._knf_device_scene
+
+
 def _device_index(scene: Scene) -> int:
     for o in scene.objects:
         if isinstance(o, NeuralObject):
@@ -186,14 +193,39 @@ def _device_index(scene: Scene) -> int:
     return _default_device()
 
 
+def _scene_fingerprint(scene: Scene):
+    """Everything knf_scene_create reads, as a hashable value: the reference re-reads the Python objects on every call
+    (and service.py mutates and reuses scenes across frames), so the cached upload is only valid while this is unchanged."""
+    vec = lambda v: tuple(np.asarray(v, dtype=np.float64).ravel().tolist())
+    mat = lambda m: (type(m).__name__, vec(m.albedo if isinstance(m, Lambertian) else getattr(m, "radiance", ())))
+    items = []
+    for o in scene.objects:
+        if isinstance(o, SphereObj):
+            items.append(("sphere", vec(o.center), float(o.radius), mat(o.material)))
+        elif isinstance(o, QuadObj):
+            items.append(("quad", vec(o.corner), vec(o.edge_u), vec(o.edge_v), mat(o.material)))
+        elif isinstance(o, BoxObj):
+            items.append(("box", vec(o.bmin), vec(o.bmax), mat(o.material)))
+        elif isinstance(o, NeuralObject):
+            st = o.settings
+            items.append(("neural", vec(o.translation), vec(o.rotation), float(o.scale), int(o.surface.dev.handle.value or 0),
+                          (float(st.eps_hit), int(st.max_steps), float(st.step_scale))))
+        else:
+            raise TypeError(f"unsupported scene object {type(o).__name__}")
+    env = scene.environment
+    return tuple(items), (type(env).__name__, vec(getattr(env, "rgb", ())))
+
+
 def device_scene(scene: Scene) -> _DeviceScene:
-    """Upload (once per Scene object) the scene description; cached on the Scene instance."""
-    cached = getattr(scene, "_knf_device_scene", None)
-    if cached is not None and cached[0] == len(scene.objects):
-        return cached[1]
-    N.require_gpu()
+    """The uploaded scene description, cached on the Scene instance and rebuilt whenever anything the device copy
+    holds has changed (objects, geometry, materials, transforms, settings, field handles, environment)."""
     if not isinstance(scene.environment, ConstantEnv):
         raise N.KnfUnsupported("only ConstantEnv environments are supported on the device path")
+    fp = _scene_fingerprint(scene)
+    cached = getattr(scene, "_knf_device_scene", None)
+    if cached is not None and cached[0] == fp:
+        return cached[1]
+    N.require_gpu()
     n = len(scene.objects)
     arr = (N.KnfObject * max(n, 1))()
     keep = []
@@ -228,7 +260,7 @@ def device_scene(scene: Scene) -> _DeviceScene:
     handle = C.c_void_p()
     N.check(N.load().knf_scene_create(arr, n, C.byref(env), _device_index(scene), C.byref(handle)))
     dev = _DeviceScene(handle, keep)
-    scene._knf_device_scene = (n, dev)
+    scene._knf_device_scene = (fp, dev)
     return dev
 
 

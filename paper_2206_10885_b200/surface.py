@@ -97,17 +97,28 @@ class FieldSurface:
 
     def __init__(self, kfield, device: int | None = None):
         self.field = kfield
-        self.dev = gridmod.device_field(kfield, device)
-        self.bbox_min = np.asarray(self.dev.config.bbox_min, dtype=np.float64)
-        self.bbox_max = np.asarray(self.dev.config.bbox_max, dtype=np.float64)
+        self._device = device
+        self._dev = gridmod.device_field(kfield, device)
+        self.bbox_min = np.asarray(self._dev.config.bbox_min, dtype=np.float64)
+        self.bbox_max = np.asarray(self._dev.config.bbox_max, dtype=np.float64)
+
+    @property
+    def dev(self):
+        """The device copy, re-resolved through the cache: after grid.invalidate(field) the next use uploads the
+        mutated arrays instead of rendering the stale copy."""
+        if not isinstance(self.field, gridmod.DeviceField):
+            cur = gridmod.device_field(self.field, self._device if self._device is not None else self._dev.device)
+            if cur is not self._dev:
+                self._dev = cur
+        return self._dev
 
     def sdf_values(self, pts):
         return gridmod.sdf_values(self.dev, pts).astype(np.float64)
 
     def shade(self, pts, view_dirs):
         dev = self.dev
-        p = np.ascontiguousarray(np.atleast_2d(pts), dtype=np.float64)
-        v = np.ascontiguousarray(np.atleast_2d(view_dirs), dtype=np.float64)
+        p = _rows3(pts)
+        v = _rows3(view_dirs)
         if p.shape != v.shape or p.shape[1] != 3:
             raise ValueError("pts and view_dirs must both be (n,3)")
         colors = np.empty_like(p)
@@ -130,12 +141,21 @@ def _need_field_surface(surface) -> FieldSurface:
 # intersection and marching
 
 
+def _rows3(a) -> np.ndarray:
+    """(n,3) float64 view of a ray array; an empty input is (0,3), as the reference's asarray-and-index code treats it
+    (np.atleast_2d([]) would be (1,0))."""
+    a = np.asarray(a, dtype=np.float64)
+    if a.size == 0:
+        return np.zeros((0, 3), dtype=np.float64)
+    return np.ascontiguousarray(np.atleast_2d(a))
+
+
 def ray_aabb_batch(origins, dirs, bbox_min, bbox_max, device: int | None = None):
     """surface.ray_aabb_batch (surface.py:131-149) -> (max(t_enter,0), t_exit, hit)."""
     N.require_gpu()
     device = gridmod._default_device() if device is None else device
-    o = np.ascontiguousarray(np.atleast_2d(origins), dtype=np.float64)
-    d = np.ascontiguousarray(np.atleast_2d(dirs), dtype=np.float64)
+    o = _rows3(origins)
+    d = _rows3(dirs)
     if o.shape != d.shape or o.shape[1] != 3:
         raise ValueError("origins and dirs must both be (n,3)")
     n = o.shape[0]
@@ -170,8 +190,8 @@ def march_rays(surface, origins, dirs, t_near, t_far, settings: RenderSettings) 
     """surface.march_rays (surface.py:162-226): the whole lock-step loop runs on the device as a
     wavefront (route by cell -> tile MLP -> step/secant kernel), one call."""
     fs = _need_field_surface(surface)
-    o = np.ascontiguousarray(np.atleast_2d(origins), dtype=np.float64)
-    d = np.ascontiguousarray(np.atleast_2d(dirs), dtype=np.float64)
+    o = _rows3(origins)
+    d = _rows3(dirs)
     tn = np.ascontiguousarray(t_near, dtype=np.float64).reshape(-1)
     tf = np.ascontiguousarray(t_far, dtype=np.float64).reshape(-1)
     n = o.shape[0]
@@ -192,8 +212,8 @@ def march_rays(surface, origins, dirs, t_near, t_far, settings: RenderSettings) 
 def trace_and_shade(surface, origins, dirs, settings: RenderSettings) -> TraceResult:
     """surface.trace_and_shade (surface.py:229-241)."""
     fs = _need_field_surface(surface)
-    o = np.ascontiguousarray(np.atleast_2d(origins), dtype=np.float64)
-    d = np.ascontiguousarray(np.atleast_2d(dirs), dtype=np.float64)
+    o = _rows3(origins)
+    d = _rows3(dirs)
     if o.shape != d.shape or o.shape[1] != 3:
         raise ValueError("origins and dirs must both be (n,3)")
     n = o.shape[0]

@@ -1,0 +1,293 @@
+"""GPU: the decision filter under attack (VERDICT r1 "what's weak" 2) and the host-side hazards ADVICE r1 listed.
+
+The decision filter (knf_march.cuh) may only change WHICH kernel looks at a sample.  Every test here renders / marches
+the same rays with the filter forced off and forced on and demands bit-identical results, on inputs chosen to break
+the assumptions behind the per-cell error bound: samples outside the box (caller-supplied t ranges), weights scaled
+until hidden activations leave the fp16 range, non-zero biases, fine grids, cameras inside the object, tiny step
+budgets.  Each case is also compared with the CPU oracle's march of the same rays."""
+
+import copy
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import oracle_from_product
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2206_10885_b200 import surface
+
+    return surface
+
+
+@pytest.fixture(scope="module")
+def G():
+    from paper_2206_10885_b200 import grid
+
+    return grid
+
+
+def _camera_rays(w, h, pos=(0, 0, 2.5), fov=40):
+    cam = oracle.camera_look_at(pos, (0, 0, 0), (0, 1, 0), np.deg2rad(fov), w, h)
+    o, d = oracle.camera_rays(cam)
+    tn, tf, inside = oracle.slab_intersect(o, d, (-1, -1, -1), (1, 1, 1))
+    return o, d, np.where(inside, tn, 1.0), np.where(inside, tf, 0.0)
+
+
+def _march_on_off(S, field, o, d, tn, tf, settings):
+    """march_rays with the filter off / on / auto; asserts bit-identity, returns (result, stats_on)."""
+    fs = S.FieldSurface(field)
+    out = {}
+    try:
+        for mode in ("off", "on", "auto"):
+            fs.dev.set_filter(mode)
+            fs.dev.reset_stats()
+            out[mode] = (S.march_rays(fs, o, d, tn, tf, settings), fs.dev.stats())
+    finally:
+        fs.dev.set_filter("auto")
+    r0, st0 = out["off"]
+    assert st0["filter_evals"] == 0 and st0["filter_skipped"] == 0
+    for mode in ("on", "auto"):
+        r = out[mode][0]
+        assert np.array_equal(r.hit, r0.hit), mode
+        assert np.array_equal(r.t, r0.t), mode
+        assert np.array_equal(r.steps, r0.steps), mode
+        assert np.array_equal(r.position, r0.position), mode
+    return r0, out["on"][1], fs
+
+
+def _vs_oracle(name, res, field, o, d, tn, tf, cfg, hit_bar, step_bar):
+    ref = oracle.march(oracle.FieldTraceable(oracle_from_product(field)), o, d, tn, tf, cfg)
+    agree = float((res.hit == ref.hit).mean())
+    steps_eq = float((res.steps == ref.steps).mean())
+    both = res.hit & ref.hit
+    drel = np.abs(res.t[both] - ref.t[both]) / np.maximum(np.abs(ref.t[both]), 1e-12) if both.any() else np.zeros(1)
+    print(f"{name}: vs oracle hit agreement {agree:.4%}, steps equal {steps_eq:.4%}, depth rel <= 1e-4 on {np.mean(drel <= 1e-4):.4%} "
+          f"of {int(both.sum())} both-hit rays")
+    assert agree >= hit_bar, name
+    assert steps_eq >= step_bar, name
+    assert np.mean(drel <= 1e-4) >= hit_bar, name
+    return ref
+
+
+def test_filter_with_t_ranges_that_leave_the_box(S, G):
+    """march_rays accepts caller-supplied [t_near, t_far] (surface.py:162-178): samples outside the box clamp to
+    boundary cells with raw coordinates beyond what the filter's bound was derived for.  They must go to the exact
+    kernel; results stay bit-identical and agree with the oracle."""
+    field = G.field_init(G.GridConfig(resolution=16), seed=0)
+    rng = np.random.default_rng(5)
+    n = 6000
+    o = rng.uniform(-2.5, 2.5, size=(n, 3))
+    o[: n // 3] = rng.uniform(-0.9, 0.9, size=(n // 3, 3))  # a third start inside the box
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    tn = np.zeros(n)
+    tf = rng.uniform(0.5, 6.0, size=n)  # far beyond the box for most rays
+    res, st, _ = _march_on_off(S, field, o, d, tn, tf, S.RenderSettings())
+    assert st["filter_evals"] > 0  # the crawl inside the box still runs on the filter
+    # outside the box a random-init network of sin/cos features keeps crawling too, so most rays burn the 128 steps
+    _vs_oracle("t ranges leaving the box", res, field, o, d, tn, tf, oracle.MarchSettings(), 0.995, 0.99)
+
+
+@pytest.mark.parametrize("scale,expect_filter", [(10.0, True), (100.0, False)])
+def test_filter_with_scaled_weights_and_biases(S, G, scale, expect_filter):
+    """Weights x10 / x100 with non-zero biases: activations grow until fp16 operand pieces overflow (x100).  The bound
+    must either still hold (x10, larger delta) or switch the filter off for the cell (delta = +inf)."""
+    field = G.field_init(G.GridConfig(resolution=8), seed=11)
+    rng = np.random.default_rng(12)
+    for k in range(2):  # hidden layers
+        field.sdf.weights[k] *= np.float32(scale)
+    for k in range(3):
+        field.sdf.biases[k] += rng.normal(scale=0.5, size=field.sdf.biases[k].shape).astype(np.float32)
+    field.sdf.biases[2][:, 0] -= np.float32(2.0 * scale)  # keep a negative region so rays crawl
+    o, d, tn, tf = _camera_rays(72, 72)
+    res, st, fs = _march_on_off(S, field, o, d, tn, tf, S.RenderSettings())
+    off = fs.dev.filter_cells_off()
+    print(f"weights x{scale:g}: delta {fs.dev.filter_delta():.3g}, cells off {off}/{8**3}, filter evals {st['filter_evals']}, "
+          f"undecided {st['filter_deferred']}, exact {st['sdf_evals']}")
+    if expect_filter:
+        assert off == 0 and st["filter_evals"] > 0
+    else:
+        assert off == 8**3 and st["filter_evals"] == 0  # every cell's activation bound exceeds the fp16 range
+    # scaled fields are far more chaotic than random-init (|grad d| grows with scale^2): the oracle comparison is a
+    # sanity bar, bit-identity above is the proof
+    _vs_oracle(f"weights x{scale:g}", res, field, o, d, tn, tf, oracle.MarchSettings(), 0.97, 0.95)
+
+
+def test_filter_with_some_cells_beyond_fp16(S, G):
+    """Only a slab of cells gets x200 weights: those cells carry delta = +inf and are served by the exact kernel while
+    their neighbours keep the filter."""
+    field = G.field_init(G.GridConfig(resolution=8), seed=4)
+    big = np.zeros((8, 8, 8), dtype=bool)
+    big[:, :, 3:5] = True
+    big = big.reshape(-1)
+    for k in range(2):
+        field.sdf.weights[k][big] *= np.float32(200.0)
+    o, d, tn, tf = _camera_rays(64, 64)
+    res, st, fs = _march_on_off(S, field, o, d, tn, tf, S.RenderSettings())
+    assert fs.dev.filter_cells_off() == int(big.sum())
+    assert st["filter_evals"] > 0 and st["filter_deferred"] > 0
+    _vs_oracle("x200 slab", res, field, o, d, tn, tf, oracle.MarchSettings(), 0.97, 0.95)
+
+
+def test_filter_on_a_32_cubed_field(S, G):
+    field = G.field_init(G.GridConfig(resolution=32), seed=2)
+    o, d, tn, tf = _camera_rays(96, 96, pos=(0.4, 0.3, 2.4))
+    res, st, _ = _march_on_off(S, field, o, d, tn, tf, S.RenderSettings())
+    assert st["filter_evals"] > st["sdf_evals"]
+    _vs_oracle("32^3", res, field, o, d, tn, tf, oracle.MarchSettings(), 0.995, 0.99)
+
+
+def test_filter_with_camera_inside_the_object(S, distilled_field):
+    """Camera inside the distilled sphere: every ray starts in the negative region and crawls outwards."""
+    o, d, _, _ = _camera_rays(80, 80, pos=(0.05, 0.02, 0.1), fov=70)
+    tn, tf, inside = oracle.slab_intersect(o, d, (-1, -1, -1), (1, 1, 1))
+    assert inside.all()
+    res, st, _ = _march_on_off(S, distilled_field, o, d, tn, tf, S.RenderSettings())
+    assert st["filter_evals"] > 0
+    _vs_oracle("camera inside", res, distilled_field, o, d, tn, tf, oracle.MarchSettings(), 0.999, 0.995)
+
+
+@pytest.mark.parametrize("max_steps", [1, 7, 128])
+def test_filter_with_step_budgets(S, G, max_steps):
+    field = G.field_init(G.GridConfig(resolution=16), seed=0)
+    o, d, tn, tf = _camera_rays(64, 64)
+    settings = S.RenderSettings(max_steps=max_steps)
+    res, st, _ = _march_on_off(S, field, o, d, tn, tf, settings)
+    assert res.steps.max() <= max_steps
+    _vs_oracle(f"max_steps={max_steps}", res, field, o, d, tn, tf, oracle.MarchSettings(max_steps=max_steps), 0.995, 0.99)
+
+
+def test_frames_identical_filter_on_off_vs_oracle(S, G):
+    """Whole frames (march + refinement + FD normals + colour), filter off / on, and against oracle.render."""
+    from paper_2206_10885_b200 import cameras
+
+    field = G.field_init(G.GridConfig(resolution=16), seed=0)
+    pose = cameras.look_at_pose((0.3, 0.4, 2.4), (0, 0, 0), (0, 1, 0), np.deg2rad(40), 128, 128)
+    fs = S.FieldSurface(field)
+    frames = {}
+    try:
+        for mode in ("off", "on"):
+            fs.dev.set_filter(mode)
+            frames[mode] = S.render_frame(fs, pose)
+    finally:
+        fs.dev.set_filter("auto")
+    for k in ("color", "depth", "normal", "hit"):
+        assert np.array_equal(getattr(frames["on"], k), getattr(frames["off"], k)), k
+    ocam = oracle.camera_look_at((0.3, 0.4, 2.4), (0, 0, 0), (0, 1, 0), np.deg2rad(40), 128, 128)
+    ref = oracle.render(oracle.FieldTraceable(oracle_from_product(field)), ocam, oracle.MarchSettings())
+    fb = frames["on"]
+    agree = (fb.hit == ref.hit).mean()
+    both = fb.hit & ref.hit
+    rel = np.abs(fb.depth[both] - ref.depth[both]) / ref.depth[both]
+    print(f"128^2 filtered frame vs oracle: hits {agree:.4%}, depth<=1e-4 {np.mean(rel <= 1e-4):.4%}")
+    assert agree >= 0.998 and np.mean(rel <= 1e-4) >= 0.998
+
+
+# ---- host-side hazards ------------------------------------------------------------------------------
+
+
+def test_degenerate_gradient_raises(G):
+    """pkg/tests/test_grid.py:255-267: an all-zero SDF family has no gradient anywhere."""
+    field = G.field_init(G.GridConfig(resolution=4), seed=7)
+    for w in field.sdf.weights:
+        w[...] = 0
+    for b in field.sdf.biases:
+        b[...] = 0
+    with pytest.raises(G.DegenerateGradientError):
+        G.normal(field, np.array([0.2, 0.2, 0.2]))
+    nrm, ok = G.normal_batch(field, np.array([[0.2, 0.2, 0.2], [-0.5, 0.1, 0.9]]))
+    assert not ok.any() and np.all(np.isfinite(nrm))  # never NaN (the reference's test name says as much)
+
+
+def test_empty_march_and_trace(S, small_field):
+    fs = S.FieldSurface(small_field)
+    r = S.march_rays(fs, [], [], [], [], S.RenderSettings())
+    assert r.hit.shape == (0,) and r.t.shape == (0,) and r.position.shape == (0, 3) and r.steps.shape == (0,)
+    r = S.trace_and_shade(fs, np.zeros((0, 3)), np.zeros((0, 3)), S.RenderSettings())
+    assert r.hit.shape == (0,) and r.color.shape == (0, 3)
+
+
+def test_upload_rejects_what_it_cannot_reproduce(G, small_field):
+    from paper_2206_10885_b200._native import KnfUnsupported
+
+    f64 = G.field_init(G.GridConfig(resolution=2), seed=1, dtype=np.float64)
+    with pytest.raises(KnfUnsupported):
+        G.sdf_values(f64, np.zeros((4, 3), np.float32))  # the reference evaluates a float64 field in float64
+    bad = copy.deepcopy(small_field)
+    bad.sdf.biases[1] = bad.sdf.biases[1][:, :16]
+    with pytest.raises(ValueError):
+        G.sdf_values(bad, np.zeros((4, 3), np.float32))
+    bad = copy.deepcopy(small_field)
+    bad.sdf.activations = [G.RELU, G.SOFTPLUS, G.IDENTITY]
+    with pytest.raises(KnfUnsupported):
+        G.sdf_values(bad, np.zeros((4, 3), np.float32))
+
+
+def test_invalidate_reuploads_and_keeps_live_handles_valid(S, G):
+    """grid.invalidate() after mutating a field: the next query sees the new weights, a FieldSurface built earlier
+    follows, and a path-trace scene that captured the old handle keeps rendering (no use-after-free)."""
+    from paper_2206_10885_b200 import cameras, pathtrace
+
+    field = G.field_init(G.GridConfig(resolution=4), seed=3)
+    pts = np.random.default_rng(0).uniform(-1, 1, size=(512, 3)).astype(np.float32)
+    fs = S.FieldSurface(field)
+    before = G.sdf_values(field, pts)
+    scene = pathtrace.Scene([pathtrace.QuadObj((-2, -1.01, -2), (4, 0, 0), (0, 0, 4), pathtrace.Lambertian((0.7, 0.7, 0.7))),
+                             pathtrace.NeuralObject(fs)], pathtrace.ConstantEnv((1, 1, 1)))
+    pose = cameras.look_at_pose((0, 0.5, 2.8), (0, 0, 0), (0, 1, 0), np.deg2rad(40), 24, 24)
+    img0 = pathtrace.render_pathtraced(scene, pose, spp=1, seed=1).hdr
+    field.sdf.biases[2][:, 0] += np.float32(0.25)
+    G.invalidate(field)
+    after = G.sdf_values(field, pts)
+    assert np.allclose(after - before, 0.25, atol=1e-6)
+    assert np.allclose(fs.sdf_values(pts.astype(np.float64)) - before, 0.25, atol=1e-6)  # the surface re-resolved its device copy
+    img1 = pathtrace.render_pathtraced(scene, pose, spp=1, seed=1).hdr  # scene notices the new handle and rebuilds
+    assert np.all(np.isfinite(img1)) and img1.shape == img0.shape
+    fresh = pathtrace.Scene(list(scene.objects), scene.environment)
+    assert np.array_equal(pathtrace.render_pathtraced(fresh, pose, spp=1, seed=1).hdr, img1)
+
+
+def test_scene_cache_follows_edits(S, distilled_field):
+    """pathtrace.device_scene caches the upload on the Scene; the reference re-reads the Python objects on every call
+    (service.py mutates and reuses scenes), so edits must show."""
+    from paper_2206_10885_b200 import cameras, pathtrace
+
+    quad = pathtrace.QuadObj((-2, -0.8, -2), (4, 0, 0), (0, 0, 4), pathtrace.Lambertian((0.7, 0.7, 0.7)))
+    ball = pathtrace.SphereObj((0.0, 0.0, 0.0), 0.5, pathtrace.Lambertian((0.9, 0.2, 0.2)))
+    scene = pathtrace.Scene([quad, ball], pathtrace.ConstantEnv((1, 1, 1)))
+    pose = cameras.look_at_pose((0, 0.6, 3.0), (0, 0, 0), (0, 1, 0), np.deg2rad(40), 32, 32)
+    a = pathtrace.render_pathtraced(scene, pose, spp=2, seed=3).hdr
+    scene.objects[1] = pathtrace.SphereObj((0.4, 0.0, 0.0), 0.5, pathtrace.Lambertian((0.2, 0.9, 0.2)))  # same count, new object
+    b = pathtrace.render_pathtraced(scene, pose, spp=2, seed=3).hdr
+    ref = pathtrace.render_pathtraced(pathtrace.Scene([quad, scene.objects[1]], pathtrace.ConstantEnv((1, 1, 1))), pose, spp=2, seed=3).hdr
+    assert not np.array_equal(a, b) and np.array_equal(b, ref)
+    scene.environment = pathtrace.ConstantEnv((0.2, 0.3, 0.9))
+    c = pathtrace.render_pathtraced(scene, pose, spp=2, seed=3).hdr
+    assert not np.array_equal(b, c)
+
+
+def test_two_streams_share_a_handle(S, G):
+    """KNF_MEM_DEVICE calls return while their kernels run; a call on ANOTHER stream must wait for them instead of
+    reusing the handle's workspace underneath (CallScope, knf_engine.cu).  Also: a call must not change the caller's
+    current device."""
+    import torch
+
+    field = G.field_init(G.GridConfig(resolution=8), seed=9)
+    dev = G.device_field(field)
+    pts = torch.rand((400_000, 3), device="cuda", dtype=torch.float32) * 2 - 1
+    want = G.sdf_query(dev, pts).value.clone()
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for rep in range(6):
+        with torch.cuda.stream(s1 if rep % 2 == 0 else s2):
+            outs.append(G.sdf_query(dev, pts).value)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o, want)
+    assert torch.cuda.current_device() == 0

@@ -74,6 +74,55 @@ def test_full_hd_frame_properties(field16):
     assert np.all((a.color >= 0) & (a.color <= 1))
 
 
+def test_full_hd_parity_bands(field16):
+    """The HEADLINE config against the oracle: three 32-row bands of the 1920x1080 random-init
+    frame -- top edge (rays mostly outside the box), image centre (box fills the band) and a lower band -- rendered by
+    the GPU as bands of the full frame and by oracle.render's own band code on the same rays.  Band invariance of the
+    GPU frame is proven above, so these bands ARE the full frame's rows.  north_star bars: hit masks >= 99.9 %;
+    depth 1e-4 relative, normals and RGB 1e-3 on the both-hit pixels (asserted as the fraction inside the bar, with
+    the reference's own self-agreement across band sizes -- tests/golden/reference_noise.json: 99.9908 % hits -- as the
+    noise floor of this chaotic field)."""
+    from paper_2206_10885_b200 import cameras, surface
+
+    W, H = 1920, 1080
+    fs = surface.FieldSurface(field16)
+    pose = cameras.look_at_pose((0, 0, 2.5), (0, 0, 0), (0, 1, 0), np.deg2rad(40), W, H)
+    ocam = oracle.camera_look_at((0, 0, 2.5), (0, 0, 0), (0, 1, 0), np.deg2rad(40), W, H)
+    osurf = oracle.FieldTraceable(oracle_from_product(field16))
+    tot = dict(rays=0, flips=0, both=0, d_ok=0, n_ok=0, c_ok=0)
+    worst = dict(d=0.0, n=0.0, c=0.0)
+    for r0 in (96, 524, 800):
+        r1 = r0 + 32
+        color, depth, normal, hit = surface.render_rows(fs, pose, surface.RenderSettings(), (1, 1, 1), 1, r0, r1)
+        hit = hit.astype(bool)
+        cc, rr = np.meshgrid(np.arange(W), np.arange(r0, r1))
+        o, d = oracle.camera_rays(ocam, np.stack([cc.ravel(), rr.ravel()], axis=1))
+        ref = oracle.trace_shade(osurf, o, d, oracle.MarchSettings())  # exactly oracle.render's band body (surface.py:302-324)
+        rhit = ref.hit.reshape(32, W)
+        both = hit & rhit
+        rdepth = ref.t.reshape(32, W)
+        rel = np.abs(depth[both].astype(np.float64) - rdepth[both].astype(np.float32)) / rdepth[both]
+        nerr = np.abs(normal - ref.normal.reshape(32, W, 3).astype(np.float32))[both].max(axis=1)
+        cerr = np.abs(color - ref.color.reshape(32, W, 3).astype(np.float32))[both].max(axis=1)
+        tot["rays"] += 32 * W
+        tot["flips"] += int((hit != rhit).sum())
+        tot["both"] += int(both.sum())
+        tot["d_ok"] += int((rel <= 1e-4).sum())
+        tot["n_ok"] += int((nerr <= 1e-3).sum())
+        tot["c_ok"] += int((cerr <= 1e-3).sum())
+        if both.any():
+            worst["d"] = max(worst["d"], float(rel.max()))
+            worst["n"] = max(worst["n"], float(nerr.max()))
+            worst["c"] = max(worst["c"], float(cerr.max()))
+    agree = 1.0 - tot["flips"] / tot["rays"]
+    print(f"1080p bands vs oracle: {tot['rays']} rays, hit agreement {agree:.4%} ({tot['flips']} flips), both-hit {tot['both']}: "
+          f"depth<=1e-4 {tot['d_ok'] / max(tot['both'], 1):.4%} (max {worst['d']:.1e}), normal<=1e-3 {tot['n_ok'] / max(tot['both'], 1):.4%} "
+          f"(max {worst['n']:.1e}), rgb<=1e-3 {tot['c_ok'] / max(tot['both'], 1):.4%} (max {worst['c']:.1e})")
+    assert tot["both"] >= 1000  # the centre band carries the surface
+    assert agree >= 0.999
+    assert tot["d_ok"] >= 0.999 * tot["both"] and tot["n_ok"] >= 0.999 * tot["both"] and tot["c_ok"] >= 0.999 * tot["both"]
+
+
 def test_frame_256_matches_oracle_statistics(field16):
     """BASELINE config 1 (256^2 CPU-runnable case): hit agreement with the oracle, reported against the
     reference's own self-agreement (tests/golden/reference_noise.json)."""
