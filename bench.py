@@ -4,10 +4,13 @@
 
     python bench.py --gpus 1 --steps 20 --warmup 3           # our arm, one GPU
     torchrun --nproc-per-node N ... bench.py --gpus N ...    # one rank per GPU, views sharded (weak scaling)
-    python bench.py --impl reference --gpus 1 ...            # the reference algorithm's CPU path (oracle port)
+    torchrun ... bench.py --gpus N --shard rows              # one frame per step split into interleaved row bands (strong scaling)
+    python bench.py --impl reference --gpus 1 ...            # the reference's own CPU renderer (oracle/_ref: the unmodified
+                                                             # kilofield package, installed by oracle/build_ref.py), all host threads
 
 One "step" = every rank renders one orbit view (view = step * N + rank) with the field resident in
-HBM, then the finished colour frames are all-gathered over NCCL.  Prints ONE JSON line (rank 0).
+HBM, then the finished buffers (colour, depth, normal, hit) are all-gathered over NCCL.  Prints ONE JSON line (rank 0).
+At N = 1 the line also carries the other BASELINE.json configs (`configs`: 2 orbit, 4 batched forward, 5 4K path trace).
 """
 
 from __future__ import annotations
@@ -140,70 +143,232 @@ def orbit_view(k: int, width: int, height: int):
     return orbit_pose(k % ORBIT_VIEWS, ORBIT_VIEWS, ORBIT_RADIUS, ORBIT_ELEV, FOV, width, height)
 
 
-def oracle_rays_per_second(width: int, height: int, view: int, repeats: int = 1):
-    """Times the CPU restatement of the reference renderer (oracle/, NumPy + OpenBLAS) on a
-    (width x height) raster of the SAME camera and field.  Returns (rays/s, seconds, frame)."""
+def _reference_package():
+    """The unmodified reference (kilofield) installed in oracle/_ref by oracle/build_ref.py, or None."""
+    try:
+        from oracle import build_ref
+
+        return build_ref.import_reference() if build_ref.available() else None
+    except Exception:
+        return None
+
+
+_REF_CACHE: dict = {}
+
+
+def cpu_frame_seconds(width: int, height: int, view: int, threads: int):
+    """One (width x height) frame of the SAME camera and field on the host CPU: the reference's own
+    kilofield.surface.render_frame (kind "reference") when oracle/_ref is installed, else the oracle port of it
+    (kind "port").  Returns (seconds, kind, hit_fraction).  KNF_THREADS is the reference's own knob (surface.py:32-39)."""
+    pose = orbit_view(view, width, height)
+    kf = _reference_package()
+    os.environ["KNF_THREADS"] = str(max(1, int(threads)))
+    if kf is not None:
+        if "ref" not in _REF_CACHE:
+            field = kf.grid.field_init(kf.grid.GridConfig(), seed=0)
+            _REF_CACHE["ref"] = kf.surface.FieldSurface(field)
+        cam = kf.cameras.CameraPose(np.asarray(pose.position, dtype=np.float64), np.asarray(pose.rotation, dtype=np.float64),
+                                    float(pose.fov_y), int(width), int(height))
+        t0 = time.perf_counter()
+        fb = kf.surface.render_frame(_REF_CACHE["ref"], cam, kf.surface.RenderSettings())
+        return time.perf_counter() - t0, "reference", float(fb.hit.mean())
     import oracle
 
-    spec = oracle.FieldSpec(resolution=16)
-    field = oracle.make_random_field(spec, seed=0)
-    pose = orbit_view(view, width, height)
+    if "port" not in _REF_CACHE:
+        _REF_CACHE["port"] = oracle.FieldTraceable(oracle.make_random_field(oracle.FieldSpec(resolution=16), seed=0))
     cam = oracle.Camera(pose.position, pose.rotation, pose.fov_y, width, height)
-    surf = oracle.FieldTraceable(field)
-    best = None
-    for _ in range(repeats):
-        t0 = time.perf_counter()
-        frame = oracle.render(surf, cam, oracle.MarchSettings())
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    return width * height / best, best, frame
+    t0 = time.perf_counter()
+    frame = oracle.render(_REF_CACHE["port"], cam, oracle.MarchSettings())
+    return time.perf_counter() - t0, "port", float(frame.hit.mean())
 
 
 def sample_raster(budget_rays: float):
-    """A 16:9 raster with about `budget_rays` rays, between 64x36 and 384x216."""
-    h = int(np.clip(np.sqrt(budget_rays * 9 / 16), 36, 216))
+    """A 16:9 raster with about `budget_rays` rays, between 64x36 and 480x270."""
+    h = int(np.clip(np.sqrt(budget_rays * 9 / 16), 36, 270))
     return (h * 16) // 9, h
 
 
+def host_description():
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"host_cpus": os.cpu_count(), "cpu_model": model, "numpy": np.__version__}
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the reference algorithm on the host CPU (oracle port of its NumPy renderer;
-    the reference itself is Python and is not present on the GPU box).  Rank 0 only."""
+    """--impl reference: the reference's own CPU renderer on this box's host cores, rank 0 only.
+
+    Timed steps: each step renders ONE bounded sample raster (same orbit view, same field, same settings) with
+    KNF_THREADS = all host cores -- `ms_per_step` is the time of exactly those steps.  `value` (frames/s at WxH) comes from
+    ONE full WxH frame rendered un-extrapolated after the steps (BENCH_REF_FULL=0 skips it and scales the sample per
+    ray instead, labelled as such); the 1-thread figure (BASELINE.md section 3 asks for both) is measured on the sample raster."""
     if rank != 0:
         return
     W, H = args.width, args.height
     total = args.steps + args.warmup
-    w, h = sample_raster(150.0 * 8000.0 / max(total, 1))
-    times = []
+    ncpu = os.cpu_count() or 1
+    w, h = sample_raster(48.0 * 20000.0 / max(total, 1))  # ~20 krays/s on one core: ~48 s for all the steps together
+    times, kind = [], "port"
     for s in range(total):
-        rps, dt, _ = oracle_rays_per_second(w, h, s)
+        dt, kind, _ = cpu_frame_seconds(w, h, s, ncpu)
         if s >= args.warmup:
             times.append(dt)
     sec = float(np.sum(times))
-    rays_per_s = len(times) * w * h / sec
-    fps = rays_per_s / (W * H)
-    sample = f"{w}x{h} raster of the same orbit views per step, extrapolated per ray to {W}x{H}"
+    sample_rps_all = len(times) * w * h / sec
+    one = [cpu_frame_seconds(w, h, args.warmup, 1)[0] for _ in range(2)]
+    sample_rps_one = w * h / min(one)
+    full = None
+    if os.environ.get("BENCH_REF_FULL", "1") != "0":
+        threads_full = ncpu if sample_rps_all >= sample_rps_one else 1
+        dt, kind, hitf = cpu_frame_seconds(W, H, args.warmup, threads_full)
+        full = {"seconds": dt, "threads": threads_full, "hit_fraction": hitf, "fps": 1.0 / dt, "krays_per_s": W * H / dt / 1e3}
+    fps = full["fps"] if full else max(sample_rps_all, sample_rps_one) / (W * H)
+    what = "kilofield.surface.render_frame of the unmodified reference package (oracle/_ref)" if kind == "reference" else \
+        "oracle.render, the NumPy restatement of the reference renderer (oracle/_ref not installed on this box)"
+    sample = (f"{what}; value = one full {W}x{H} frame, un-extrapolated ({full['seconds']:.1f} s, KNF_THREADS={full['threads']})" if full else
+              f"{what}; value extrapolated per ray from the {w}x{h} sample raster (BENCH_REF_FULL=0)")
+    sample += (f"; the {args.steps} timed steps are {w}x{h} rasters of the same orbit views at KNF_THREADS={ncpu} ({sample_rps_all / 1e3:.1f} krays/s; "
+               f"{sample_rps_one / 1e3:.1f} krays/s at KNF_THREADS=1)")
     line = {
         "impl": "reference", "metric": f"fps_{W}x{H}_sphere_traced", "value": fps, "unit": "frames/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / fps, "higher_is_better": True, "scaling": "weak",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / max(len(times), 1), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": workload_config(W, H, world),
-        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": 1, "kind": "port", "sample": sample,
-                         "host_cpus": os.cpu_count(), "numpy": np.__version__, "krays_per_s": rays_per_s / 1e3},
+        "config": workload_config(W, H, world, args.shard),
+        "ms_per_step_is": f"one {w}x{h} sample raster per step (what the timed steps rendered); a {W}x{H} frame takes 1e3 / value ms",
+        "cpu_baseline": dict({"value": fps, "unit": "frames/s", "cores": (full["threads"] if full else ncpu), "kind": kind, "sample": sample,
+                              "full_frame": full, "sample_raster": [w, h], "sample_krays_per_s_all_threads": sample_rps_all / 1e3,
+                              "sample_krays_per_s_1_thread": sample_rps_one / 1e3}, **host_description()),
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def workload_config(W, H, world):
+def workload_config(W, H, world, shard="views"):
+    """The SAME dict in both arms (the reference arm renders the same views of the same field with the same settings)."""
     return {
         "workload": f"{W}x{H} sphere-traced colour pass (primary rays, secant refinement, FD normals, colour MLP) of a "
                     "random-init 16^3 KiloNeuS grid (seed 0, MLPs 39-32-32-9 / 41-32-32-3), RenderSettings defaults "
                     "(eps 1e-3, 128 steps, scale 0.8), orbit views r=2.5 el=0.2 fov 40deg (BASELINE config 3)",
-        "views_per_step": world, "parallelism": f"view-sharded x{world}, field replicated, final all_gather of colour frames",
+        "views_per_step": world if shard == "views" else 1,
+        "parallelism": (f"view-sharded x{world}" if shard == "views" else f"one frame per step in interleaved 32-row bands x{world}") +
+                       ", field replicated, final all_gather of the colour / depth / normal / hit buffers",
         "preheat": f"{PREHEAT_FRAMES} untimed frames before the warm-up steps (idle B200 clocks need 1-2 s of load to settle)",
         "l2": "no explicit flush: the per-step working set (ray state + request buffers, >400 MB) exceeds the 126 MB L2; "
               "the 45 MB SDF weight blobs are meant to stay L2-resident",
     }
+
+
+def ncu_traffic(which: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture (profiles/ncu_traffic.json:
+    {"filter": {"kernel": ..., "dram_bytes_per_launch": ...}, ...}); None when absent or captured from another kernel."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            ent = json.load(fh).get(which)
+        if ent and (which != "filter" or ent.get("kernel") == filter_kernel_name()):
+            return float(ent["dram_bytes_per_launch"])
+    except Exception:
+        pass
+    return None
+
+
+def filter_kernel_name():
+    try:
+        from paper_2206_10885_b200 import _native as N
+
+        fn = getattr(N.load(), "knf_filter_kernel_name", None)
+        if fn is not None:
+            import ctypes
+
+            fn.restype = ctypes.c_char_p
+            return fn().decode()
+    except Exception:
+        pass
+    return "march_mma_kernel<2, true>"
+
+
+def _event_ms(fn, warm=1, it=3):
+    import torch
+
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(it):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def other_configs(fs, field, peaks, ffma_peak, tensor_peak):
+    """BASELINE.json configs 2, 4 and 5 on one GPU, device-resident, CUDA-event timed (median of 3 after a warm-up).
+    Reported next to the headline so every config has a driver-run number; not part of `value`."""
+    import torch
+
+    from paper_2206_10885_b200 import cameras, grid, pathtrace, surface
+    from paper_2206_10885_b200.modelio import load_model
+
+    out = {}
+    dev = fs.dev
+    settings = surface.RenderSettings()
+    # config 4: batched multi-network forward, uniform points over all cells (cli.py:177-178), per precision mode
+    fwd = {}
+    for M in (1_000_000, 1 << 24):
+        pts = torch.as_tensor(np.random.default_rng(0).uniform(-1, 1, (M, 3)).astype(np.float32), device=f"cuda:{dev.device}")
+        for mode in ("fp32_chain", "tensor_bf16x3", "tensor_fp16x2"):
+            try:
+                dev.set_precision(mode)
+            except Exception:
+                continue
+            ms = _event_ms(lambda: grid.sdf_query(dev, pts))
+            tf = M * FLOP_PER_SDF_EVAL / ms / 1e9
+            peak = ffma_peak if mode == "fp32_chain" else tensor_peak
+            fwd[f"sdf_{mode}_{M}"] = {"ms": ms, "Gq_per_s": M / ms / 1e6, "tflops": tf, "frac_of_peak": tf / peak,
+                                      "peak": peak, "bound": "fp32" if mode == "fp32_chain" else "tensor"}
+        dev.set_precision("fp32_chain")
+        z = grid.sdf_query(dev, pts).features.contiguous()
+        v = torch.nn.functional.normalize(torch.randn(M, 3, device=pts.device), dim=1)
+        ms = _event_ms(lambda: grid.color_query(dev, pts, v, v, z))
+        tf = M * FLOP_PER_COLOR_EVAL / ms / 1e9
+        fwd[f"color_fp32_chain_{M}"] = {"ms": ms, "Gq_per_s": M / ms / 1e6, "tflops": tf, "frac_of_peak": tf / ffma_peak, "peak": ffma_peak, "bound": "fp32"}
+        del pts, z, v
+    out["config4_batched_forward"] = dict(fwd, note="uniform points over all 4096 cells (244 and 4096 per cell); 5120 / 4864 flop per query; I/O 12 B in + 36 B out (SDF)")
+    # config 2: 800x800 orbit, primary rays + normals + colour, 25 of the 100 views (every 4th)
+    def orbit(surf, views=25):
+        for k in range(views):
+            surface.render_rows(surf, cameras.orbit_pose(4 * k, 100, ORBIT_RADIUS, ORBIT_ELEV, FOV, 800, 800), settings, (1, 1, 1), 1, 0, 800, device_out=True)
+    ms = _event_ms(lambda: orbit(fs), warm=1, it=1)
+    out["config2_orbit_800x800_random_init_16"] = {"views": 25, "ms_total": ms, "fps": 25e3 / ms, "mrays_per_s": 25 * 640000 / ms / 1e3}
+    trained = {}
+    for name in ("sphere_stripes_r16_distilled.knf", "sphere_stripes_r8_distilled.knf", "sphere_r4_distilled.knf"):
+        path = os.path.join(ROOT, "tests", "golden", name)
+        if os.path.exists(path):
+            trained[name] = surface.FieldSurface(load_model(path))
+    for name, surf in trained.items():
+        ms = _event_ms(lambda: orbit(surf), warm=1, it=1)
+        out[f"config2_orbit_800x800_{name}"] = {"views": 25, "ms_total": ms, "fps": 25e3 / ms, "mrays_per_s": 25 * 640000 / ms / 1e3}
+        pose = orbit_view(3, 1920, 1080)
+        ms = _event_ms(lambda: surface.render_rows(surf, pose, settings, (1, 1, 1), 1, 0, 1080, device_out=True), warm=2, it=5)
+        out[f"config3_1920x1080_{name}"] = {"ms": ms, "fps": 1e3 / ms, "note": "trained field: the decision filter switches itself off, this is the exact FP32 path"}
+    # config 5: 3840x2160 path tracing, floor quad + neural object, 1 spp, 8 bounces
+    pose = cameras.look_at_pose((0.5, 0.8, 3.2), (0, -0.2, 0), (0, 1, 0), np.deg2rad(45), 3840, 2160)
+    quad = pathtrace.QuadObj((-3, -1.0, -3), (6, 0, 0), (0, 0, 6), pathtrace.Lambertian((0.7, 0.7, 0.7)))
+    surfs = {"random_init_16": fs}
+    surfs.update({k: v for k, v in list(trained.items())[:1]})
+    for name, surf in surfs.items():
+        scene = pathtrace.Scene([quad, pathtrace.NeuralObject(surf)], pathtrace.ConstantEnv((1, 1, 1)))
+        ms = _event_ms(lambda: pathtrace.pathtrace_rows(scene, pose, 1, 0, 8, 0, 0, 2160, device_out=True), warm=1, it=2)
+        out[f"config5_pathtrace_3840x2160_spp1_{name}"] = {"ms": ms, "Mpaths_per_s": 3840 * 2160 / ms / 1e3}
+    return out
 
 
 def main():
@@ -215,6 +380,9 @@ def main():
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="views", choices=["views", "rows"],
+                    help="N > 1: one view per rank and step (weak scaling) or one frame per step in interleaved row bands (strong)")
+    ap.add_argument("--no-extras", action="store_true", help="skip the other BASELINE configs (2, 4, 5) appended at N = 1")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
 
@@ -229,7 +397,8 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2206_10885_b200 import _native as N
+    from paper_2206_10885_b200 import _native as N  # noqa: F401
+    from paper_2206_10885_b200 import dist as kdist
     from paper_2206_10885_b200 import grid, surface
 
     if not torch.cuda.is_available():
@@ -246,14 +415,34 @@ def main():
     fs = surface.FieldSurface(field, device=local)
     settings = surface.RenderSettings()
     dev = torch.device("cuda", local)
-    bufs = (torch.empty((H, W, 3), dtype=torch.float32, device=dev), torch.empty((H, W), dtype=torch.float32, device=dev),
-            torch.empty((H, W, 3), dtype=torch.float32, device=dev), torch.empty((H, W), dtype=torch.uint8, device=dev))
-    gathered = torch.empty((world, H, W, 3), dtype=torch.float32, device=dev) if use_dist else None
+    rows_mode = args.shard == "rows" and world > 1
+    BAND = 32
+    my_bands = kdist.shard_rows_interleaved(H, rank, world, BAND) if rows_mode else [(0, H)]
+    my_rows = sum(b[1] - b[0] for b in my_bands)
+    bufs = (torch.empty((my_rows, W, 3), dtype=torch.float32, device=dev), torch.empty((my_rows, W), dtype=torch.float32, device=dev),
+            torch.empty((my_rows, W, 3), dtype=torch.float32, device=dev), torch.empty((my_rows, W), dtype=torch.uint8, device=dev))
+    # one all_gather per step moves all four finished buffers: 29 B per pixel packed into one byte tensor
+    PIX_BYTES = 12 + 4 + 12 + 1
+    tallest = max(sum(b[1] - b[0] for b in kdist.shard_rows_interleaved(H, r, world, BAND)) for r in range(world)) if rows_mode else H
+    packed = torch.empty((tallest * W * PIX_BYTES,), dtype=torch.uint8, device=dev) if use_dist else None
+    gathered = torch.empty((world * tallest * W * PIX_BYTES,), dtype=torch.uint8, device=dev) if use_dist else None
+
+    def render_mine(view, out):
+        at = 0
+        for r0, r1 in my_bands:
+            sub = tuple(o[at : at + (r1 - r0)] for o in out)
+            surface.render_rows(fs, orbit_view(view, W, H), settings, (1.0, 1.0, 1.0), 1, r0, r1, out=sub, device_out=True)
+            at += r1 - r0
 
     def resident_step(s):
-        surface.render_rows(fs, orbit_view(s * world + rank, W, H), settings, (1.0, 1.0, 1.0), 1, 0, H, out=bufs, device_out=True)
+        render_mine(s if rows_mode else s * world + rank, bufs)
         if use_dist:
-            dist.all_gather_into_tensor(gathered.view(world * H, W, 3), bufs[0], async_op=False)
+            at = 0
+            for b in bufs:
+                nb = b.numel() * b.element_size()
+                packed[at : at + nb].copy_(b.reshape(-1).view(torch.uint8))
+                at += nb
+            dist.all_gather_into_tensor(gathered, packed, async_op=False)
 
     def barrier():
         if use_dist:
@@ -290,13 +479,17 @@ def main():
     fs.dev.set_profiling(False)
 
     # ---- timed region 2: end to end through the NumPy plugin API, host buffers ------------------------
-    pinned = (torch.empty((H, W, 3), dtype=torch.float32).pin_memory(), torch.empty((H, W), dtype=torch.float32).pin_memory(),
-              torch.empty((H, W, 3), dtype=torch.float32).pin_memory(), torch.empty((H, W), dtype=torch.uint8).pin_memory())
+    pinned = (torch.empty((my_rows, W, 3), dtype=torch.float32).pin_memory(), torch.empty((my_rows, W), dtype=torch.float32).pin_memory(),
+              torch.empty((my_rows, W, 3), dtype=torch.float32).pin_memory(), torch.empty((my_rows, W), dtype=torch.uint8).pin_memory())
     host_out = tuple(p.numpy() for p in pinned)
 
     def e2e_step(s):
-        surface.render_rows(fs, orbit_view(s * world + rank, W, H), settings, (1.0, 1.0, 1.0), 1, 0, H, out=host_out)
-        return float(host_out[0][H // 2, W // 2, 0])  # touch the host result
+        at = 0
+        for r0, r1 in my_bands:
+            sub = tuple(o[at : at + (r1 - r0)] for o in host_out)
+            surface.render_rows(fs, orbit_view(s if rows_mode else s * world + rank, W, H), settings, (1.0, 1.0, 1.0), 1, r0, r1, out=sub)
+            at += r1 - r0
+        return float(host_out[0][my_rows // 2, W // 2, 0])  # touch the host result
 
     for s in range(2):
         e2e_step(s)
@@ -313,8 +506,9 @@ def main():
 
     if rank == 0:
         peaks, peak_src = measured_peaks()
-        fps = args.steps * world / (ms / 1e3)
-        e2e_fps = args.steps * world / e2e_s
+        frames_per_step = 1 if rows_mode else world
+        fps = args.steps * frames_per_step / (ms / 1e3)
+        e2e_fps = args.steps * frames_per_step / e2e_s
         ck = clocks.summary()
         ffma_peak = SM_COUNT * FFMA_LANES_PER_SM * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
         tensor_peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0)))
@@ -337,9 +531,9 @@ def main():
             "kernel": "march_mma_kernel<2, filter> (decision filter: Fourier recurrence + fp16x2 split mma.sync.m16n8k16 layers chained in registers + MUFU softplus "
                       "+ sphere-trace crawl step + certified skipping)",
             "bound": "tensor", "achieved": filter_tflops, "peak": tensor_peak, "unit": "TFLOP/s", "frac": (filter_tflops / tensor_peak) if filter_tflops else None,
-            "traffic": 195.3e6,
-            "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of ONE dense filter launch (1.00 ms under ncu, ~12 M evaluations) from "
-                            "profiles/ncu_r1_filter_v3.summary.txt (ncu --set full); weights (50 MB of fp16 fragments) and ray state are L2-resident, DRAM is 2 % busy",
+            "traffic": ncu_traffic("filter"),
+            "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch of the filter kernel, read from the committed ncu --set full capture "
+                            "profiles/ncu_traffic.json (null when that file has no entry for the kernel this build runs); weights and ray state are L2-resident",
             "peak_source": f"{peak_src} MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS, tcgen05 path); mma.sync (HMMA.16816) issue peak measured on this pool: "
                            "553 TFLOP/s (profiles/hmma_split_r1.txt)",
             "algorithmic_flop_per_launch": stats["filter_evals"] * FLOP_PER_SDF_EVAL / max(stats["filter_launches"], 1),
@@ -353,9 +547,10 @@ def main():
         dominant = roof_filter if stats["filter_ms"] >= stats["sdf_mlp_ms"] else roof_exact
         line = {
             "metric": f"fps_{W}x{H}_sphere_traced", "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": dict(workload_config(W, H, world), precision=fs.dev.get_precision(),
-                                                                                     decision_filter="auto (results bit-identical to filter off)"),
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong" if rows_mode else "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload_config(W, H, world, args.shard),
+            "engine": {"precision": fs.dev.get_precision(), "decision_filter": "auto (results bit-identical to filter off)",
+                       "filter_kernel": filter_kernel_name()},
             "mrays_per_s": fps * W * H / 1e6,
             "sdf_evals_per_s": ref_evals * world / (ms / 1e3),
             "sdf_evals_per_ray": ref_evals / max(stats["rays"], 1),
@@ -365,7 +560,7 @@ def main():
                                     "note": "sdf_evals_per_s / per_ray count what the reference evaluates for these frames (exact + filter - undecided + certified)"},
             "hit_fraction": stats["hits"] / max(stats["rays"], 1),
             "clocks": ck,
-            "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": 160 * world,
+            "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": 160 * world * len(my_bands),
                     "d2h_bytes_per_step": int(sum(a.nbytes for a in host_out)) * world,
                     "note": "surface.render_frame-equivalent C-ABI call (KNF_MEM_HOST) into pinned host buffers; the only "
                             "per-step input is the camera/settings structs, the field is uploaded once like the reference loads it once"},
@@ -382,12 +577,21 @@ def main():
                 "launches": int(stats["route_launches"]),
             },
         }
+        if world == 1 and not args.no_extras:
+            line["configs"] = other_configs(fs, field, peaks, ffma_peak, tensor_peak)
         if world == 1 and not args.no_cpu_baseline:
-            w, h = 288, 162
-            rps, sec, _ = oracle_rays_per_second(w, h, args.warmup)
-            line["cpu_baseline"] = {"value": rps / (W * H), "unit": "frames/s", "cores": 1, "kind": "port",
-                                    "sample": f"one {w}x{h} frame of the same camera/field ({sec:.1f} s of oracle time), extrapolated per ray to {W}x{H}",
-                                    "krays_per_s": rps / 1e3, "host_cpus": os.cpu_count(), "numpy": np.__version__}
+            # the reference's own renderer on this box's host cores, one bounded raster at 1 thread and at all cores
+            w, h = 384, 216
+            ncpu = os.cpu_count() or 1
+            dt1, kind, _ = cpu_frame_seconds(w, h, args.warmup, 1)
+            dtn, kind, _ = cpu_frame_seconds(w, h, args.warmup, ncpu)
+            best, cores = (dt1, 1) if dt1 <= dtn else (dtn, ncpu)
+            line["cpu_baseline"] = dict({"value": w * h / best / (W * H), "unit": "frames/s", "cores": cores, "kind": kind,
+                                         "sample": f"one {w}x{h} frame of the same camera/field by "
+                                                   f"{'kilofield.surface.render_frame (unmodified reference, oracle/_ref)' if kind == 'reference' else 'oracle.render (port)'}: "
+                                                   f"{dt1:.1f} s at KNF_THREADS=1, {dtn:.1f} s at KNF_THREADS={ncpu}; scaled per ray to {W}x{H} "
+                                                   "(bench.py --impl reference renders the full frame un-extrapolated)",
+                                         "krays_per_s_1_thread": w * h / dt1 / 1e3, "krays_per_s_all_threads": w * h / dtn / 1e3}, **host_description())
         print(json.dumps(line), flush=True)
     if use_dist:
         dist.destroy_process_group()

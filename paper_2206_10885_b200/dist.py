@@ -52,6 +52,44 @@ def gather_row_bands(local, height: int, group=None):
     return torch.cat(pieces, dim=0)
 
 
+def shard_rows_interleaved(height: int, rank: int, world: int, band: int = 32) -> list[tuple[int, int]]:
+    """Row bands of `band` rows dealt round-robin: band b = rows [b * band, min((b + 1) * band, height)) goes to rank
+    b % world.  Silhouette rows cost several times more than background rows, so contiguous bands leave the
+    ranks that own the image centre with most of the work; interleaving evens it out to within one band."""
+    if not (0 <= rank < world):
+        raise ValueError("rank out of range")
+    if band < 1:
+        raise ValueError("band must be >= 1")
+    n_bands = (height + band - 1) // band
+    return [(b * band, min((b + 1) * band, height)) for b in range(rank, n_bands, world)]
+
+
+def gather_interleaved_bands(local, height: int, band: int = 32, group=None):
+    """All-gather buffers whose rows are the concatenation of this rank's shard_rows_interleaved bands into the full
+    (height, ...) tensor (rows back in image order), on every rank: one all_gather_into_tensor + one index_select."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    per_rank = [shard_rows_interleaved(height, r, world, band) for r in range(world)]
+    rows_of = [sum(b[1] - b[0] for b in bands) for bands in per_rank]
+    if local.shape[0] != rows_of[rank]:
+        raise ValueError("local buffer has the wrong number of rows")
+    tallest = max(rows_of)
+    padded = torch.zeros((tallest,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    padded[: local.shape[0]] = local
+    out = torch.empty((world * tallest,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, padded.contiguous(), group=group)
+    src = np.empty(height, dtype=np.int64)  # image row -> row of `out`
+    for r, bands in enumerate(per_rank):
+        at = r * tallest
+        for r0, r1 in bands:
+            src[r0:r1] = np.arange(at, at + (r1 - r0))
+            at += r1 - r0
+    return out.index_select(0, torch.as_tensor(src, device=local.device))
+
+
 def gather_views(local, group=None):
     """All-gather one finished per-rank buffer (e.g. a colour frame) -> (world, ...) on every rank."""
     import torch
@@ -65,12 +103,15 @@ def gather_views(local, group=None):
 
 
 def render_frame_sharded(surface, pose, settings=None, background=(1.0, 1.0, 1.0), supersample: int = 1, group=None,
-                         render_rows=None):
+                         render_rows=None, interleave: int = 0):
     """One frame split into row bands across the ranks of `group`, assembled on every rank.
 
     Returns (color (H,W,3) f32, depth (H,W) f32, normal (H,W,3) f32, hit (H,W) u8) torch tensors on
     the rank's device.  `render_rows` is injectable so the host logic can be tested without a GPU.
+    interleave = 0: one contiguous band per rank (shard_rows); interleave = b > 0: bands of b rows dealt round-robin
+    (shard_rows_interleaved) -- better balanced when the object covers only part of the image.
     """
+    import torch
     import torch.distributed as dist
 
     from . import surface as S
@@ -81,6 +122,14 @@ def render_frame_sharded(surface, pose, settings=None, background=(1.0, 1.0, 1.0
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     H = int(pose.height)
+    if interleave > 0:
+        mine = shard_rows_interleaved(H, rank, world, interleave)
+        parts = [render_rows(r0, r1) for r0, r1 in mine]
+        if parts:
+            local = tuple(torch.cat([p[i] for p in parts], dim=0) for i in range(len(parts[0])))
+        else:
+            local = tuple(b[:0] for b in render_rows(0, 1))
+        return tuple(gather_interleaved_bands(b, H, interleave, group) for b in local)
     r0, r1 = shard_rows(H, rank, world)
     if r1 > r0:
         bands = render_rows(r0, r1)

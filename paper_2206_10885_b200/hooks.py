@@ -96,3 +96,43 @@ def photometric_loss(field, pose, pixels, target, n_s: int, jitter=None, backgro
     origins, dirs = pixel_rays(pose, pixels)
     colors = volume_forward(field, origins, dirs, n_s, jitter, background)
     return float(np.abs(colors - np.asarray(target, dtype=np.float64)).sum() / len(colors))
+
+
+class ProgressivePathtracer:
+    """The progressive path-trace branch of ``service.RenderService._render_once`` (service.py:289-300) with the
+    accumulator kept on the device: every ``add_sample()`` traces ONE more sample per pixel
+    (``render_pathtraced(scene, pose, spp=1, seed, sample_offset=k)``), adds it to the running fp64 sum in HBM and
+    returns ``to_uint8(clip(sum / k, 0, 1) ** (1 / 2.2))`` -- 3 bytes per pixel cross PCIe per cycle instead of the
+    24-byte fp64 radiance the reference's host-side accumulation would need.  ``hdr()`` downloads the running mean
+    (== ``render_pathtraced(spp=k).hdr`` up to the summation order: the per-pixel counter RNG makes sample k
+    independent of how the samples are batched, pathtrace.py:439-442)."""
+
+    def __init__(self, scene, pose, seed: int = 12345, max_bounces: int = 8):
+        import torch
+
+        from . import pathtrace as P
+
+        self._P, self._torch = P, torch
+        self.scene, self.pose, self.seed, self.max_bounces = scene, pose, int(seed), int(max_bounces)
+        self.device = P._device_index(scene)
+        self.accum = torch.zeros((int(pose.height), int(pose.width), 3), dtype=torch.float64, device=torch.device("cuda", self.device))
+        self.spp = 0
+        self._u8 = torch.empty((int(pose.height), int(pose.width), 3), dtype=torch.uint8, device=self.accum.device)
+        self._host = torch.empty((int(pose.height), int(pose.width), 3), dtype=torch.uint8).pin_memory()
+
+    def add_sample(self, abort_check=None) -> np.ndarray:
+        if abort_check is not None and abort_check():
+            raise RenderAborted("stale path-trace batch")
+        H = int(self.pose.height)
+        hdr = self._P.pathtrace_rows(self.scene, self.pose, 1, self.seed, self.max_bounces, self.spp, 0, H, device_out=True)
+        if abort_check is not None and abort_check():
+            raise RenderAborted("stale path-trace batch")  # service.py:294-295: the batch is dropped, the sum untouched
+        self.accum.add_(hdr)
+        self.spp += 1
+        N.check(N.load().knf_tonemap_u8(N.ptr(self.accum), self.accum.numel(), float(self.spp), 1, N.ptr(self._u8), self.device,
+                                        N.MEM_DEVICE, N.current_stream(self.device)))
+        self._host.copy_(self._u8, non_blocking=False)
+        return self._host.numpy().copy()
+
+    def hdr(self) -> np.ndarray:
+        return (self.accum / max(self.spp, 1)).cpu().numpy()

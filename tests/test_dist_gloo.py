@@ -49,6 +49,20 @@ def _fake_bands(width):
     return render_rows
 
 
+def test_interleaved_bands_tile_the_frame():
+    for h, w, band in [(1080, 8, 32), (1080, 3, 32), (7, 2, 2), (5, 4, 32), (33, 2, 8)]:
+        owned = np.full(h, -1)
+        for r in range(w):
+            for r0, r1 in kd.shard_rows_interleaved(h, r, w, band):
+                assert np.all(owned[r0:r1] == -1) and r1 - r0 <= band
+                owned[r0:r1] = r
+        assert np.all(owned >= 0)
+        rows = [int((owned == r).sum()) for r in range(w)]
+        assert max(rows) - min(rows) <= band  # balanced to within one band
+    with pytest.raises(ValueError):
+        kd.shard_rows_interleaved(10, 0, 2, 0)
+
+
 def _worker(rank, world, port, height, width, out_dir):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -61,8 +75,10 @@ def _worker(rank, world, port, height, width, out_dir):
         pose.height, pose.width = height, width
         color, depth, normal, hit = kd.render_frame_sharded(None, pose, settings=object(), render_rows=_fake_bands(width))
         views = kd.gather_views(torch.full((2, 3), float(rank)))
+        inter = kd.render_frame_sharded(None, pose, settings=object(), render_rows=_fake_bands(width), interleave=2)
         np.savez(os.path.join(out_dir, f"r{rank}.npz"), color=color.numpy(), depth=depth.numpy(), normal=normal.numpy(),
-                 hit=hit.numpy(), views=views.numpy())
+                 hit=hit.numpy(), views=views.numpy(), icolor=inter[0].numpy(), idepth=inter[1].numpy(), inormal=inter[2].numpy(),
+                 ihit=inter[3].numpy())
     finally:
         dist.destroy_process_group()
 
@@ -79,3 +95,6 @@ def test_sharded_frame_equals_single_process(tmp_path, height):
         assert np.array_equal(got["normal"], want[2].numpy())
         assert np.array_equal(got["hit"], want[3].numpy())
         assert np.array_equal(got["views"][:, 0, 0], np.arange(world, dtype=np.float32))
+        # bands of 2 rows dealt round-robin, reassembled in image order
+        assert np.array_equal(got["icolor"], want[0].numpy()) and np.array_equal(got["idepth"], want[1].numpy())
+        assert np.array_equal(got["inormal"], want[2].numpy()) and np.array_equal(got["ihit"], want[3].numpy())
