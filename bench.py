@@ -225,7 +225,7 @@ def run_reference(args, rank, world):
     sample_rps_one = w * h / min(one)
     full = None
     if os.environ.get("BENCH_REF_FULL", "1") != "0":
-        threads_full = ncpu if sample_rps_all >= sample_rps_one else 1
+        threads_full = ncpu if sample_rps_all >= 1.3 * sample_rps_one else 1  # threads barely help the reference (GIL + BLAS oversubscription) and hurt on large bands
         dt, kind, hitf = cpu_frame_seconds(W, H, args.warmup, threads_full)
         full = {"seconds": dt, "threads": threads_full, "hit_fraction": hitf, "fps": 1.0 / dt, "krays_per_s": W * H / dt / 1e3}
     fps = full["fps"] if full else max(sample_rps_all, sample_rps_one) / (W * H)

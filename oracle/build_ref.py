@@ -61,6 +61,7 @@ def import_reference():
     import kilofield  # noqa: F401
     import kilofield.cameras  # noqa: F401
     import kilofield.grid  # noqa: F401
+    import kilofield.modelio  # noqa: F401
     import kilofield.pathtrace  # noqa: F401
     import kilofield.surface  # noqa: F401
 

@@ -12,6 +12,8 @@
 #include "knf_mlp.cuh"
 #include "knf_grad.cuh"
 #include "knf_mma.cuh"
+#define KNF_TC5_LAYOUT_ONLY  // the blob layout, not the kernels (those are compiled in knf_engine.cu)
+#include "knf_tc5.cuh"
 #include "knf_rays.cuh"
 
 using namespace knf;
@@ -189,7 +191,7 @@ static inline void split_fp16x2(float w, uint16_t p[2]) {
 // Inputs are bounded by 1 (sin / cos) and by the box (raw coordinates).
 constexpr double kFp16Safe = 60000.0;  // below the largest finite fp16 (65504) with room for the rounding of a piece
 static double filter_delta(int pieces, const float* w1, const float* b1, const float* w2, const float* b2, const float* w3,
-                           const float* b3, double x_raw) {
+                           const float* b3, double x_raw, bool bias1_in_mma = false) {
   const double e_rep = pieces == 2 ? 3.1 * std::ldexp(1.0, -22) : 0.0;
   const double e = e_rep + 155.0 * std::ldexp(1.0, -24) + std::ldexp(1.0, -18);
   const double sp_rel = 2.0 * std::ldexp(1.0, -22), sp_abs = (double)kFastSoftplusErr;
@@ -198,8 +200,10 @@ static double filter_delta(int pieces, const float* w1, const float* b1, const f
   for (int n = 0; n < kHidden; n++) {
     double s = 0.0;
     for (int k = 0; k < kSdfIn; k++) s += std::fabs((double)w1[n * kSdfIn + k]) * (k < 3 ? x_raw : 1.0);
+    // knf_tc5.cuh feeds b1 through the tensor core as the weight of a constant-1 feature: one more product term
+    const double s_mma = s + (bias1_in_mma ? std::fabs((double)b1[n]) : 0.0);
     H1[n] = softplus(std::fabs((double)b1[n]) + s);
-    eh1[n] = e * s + std::ldexp(1.0, -22) * (std::fabs((double)b1[n]) + s) + sp_abs + sp_rel * H1[n];
+    eh1[n] = e * s_mma + std::ldexp(1.0, -22) * (std::fabs((double)b1[n]) + s) + sp_abs + sp_rel * H1[n];
   }
   for (int n = 0; n < kHidden; n++) {
     double s = 0.0, err = 0.0;
@@ -352,6 +356,55 @@ void pack_sdf_mma(int n_cells, const float* const w[3], const float* const b[3],
   }
 }
 
+// Pack the SDF family into knf_tc5.cuh Tc5Blob: fp16 x 2 weight pieces as K-major no-swizzle tcgen05 B operands (8-row x
+// 16-byte core matrices: [K chunk][row][8 fp16]), rows 0..31 first pieces, rows 32..63 second pieces (x 2^11); layer 1 carries
+// its bias as the weight of the constant-1 feature k = 39.  Then the fp32 constants, the filter bound delta and the Lipschitz
+// bounds (same analysis as pack_sdf_mma<2>: same operand pieces, same number of tensor-core accumulation steps per output).
+void pack_sdf_tc5(int n_cells, const float* const w[3], const float* const b[3], double x_raw, std::vector<uint8_t>& out,
+                  double* delta_max, int* cells_off) {
+  out.assign((size_t)n_cells * Tc5Blob::bytes, 0);
+  for (int c = 0; c < n_cells; c++) {
+    uint8_t* blob = out.data() + (size_t)c * Tc5Blob::bytes;
+    const float* w1 = w[0] + (size_t)c * kHidden * kSdfIn;
+    const float* w2 = w[1] + (size_t)c * kHidden * kHidden;
+    const float* w3 = w[2] + (size_t)c * kSdfOut * kHidden;
+    const float* b1 = b[0] + (size_t)c * kHidden;
+    const float* b2 = b[1] + (size_t)c * kHidden;
+    const float* b3 = b[2] + (size_t)c * kSdfOut;
+    uint16_t* B1 = reinterpret_cast<uint16_t*>(blob + Tc5Blob::off_b1);
+    uint16_t* B2 = reinterpret_cast<uint16_t*>(blob + Tc5Blob::off_b2);
+    for (int n = 0; n < kHidden; n++) {
+      for (int k = 0; k < kTc5K1; k++) {
+        const float v = k < kSdfIn ? w1[n * kSdfIn + k] : (k == kTc5BiasK ? b1[n] : 0.0f);
+        uint16_t p[2];
+        split_fp16x2(v, p);
+        B1[((k / 8) * 64 + n) * 8 + (k % 8)] = p[0];
+        B1[((k / 8) * 64 + 32 + n) * 8 + (k % 8)] = p[1];
+      }
+      for (int k = 0; k < kHidden; k++) {
+        uint16_t p[2];
+        split_fp16x2(w2[n * kHidden + k], p);
+        B2[((k / 8) * 64 + n) * 8 + (k % 8)] = p[0];
+        B2[((k / 8) * 64 + 32 + n) * 8 + (k % 8)] = p[1];
+      }
+    }
+    float* f = reinterpret_cast<float*>(blob + Tc5Blob::off_f32);
+    std::memcpy(f + Tc5Blob::f_b2, b2, kHidden * sizeof(float));
+    std::memcpy(f + Tc5Blob::f_w3d, w3, kHidden * sizeof(float));
+    std::memcpy(f + Tc5Blob::f_b3, b3, kSdfOut * sizeof(float));
+    for (int j = 0; j < kSdfOut; j++)
+      for (int k = 0; k < kHidden; k++) f[Tc5Blob::f_w3t + k * kSdfOutPad + j] = w3[j * kHidden + k];
+    const double delta = filter_delta(2, w1, b1, w2, b2, w3, b3, x_raw, true);
+    const float delta_f = delta < 1e30 ? std::nextafter((float)delta, INFINITY) : INFINITY;
+    f[Tc5Blob::f_delta] = delta_f;
+    if (delta_max && std::isfinite(delta_f)) *delta_max = std::max(*delta_max, (double)delta_f);
+    if (cells_off && !std::isfinite(delta_f)) *cells_off += 1;
+    double lip[3];
+    lipschitz_bound(w1, w2, w3, lip);
+    for (int a = 0; a < 3; a++) f[Tc5Blob::f_lip + a] = std::nextafter((float)lip[a], INFINITY);
+  }
+}
+
 int validate_desc(const KnfFieldDesc* d) {
   if (!d) return fail(KNF_E_INVALID, "null field description");
   if (d->resolution < 1) return fail(KNF_E_INVALID, "resolution must be >= 1");
@@ -420,6 +473,13 @@ int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
     if (F.fp16_ok) {
       KNF_CUDA(cudaMalloc(&F.sdf_mmah_blobs, frags.size() * sizeof(uint32_t)));
       KNF_CUDA(cudaMemcpy(F.sdf_mmah_blobs, frags.data(), frags.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+      std::vector<uint8_t> tc5;
+      double dmax = 0.0;
+      int off = 0;
+      pack_sdf_tc5(F.geom.n_cells, d->sdf_w, d->sdf_b, x_raw, tc5, &dmax, &off);
+      F.filter_delta_max = std::max(F.filter_delta_max, dmax);  // crawl_below must cover whichever filter kernel runs
+      KNF_CUDA(cudaMalloc(&F.sdf_tc5_blobs, tc5.size()));
+      KNF_CUDA(cudaMemcpy(F.sdf_tc5_blobs, tc5.data(), tc5.size(), cudaMemcpyHostToDevice));
     }
   }
   F.precision = KNF_PRECISION_DEFAULT;
@@ -431,13 +491,20 @@ int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
     else return fail(KNF_E_INVALID, "KNF_PRECISION must be fp32_chain, tensor_bf16x3 or tensor_fp16x2");
   }
   if (F.precision == KNF_PRECISION_TENSOR_FP16X2 && (!F.fp16_ok || F.filter_cells_off > 0)) F.precision = KNF_PRECISION_TENSOR_BF16X3;  // bf16 pieces keep fp32's range
-  if (const char* env = std::getenv("KNF_FILTER_SKIP")) F.filter_skip = std::atoi(env) != 0;
+  if (const char* env = std::getenv("KNF_FILTER_SKIP")) F.filter_skip = std::max(0, std::min(2, std::atoi(env)));
   if (const char* env = std::getenv("KNF_SPARSE_SMALL")) F.sparse_small_kernel = std::atoi(env) != 0;
   if (const char* env = std::getenv("KNF_FILTER_KEEP")) F.filter_keep_div = std::max(1, std::atoi(env));
   if (const char* env = std::getenv("KNF_FILTER_INNER")) F.filter_max_inner = std::max(1, std::atoi(env));
   if (const char* env = std::getenv("KNF_SPARSE_DIV")) F.sparse_div = std::max(1, std::atoi(env));
   if (const char* env = std::getenv("KNF_SPARSE_INNER")) F.sparse_max_inner = std::max(1, std::atoi(env));
   if (const char* env = std::getenv("KNF_SPARSE_KEEP")) F.sparse_keep_div = std::max(1, std::atoi(env));
+  if (const char* env = std::getenv("KNF_OVERLAP")) F.overlap_queues = std::atoi(env) != 0;
+  if (const char* env = std::getenv("KNF_FILTER_KERNEL")) {
+    const std::string v(env);
+    if (v == "tc5" || v == "1") F.filter_kernel = 1;
+    else if (v == "mma" || v == "0") F.filter_kernel = 0;
+    else return fail(KNF_E_INVALID, "KNF_FILTER_KERNEL must be tc5 or mma");
+  }
   if (const char* env = std::getenv("KNF_FILTER")) {
     const std::string v(env);
     if (v == "off" || v == "0") F.filter_mode = KNF_FILTER_OFF;
@@ -709,6 +776,12 @@ int knf_field_destroy(knf_field_t f) {
     std::lock_guard<std::mutex> lk(f->f.mu);
     if (f->f.last_call_valid) cudaEventSynchronize(f->f.last_call_done);  // asynchronous (KNF_MEM_DEVICE) calls may still be using the workspace
     if (f->f.last_call_done) cudaEventDestroy(f->f.last_call_done);
+    if (f->f.side_stream) {
+      cudaStreamSynchronize(f->f.side_stream);
+      cudaStreamDestroy(f->f.side_stream);
+      cudaEventDestroy(f->f.ev_fork);
+      cudaEventDestroy(f->f.ev_join);
+    }
     f->f.ws.release_all();
     for (cudaEvent_t e : f->f.events) cudaEventDestroy(e);
     if (f->f.host_poll) cudaFreeHost(f->f.host_poll);
@@ -716,6 +789,7 @@ int knf_field_destroy(knf_field_t f) {
     if (f->f.col_blobs) cudaFree(f->f.col_blobs);
     if (f->f.sdf_mma_blobs) cudaFree(f->f.sdf_mma_blobs);
     if (f->f.sdf_mmah_blobs) cudaFree(f->f.sdf_mmah_blobs);
+    if (f->f.sdf_tc5_blobs) cudaFree(f->f.sdf_tc5_blobs);
   }
   delete f;
   if (prev_device >= 0) cudaSetDevice(prev_device);

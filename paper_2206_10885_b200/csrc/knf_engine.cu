@@ -11,6 +11,7 @@
 #include "knf_mlp.cuh"
 #include "knf_mma.cuh"
 #include "knf_rays.cuh"
+#include "knf_tc5.cuh"
 
 namespace knf {
 
@@ -50,7 +51,7 @@ void DevBuf::release() {
 }
 
 void Workspace::release_all() {
-  DevBuf* all[] = {&req_pt2, &req_cell2, &req_rank2, &req_pt3, &req_cell3, &req_rank3, &cell_count_f, &sorted, &live2, &live3, &tile_base, &req_pt1, &req_cell1, &req_rank1, &req_pt, &req_cell, &req_rank, &perm, &tiles, &cell_count, &cell_offset, &counters, &t, &t_prev,
+  DevBuf* all[] = {&sorted_f, &tiles_f, &cell_offset_f, &tile_base_f, &req_pt2, &req_cell2, &req_rank2, &req_pt3, &req_cell3, &req_rank3, &cell_count_f, &sorted, &live2, &live3, &tile_base, &req_pt1, &req_cell1, &req_rank1, &req_pt, &req_cell, &req_rank, &perm, &tiles, &cell_count, &cell_offset, &counters, &t, &t_prev,
                    &d_prev, &t_conv, &d_conv, &t_hit, &steps, &phase, &hit, &live0, &live1, &hit_list,
                    &hit_count, &sdf_out, &col_v, &col_n, &col_z, &rgb, &origins, &dirs, &t_near, &t_far, &normals64,
                    &colors64, &frame_color, &frame_depth, &frame_normal, &frame_hit};
@@ -120,6 +121,10 @@ int ensure_rays(Field& F, size_t n) {
   KNF_TRY(W.req_cell3.ensure(n * sizeof(int)));
   KNF_TRY(W.req_rank3.ensure(n * sizeof(int)));
   KNF_TRY(W.sorted.ensure(n * sizeof(float4)));
+  KNF_TRY(W.sorted_f.ensure(n * sizeof(float4)));
+  KNF_TRY(W.tiles_f.ensure((n / 32 + (size_t)F.geom.n_cells + 2) * sizeof(Tile)));  // filter tiles hold >= 32 requests except one per cell
+  KNF_TRY(W.cell_offset_f.ensure(((size_t)F.geom.n_cells + 1) * sizeof(int)));
+  KNF_TRY(W.tile_base_f.ensure(((size_t)F.geom.n_cells + 1) * sizeof(int)));
   KNF_TRY(W.live2.ensure(n * 4));
   KNF_TRY(W.live3.ensure(n * 4));
   {
@@ -148,10 +153,10 @@ RouteBuffers route_buffers(Field& F, int slot, int next_slot, int list) {
   R.req_cell = cells[list]->as<int>();
   R.req_rank = ranks[list]->as<int>();
   R.cell_count = (list >= 2 ? W.cell_count_f : W.cell_count).as<int>();
-  R.cell_offset = W.cell_offset.as<int>();
-  R.tile_base = W.tile_base.as<int>();
+  R.cell_offset = (list >= 2 ? W.cell_offset_f : W.cell_offset).as<int>();
+  R.tile_base = (list >= 2 ? W.tile_base_f : W.tile_base).as<int>();
   R.perm = W.perm.as<int>();
-  R.tiles = W.tiles.as<Tile>();
+  R.tiles = (list >= 2 ? W.tiles_f : W.tiles).as<Tile>();
   R.ctr = counters(F, slot);
   R.next_ctr = next_slot >= 0 ? counters(F, next_slot) : nullptr;
   R.eval_counter = nullptr;
@@ -214,7 +219,14 @@ int begin_call(Field& F, cudaStream_t st) {
     KNF_CUDA(cudaFuncSetAttribute(march_mma_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaMarchSmemT<2>)));
     KNF_CUDA(cudaFuncSetAttribute(march_mma_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaMarchSmemT<2>)));
     KNF_CUDA(cudaFuncSetAttribute(sdf_mma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<2>)));
+    KNF_CUDA(cudaFuncSetAttribute(march_tc5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Tc5MarchSmem)));
+    KNF_CUDA(cudaFuncSetAttribute(march_tc5_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));  // several 40 KB CTAs per SM
     if (!F.host_poll) KNF_CUDA(cudaMallocHost(&F.host_poll, 64));
+    if (!F.side_stream) {
+      KNF_CUDA(cudaStreamCreateWithFlags(&F.side_stream, cudaStreamNonBlocking));
+      KNF_CUDA(cudaEventCreateWithFlags(&F.ev_fork, cudaEventDisableTiming));
+      KNF_CUDA(cudaEventCreateWithFlags(&F.ev_join, cudaEventDisableTiming));
+    }
     F.smem_configured = true;
   }
   return 0;
@@ -418,13 +430,15 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
   bool filter_drained = false;  // the filter queue was seen empty after the filter had been switched off
   bool exact_sparse = false;    // last poll: the exact queue holds < 1/16 of the rays -> small-tile-only kernel
   const double crawl_on = -(s.eps_hit + 2.0 * F.filter_delta_max);
-  // Global wavefronts.  Every ray queued in a wavefront either advances a step or (once each) fetches its secant /
-  // re-check sample, so max_steps + 3 bounds the count; tile residency usually finishes in far fewer, which the
-  // host learns by polling the request counts.
+  // Global wavefronts.  Every ray queued in a wavefront either advances a step, fetches (once each) its secant / re-check
+  // sample, or -- a filter-queue ray whose sample the filter cannot decide -- moves to the next exact queue unchanged and
+  // advances there, so 2 * max_steps + 6 bounds the count; tile residency usually finishes in far fewer, which the host
+  // learns by polling the request counts.
   F.prof_chain = true;  // spans inside the loop are back to back on `st`: one shared event between neighbours
   F.prof_last_end = (size_t)-1;
   size_t live_upper = (size_t)n;  // upper bound on the size of any queue from here on: sizes the routing and tile grids
-  for (int w = 0; w <= s.max_steps + 2; w++) {
+  const int max_wavefronts = 2 * s.max_steps + 6;
+  for (int w = 0; w < max_wavefronts; w++) {
     const int cur = w & 1, nxt = cur ^ 1;
     const bool filter_pass = exact_mode && F.fp16_ok && F.filter_mode != 0 && !filter_drained && w > 0;
     MarchTileArgs A{};
@@ -437,15 +451,36 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     A.eval_counter = stat_counter(F, 0);
     A.max_inner = (probing && w == 0) ? 1 : F.march_max_inner;
     A.crawl_below = use_filter ? crawl_on : -INFINITY;
-    A.max_skip = F.filter_skip ? 1 : 0;
+    A.max_skip = F.filter_skip;
     A.inv_resolution = 1.0 / (double)F.geom.resolution;
     A.filter_x_raw = F.filter_x_raw;
+    for (int a = 0; a < 3; a++) A.cell_scale[a] = (double)F.geom.resolution / (F.geom.hi[a] - F.geom.lo[a]);
+    // Both queues of this wavefront were filled by the previous wavefront's kernels and hold different rays, so their tile
+    // kernels are independent: route both, then run the filter kernel on the caller's stream and the exact kernel beside
+    // it on the side stream (the exact launches of a frame are sparse and latency-bound; alone on the GPU they cost 2.6 ms
+    // per 1080p frame).  Samples the filter cannot decide join the exact queue of the NEXT wavefront.
+    const bool tc5 = F.filter_kernel == 1 && F.sdf_tc5_blobs != nullptr;
+    RouteBuffers Rf = route_buffers(F, 4 + cur, 4 + nxt, 2 + cur);
     if (filter_pass) {
-      // filter queue of this wavefront: tensor-core predicate; undecided samples join the exact queue below
-      RouteBuffers Rf = route_buffers(F, 4 + cur, 4 + nxt, 2 + cur);
-      Rf.sorted = W.sorted.as<float4>();
+      Rf.sorted = W.sorted_f.as<float4>();
       Rf.live = M.live[2 + cur];
+      Rf.small_tiles = tc5 ? 3 : 0;  // tcgen05 filter: tiles of <= 128 requests (one per thread of a 128-thread CTA)
       KNF_TRY(launch_scan_scatter(F, Rf, live_upper, st));
+    }
+    RouteBuffers R = route_buffers(F, cur, nxt, cur);
+    R.eval_counter = stat_counter(F, 3);  // requests that went through global routing
+    R.sorted = W.sorted.as<float4>();
+    R.live = M.live[cur];
+    const bool small_only = exact_mode && exact_sparse && F.sparse_small_kernel;
+    R.small_tiles = small_only ? 2 : 0;  // dense wavefronts: 64-request tiles for march_warp_kernel; sparse: <= 16 for march_small_kernel
+    KNF_TRY(launch_scan_scatter(F, R, live_upper, st));
+    cudaStream_t st_exact = st;
+    if (filter_pass && F.overlap_queues && F.side_stream) {
+      KNF_CUDA(cudaEventRecord(F.ev_fork, st));
+      KNF_CUDA(cudaStreamWaitEvent(F.side_stream, F.ev_fork, 0));
+      st_exact = F.side_stream;
+    }
+    if (filter_pass) {
       MarchTileArgs Af = A;
       Af.P.blobs = reinterpret_cast<const float*>(F.sdf_mmah_blobs);
       Af.P.perm = Rf.perm;
@@ -456,21 +491,21 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
       Af.live_in = M.live[2 + cur];
       Af.max_inner = F.filter_max_inner;
       Af.keep_div = F.filter_keep_div;
-      Af.defer = route_buffers(F, cur, -1, cur);
-      Af.live_defer = M.live[cur];
+      Af.defer = A.next;  // undecided samples: the exact queue of the next wavefront
+      Af.live_defer = A.live_out;
       {
         ProfScope prof(F, st, SPAN_FILTER);
-        march_mma_kernel<2, true><<<mlp_grid(F, live_upper, march_ctas_per_sm<2>()), 32, sizeof(MmaMarchSmemT<2>), st>>>(Af);
+        if (tc5) {
+          Af.P.blobs = reinterpret_cast<const float*>(F.sdf_tc5_blobs);
+          const size_t tiles_upper = live_upper / 64 + std::min<size_t>(live_upper, (size_t)F.geom.n_cells) + 1;
+          const int grid = (int)std::max<size_t>(1, std::min<size_t>(tiles_upper, (size_t)148 * kTc5CtasPerSm));
+          march_tc5_kernel<<<grid, kTc5Tile, sizeof(Tc5MarchSmem), st>>>(Af);
+        } else {
+          march_mma_kernel<2, true><<<mlp_grid(F, live_upper, march_ctas_per_sm<2>()), 32, sizeof(MmaMarchSmemT<2>), st>>>(Af);
+        }
       }
       F.stats.kernel_launches += 1;
     }
-    RouteBuffers R = route_buffers(F, cur, nxt, cur);
-    R.eval_counter = stat_counter(F, 3);  // requests that went through global routing
-    R.sorted = W.sorted.as<float4>();
-    R.live = M.live[cur];
-    const bool small_only = exact_mode && exact_sparse && F.sparse_small_kernel;
-    R.small_tiles = small_only ? 2 : 0;  // dense wavefronts: 64-request tiles for march_warp_kernel; sparse: <= 16 for march_small_kernel
-    KNF_TRY(launch_scan_scatter(F, R, live_upper, st));
     A.P.blobs = F.sdf_blobs;
     A.P.perm = R.perm;
     A.P.tiles = R.tiles;
@@ -479,27 +514,31 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     A.P.sorted = R.sorted;
     A.live_in = M.live[cur];
     {
-      ProfScope prof(F, st, SPAN_SDF_MLP);
+      ProfScope prof(F, st_exact, SPAN_SDF_MLP);
       if (F.precision == KNF_PRECISION_TENSOR_BF16X3) {
         A.P.blobs = reinterpret_cast<const float*>(F.sdf_mma_blobs);
-        march_mma_kernel<3, false><<<mlp_grid(F, live_upper, march_ctas_per_sm<3>()), 32, sizeof(MmaMarchSmemT<3>), st>>>(A);
+        march_mma_kernel<3, false><<<mlp_grid(F, live_upper, march_ctas_per_sm<3>()), 32, sizeof(MmaMarchSmemT<3>), st_exact>>>(A);
       } else if (F.precision == KNF_PRECISION_TENSOR_FP16X2) {
         A.P.blobs = reinterpret_cast<const float*>(F.sdf_mmah_blobs);
-        march_mma_kernel<2, false><<<mlp_grid(F, live_upper, march_ctas_per_sm<2>()), 32, sizeof(MmaMarchSmemT<2>), st>>>(A);
+        march_mma_kernel<2, false><<<mlp_grid(F, live_upper, march_ctas_per_sm<2>()), 32, sizeof(MmaMarchSmemT<2>), st_exact>>>(A);
       } else if (small_only) {
         // sparse wavefront: few tiles, the GPU is far from full -- a ray that stays in its cell keeps stepping there
         // rather than paying another routing round trip (the long tail of a frame is a chain of such round trips)
         A.max_inner = F.sparse_max_inner;
         A.keep_div = F.sparse_keep_div;
-        march_small_kernel<<<mlp_grid(F, live_upper, kSmallCtasPerSm), 32, sizeof(SdfSmallSmem), st>>>(A);
+        march_small_kernel<<<mlp_grid(F, live_upper, kSmallCtasPerSm), 32, sizeof(SdfSmallSmem), st_exact>>>(A);
       } else {
-        march_warp_kernel<<<mlp_grid(F, live_upper), 32, sizeof(SdfKernelSmem), st>>>(A);
+        march_warp_kernel<<<mlp_grid(F, live_upper), 32, sizeof(SdfKernelSmem), st_exact>>>(A);
       }
+    }
+    if (st_exact != st) {
+      KNF_CUDA(cudaEventRecord(F.ev_join, st_exact));
+      KNF_CUDA(cudaStreamWaitEvent(st, F.ev_join, 0));
     }
     F.stats.kernel_launches += 1;
     F.stats.wavefronts += 1;
     const bool poll = (w == 0 && probing) || (w == 1) || (w == 3) || (w % 8 == 7);
-    if (poll && w < s.max_steps + 2) {
+    if (poll && w + 1 < max_wavefronts) {
       // n_requests of the next exact queue and of the next filter queue
       KNF_CUDA(cudaMemcpyAsync(F.host_poll, &counters(F, nxt)->n_requests, sizeof(int), cudaMemcpyDeviceToHost, st));
       KNF_CUDA(cudaMemcpyAsync(F.host_poll + 1, &counters(F, 4 + nxt)->n_requests, sizeof(int), cudaMemcpyDeviceToHost, st));

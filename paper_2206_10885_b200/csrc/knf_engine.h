@@ -42,6 +42,8 @@ struct Workspace {
   DevBuf req_pt2, req_cell2, req_rank2, req_pt3, req_cell3, req_rank3;  // the decision filter's two request lists
   DevBuf sorted;                         // march queues: (point, ray) per sorted position
   DevBuf cell_count_f;                   // per-cell request counts of the filter queue
+  DevBuf sorted_f, tiles_f, cell_offset_f, tile_base_f;  // the filter queue's own sorted view and tile list: its tile kernel runs
+                                         // concurrently with the exact queue's (two streams), so the two cannot share them
   DevBuf live2, live3;
   DevBuf cell_count, cell_offset, tile_base;
   DevBuf counters;  // RouteCounters[4] + stats counters
@@ -67,6 +69,8 @@ struct Field {
   float* col_blobs = nullptr;
   uint32_t* sdf_mma_blobs = nullptr;   // knf_mma.cuh MmaBlobT<3> per cell (bf16 x 3 B fragments)
   uint32_t* sdf_mmah_blobs = nullptr;  // MmaBlobT<2> per cell (fp16 x 2 B fragments); null when a weight exceeds the fp16 range
+  uint8_t* sdf_tc5_blobs = nullptr;    // knf_tc5.cuh Tc5Blob per cell (fp16 x 2 pieces as tcgen05 B operands); null when !fp16_ok
+  int filter_kernel = 1;               // decision filter kernel: 1 = march_tc5_kernel (tcgen05 / TMEM), 0 = march_mma_kernel<2, true> (mma.sync); KNF_FILTER_KERNEL
   bool fp16_ok = false;
   double filter_delta_max = 0.0;       // largest FINITE per-cell decision-filter bound (knf_api.cu filter_delta)
   float filter_x_raw = 0.0f;           // coordinate magnitude the bounds were derived for (1.001 x the box's largest |coordinate|)
@@ -75,7 +79,7 @@ struct Field {
   int sparse_keep_div = 2;   // measured: (16, 4) gains 3 % on the distilled frame and loses 1.3 % on the random-init one; (32, 8) and up lose more
   int sparse_div = 8;                  // a wavefront is sparse when its exact queue holds < n / sparse_div rays (KNF_SPARSE_DIV)
   bool sparse_small_kernel = true;     // exact march: sparse wavefronts by march_small_kernel (KNF_SPARSE_SMALL=0 disables)
-  bool filter_skip = true;             // certified (Lipschitz) skipping inside the filter; KNF_FILTER_SKIP=0 disables
+  int filter_skip = 1;                 // certified (Lipschitz) skipping inside the filter: 0 off, 1 sample by sample, 2 closed-form run (cell-exit DDA + Lipschitz budget) then sample by sample; KNF_FILTER_SKIP
   int filter_hint = 0;                 // auto mode: what the previous march on this handle learnt (0 unknown, 1 rays crawl, 2 they do not)
   int filter_mode = 2;                 // decision filter of the exact march: 0 off, 1 on, 2 auto (probe the first wavefront)
   int precision = 0;                  // KNF_PRECISION_*: which SDF tile kernels run
@@ -96,6 +100,9 @@ struct Field {
   void* prof_last_stream = nullptr;
   bool prof_chain = false;            // set by the march loop
   int* host_poll = nullptr;  // pinned; early-out polling of the march loop
+  cudaStream_t side_stream = nullptr;    // the exact queue's tile kernels run here, beside the filter kernel on the caller's stream
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool overlap_queues = true;            // KNF_OVERLAP=0: one stream, filter then exact (the round-1 schedule)
   cudaEvent_t last_call_done = nullptr;  // recorded at the end of every call (CallScope)
   void* last_call_stream = nullptr;
   bool last_call_valid = false;

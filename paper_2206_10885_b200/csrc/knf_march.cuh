@@ -36,6 +36,7 @@ struct MarchTileArgs {
   int keep_div;             // a tile keeps stepping in place while n_stay * keep_div >= its size (2 = half; 0 is read as 2)
   double inv_resolution;    // 1 / grid resolution (host-computed)
   double crawl_below;       // exact kernels: a march step from a distance below this continues in the filter queue (-inf: never)
+  double cell_scale[3];     // resolution / (hi - lo) per axis (host-computed): cell_of_quick's estimate
   float filter_x_raw;       // filter kernel: the coordinate magnitude the per-cell bounds delta were derived for (knf_api.cu filter_delta);
                             // a sample with a larger |coordinate| (outside the box: caller-supplied t ranges) is left to the exact kernel
 };
@@ -147,7 +148,10 @@ __device__ __forceinline__ void march_exact_tile(const MarchTileArgs& A, SmemT& 
           pz[q] = __double2float_rn(rr[q].o[2] + t_next * rr[q].d[2]);
           const bool well_inside = px[q] > in_lo[0] && px[q] < in_hi[0] && py[q] > in_lo[1] && py[q] < in_hi[1] &&
                                    pz[q] > in_lo[2] && pz[q] < in_hi[2];
-          cell[q] = well_inside ? tile.cell : cell_of_slow(px[q], py[q], pz[q], A.G.lo[0], A.G.lo[1], A.G.lo[2], A.G.hi[0], A.G.hi[1], A.G.hi[2], A.G.resolution);
+          cell[q] = well_inside ? tile.cell : cell_of_quick(px[q], py[q], pz[q], A.G.lo, A.G.hi, A.cell_scale, A.G.resolution);
+          // a sample outside the box is not the filter's to decide (its bound was derived for coordinates inside it): keep
+          // the ray in the exact queue instead of bouncing it through the filter queue
+          if (code[q] == STEP_FILTER && !(fmaxf(fmaxf(fabsf(px[q]), fabsf(py[q])), fabsf(pz[q])) <= A.filter_x_raw)) code[q] = STEP_EXACT;
         }
       }
       stay[q] = code[q] == STEP_EXACT && cell[q] == tile.cell;
@@ -378,7 +382,7 @@ static __global__ void __maxnreg__(KNF_MARCH_MMA_MAXNREG) march_mma_kernel(March
               pz[q] = __double2float_rn(S.od[2][32 * q + lane] + t_next * S.od[5][32 * q + lane]);
               const bool well_inside = px[q] > in_lo[0] && px[q] < in_hi[0] && py[q] > in_lo[1] && py[q] < in_hi[1] &&
                                        pz[q] > in_lo[2] && pz[q] < in_hi[2];
-              cell[q] = well_inside ? tile.cell : cell_of_slow(px[q], py[q], pz[q], A.G.lo[0], A.G.lo[1], A.G.lo[2], A.G.hi[0], A.G.hi[1], A.G.hi[2], A.G.resolution);
+              cell[q] = well_inside ? tile.cell : cell_of_quick(px[q], py[q], pz[q], A.G.lo, A.G.hi, A.cell_scale, A.G.resolution);
               if (!FILTER || !well_inside) break;
               // (+ 1e-6 per axis: the fp32 roundings of the two points; the 0.99999 on `room` covers the fp32 arithmetic here)
               const float rise = lip[0] * (fabsf(px[q] - x0) + 1e-6f) + lip[1] * (fabsf(py[q] - y0) + 1e-6f) + lip[2] * (fabsf(pz[q] - z0) + 1e-6f);

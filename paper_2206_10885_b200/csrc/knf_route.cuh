@@ -33,13 +33,16 @@ struct RouteBuffers {
   unsigned long long* eval_counter;  // += n_requests per pass (nullable); statistics only
   float4* sorted;     // march queues: sorted position -> (point, ray id in .w): one coalesced load per tile point (nullable)
   const int* live;    // march queues: request slot -> ray id (read by scatter when `sorted` is set)
-  int small_tiles;    // 1: cut the last < 49 requests of a cell into tiles of <= 16 (kernels with a small-tile path); 2: every tile <= 16
+  int small_tiles;    // 1: cut the last < 49 requests of a cell into tiles of <= 16 (kernels with a small-tile path); 2: every tile <= 16;
+                      // 3: tiles of <= 128 requests, a cell's requests split evenly (knf_tc5.cuh: one request per thread of a 128-thread CTA)
 };
 
 // How a cell's k requests are cut into tiles: full 64-request tiles, then the remainder r either as one tile
 // (r >= 49, or small tiles off) or as ceil(r / 16) tiles of <= 16 requests.
 constexpr int kSmallTile = 16, kSmallTileMaxRemainder = 48;
+constexpr int kBigTile = 128;
 __device__ __forceinline__ int tiles_of_cell(int k, int small_tiles) {
+  if (small_tiles == 3) return (k + kBigTile - 1) / kBigTile;
   if (small_tiles == 2) return (k + kSmallTile - 1) / kSmallTile;
   const int full = k / kTilePts, r = k - full * kTilePts;
   if (r == 0) return full;
@@ -225,7 +228,13 @@ static __global__ void route_scatter_kernel(RouteBuffers R, int n_cells) {
     const int c = lo, j = ti - R.tile_base[c];
     const int start = R.cell_offset[c], k = R.cell_offset[c + 1] - start;
     int off, take;
-    if (R.small_tiles == 2) {
+    if (R.small_tiles == 3) {
+      // n = ceil(k / 128) tiles of an even share rounded up to whole warps (so only the last tile holds a partly filled
+      // warp): per <= 128, and (n - 1) * per < k, so the last tile is never empty
+      const int n = (k + kBigTile - 1) / kBigTile, per = ((k + n - 1) / n + 31) & ~31;
+      off = j * per;
+      take = min(per, k - off);
+    } else if (R.small_tiles == 2) {
       off = j * kSmallTile;
       take = min(kSmallTile, k - off);
     } else {

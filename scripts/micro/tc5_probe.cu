@@ -292,8 +292,74 @@ static void run(const char* name, int mode, std::vector<float>& a, std::vector<f
   cudaFree(dA); cudaFree(dB); cudaFree(dD); cudaFree(dC);
 }
 
+
+// Alignment probe: one product of 1.0 plus fifteen equal tiny products p = 1.5 * 2^-q in one K = 16 MMA.  What the fp32
+// result keeps of the tiny addends shows where the tensor core truncates addends relative to the largest exponent.
+static void alignment_probe() {
+  std::vector<float> a(128 * 16), b(32 * 16);
+  for (int r = 0; r < 128; r++) {
+    const int q = 14 + (r % 32);          // p = 1.5 * 2^-q, q = 14 .. 45
+    const int qa = q / 2, qb = q - qa;    // a = 1.5 * 2^-qa, b = 2^-qb (both normal fp16 for q <= 28; beyond: via subnormals / zero)
+    a[r * 16] = 1.0f;
+    for (int k = 1; k < 16; k++) a[r * 16 + k] = (r / 32 == 1 ? -1.0f : 1.0f) * ldexpf(1.5f, -std::min(qa, 14));
+    (void)qb;
+  }
+  // B differs per column group: column n uses b = 2^-(q - qa) for the row's q -- but B is shared by all rows, so instead fix
+  // b = 2^-14 (columns 0..7), 2^-10 (8..15), 2^-6 (16..23), 2^-2 (24..31) and let the row choose a's exponent.
+  for (int n = 0; n < 32; n++) {
+    b[n * 16] = 1.0f;
+    for (int k = 1; k < 16; k++) b[n * 16 + k] = ldexpf(1.0f, -(14 - 4 * (n / 8)));
+  }
+  for (int r = 0; r < 128; r++) {
+    const int ea = (r % 32) / 2;  // a = (1.5 or 1.0) * 2^-ea, ea = 0 .. 15 (fp16 normal down to 2^-14, 2^-15 subnormal but exact)
+    const float mant = (r % 2) ? 1.5f : 1.0f;
+    for (int k = 1; k < 16; k++) a[r * 16 + k] = (r / 32 == 1 ? -1.0f : 1.0f) * ldexpf(mant, -ea);
+    if (r / 32 >= 2) a[r * 16] = (r / 32 == 2) ? 0.0f : 1024.0f;  // no large addend / a larger one
+  }
+  std::vector<uint32_t> ha(128 * 8), hb(32 * 8);
+  auto packh = [](const std::vector<float>& src, std::vector<uint32_t>& dst, int rows) {
+    for (int r = 0; r < rows; r++)
+      for (int k = 0; k < 16; k += 2) {
+        __half h0 = __float2half_rn(src[r * 16 + k]), h1 = __float2half_rn(src[r * 16 + k + 1]);
+        uint16_t u0, u1;
+        memcpy(&u0, &h0, 2); memcpy(&u1, &h1, 2);
+        dst[r * 8 + k / 2] = u0 | ((uint32_t)u1 << 16);
+      }
+  };
+  packh(a, ha, 128);
+  packh(b, hb, 32);
+  uint32_t *dA, *dB; float* dD;
+  CK(cudaMalloc(&dA, ha.size() * 4)); CK(cudaMalloc(&dB, hb.size() * 4)); CK(cudaMalloc(&dD, 128 * 32 * 4));
+  CK(cudaMemcpy(dA, ha.data(), ha.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dB, hb.data(), hb.size() * 4, cudaMemcpyHostToDevice));
+  mma_probe<false, 16><<<1, 128>>>(dA, dB, dD, 0, 1, nullptr);
+  CK(cudaDeviceSynchronize());
+  std::vector<float> d(128 * 32);
+  CK(cudaMemcpy(d.data(), dD, d.size() * 4, cudaMemcpyDeviceToHost));
+  printf("alignment probe (K = 16, one MMA): big addend B0, fifteen addends p each; shown: log2(p / B0), exact (sum - B0) / ulp(B0), measured\n");
+  double worst_rel = 0;
+  for (int grp = 0; grp < 4; grp++) {
+    const double big = grp == 2 ? 0.0 : (grp == 3 ? 1024.0 : 1.0);
+    for (int r = grp * 32; r < grp * 32 + 32; r++)
+      for (int n = 0; n < 32; n += 8) {
+        const double p = (double)a[r * 16 + 1] * (double)b[n * 16 + 1];
+        const double exact = big + 15.0 * p;
+        const double ulp = big > 0 ? ldexp(1.0, (int)floor(log2(big)) - 23) : 0.0;
+        const double meas = d[r * 32 + n];
+        const double err = fabs(meas - exact);
+        const double mag = fabs(big) + 15.0 * fabs(p);
+        worst_rel = fmax(worst_rel, err / mag);
+        if (big > 0 && fabs(p) / big < ldexp(1.0, -17) && fabs(p) / big > ldexp(1.0, -30) && (r % 2 == 1))
+          printf("  grp %d log2(|p|/B0) = %6.2f  exact %+9.3f ulp  measured %+9.3f ulp\n", grp, log2(fabs(p) / big), (exact - big) / ulp, (meas - big) / ulp);
+      }
+  }
+  printf("alignment probe: worst |err| / sum|xw| over all patterns = 2^%.2f\n", log2(worst_rel));
+  cudaFree(dA); cudaFree(dB); cudaFree(dD);
+}
+
 int main() {
   srand(1);
+  alignment_probe();
   auto rnd = [] { return (float)rand() / RAND_MAX * 2.0f - 1.0f; };
   {
     std::vector<float> a(128 * 48), b(32 * 48);
