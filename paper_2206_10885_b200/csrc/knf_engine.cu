@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 
 #include "knf_march.cuh"
@@ -72,7 +73,7 @@ static inline int blocks_for(size_t n, int threads = 256) {
   } while (0)
 
 constexpr int kRouteSlots = 6;    // 0/1 exact march queue (ping-pong), 2 SDF forward, 3 colour forward, 4/5 filter march queue
-constexpr int kStatCounters = 8;  // see finish_stats
+constexpr int kStatCounters = 32;  // see finish_stats; [16..25]: optional section cycles of march_tc5_kernel (-DKNF_TC5_TIMING)
 constexpr size_t kCounterBytes = kRouteSlots * sizeof(RouteCounters) + kStatCounters * sizeof(unsigned long long);
 
 int ensure_requests(Field& F, size_t n) {
@@ -292,6 +293,17 @@ int finish_stats(Field& F, cudaStream_t st) {
   F.stats.filter_deferred = (int64_t)host[5];
   F.stats.filter_skipped = (int64_t)host[6];
   F.stats.filter_lane_slots = (int64_t)host[7];
+#ifdef KNF_TC5_TIMING
+  {
+    static const char* names[10] = {"tile setup", "encode+split+store", "barriers", "layer-1 MMA wait", "h1 epilogue", "layer-2 MMA wait", "h2 epilogue+output",
+                                    "march step+skip", "emit", "loop top"};
+    double tot = 0;
+    for (int i = 0; i < 10; i++) tot += (double)host[16 + i];
+    fprintf(stderr, "march_tc5_kernel warp-cycles by section (total %.3g):", tot);
+    for (int i = 0; i < 10; i++) fprintf(stderr, " %s %.1f%% |", names[i], 100.0 * (double)host[16 + i] / (tot > 0 ? tot : 1));
+    fprintf(stderr, "\n");
+  }
+#endif
   return 0;
 }
 
@@ -300,6 +312,16 @@ int launch_scan_scatter(Field& F, const RouteBuffers& R, size_t n_upper, cudaStr
   ProfScope prof(F, st, SPAN_ROUTE);
   route_scan_kernel<<<1, kScanThreads, 0, st>>>(R, F.geom.n_cells, seg_cell, seg_start, n_seg);
   route_scatter_kernel<<<blocks_for(std::max<size_t>(n_upper, (size_t)F.geom.n_cells)), 256, 0, st>>>(R, F.geom.n_cells);
+  F.stats.kernel_launches += 2;
+  KNF_CUDA(cudaGetLastError());
+  return 0;
+}
+
+// scan + scatter of the two queues of one march wavefront in two launches instead of four
+static int launch_scan_scatter2(Field& F, const RouteBuffers& Ra, const RouteBuffers& Rb, size_t n_upper, cudaStream_t st) {
+  ProfScope prof(F, st, SPAN_ROUTE);
+  route_scan2_kernel<<<2, kScanThreads, 0, st>>>(Ra, Rb, F.geom.n_cells);
+  route_scatter2_kernel<<<blocks_for(std::max<size_t>(n_upper, (size_t)F.geom.n_cells)), 256, 0, st>>>(Ra, Rb, F.geom.n_cells);
   F.stats.kernel_launches += 2;
   KNF_CUDA(cudaGetLastError());
   return 0;
@@ -465,7 +487,6 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
       Rf.sorted = W.sorted_f.as<float4>();
       Rf.live = M.live[2 + cur];
       Rf.small_tiles = tc5 ? 3 : 0;  // tcgen05 filter: tiles of <= 128 requests (one per thread of a 128-thread CTA)
-      KNF_TRY(launch_scan_scatter(F, Rf, live_upper, st));
     }
     RouteBuffers R = route_buffers(F, cur, nxt, cur);
     R.eval_counter = stat_counter(F, 3);  // requests that went through global routing
@@ -473,7 +494,8 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     R.live = M.live[cur];
     const bool small_only = exact_mode && exact_sparse && F.sparse_small_kernel;
     R.small_tiles = small_only ? 2 : 0;  // dense wavefronts: 64-request tiles for march_warp_kernel; sparse: <= 16 for march_small_kernel
-    KNF_TRY(launch_scan_scatter(F, R, live_upper, st));
+    if (filter_pass) KNF_TRY(launch_scan_scatter2(F, Rf, R, live_upper, st));
+    else KNF_TRY(launch_scan_scatter(F, R, live_upper, st));
     cudaStream_t st_exact = st;
     if (filter_pass && F.overlap_queues && F.side_stream) {
       KNF_CUDA(cudaEventRecord(F.ev_fork, st));

@@ -151,10 +151,8 @@ __device__ __forceinline__ void block_scan3(int& a, int& b, int& c, int* s_warp 
 // One CTA: per-cell request offsets and per-cell tile bases (the tile descriptors themselves are
 // written in parallel by route_scatter_kernel).  Optionally emits grid.route's occupied segments
 // (cells ascending, starts).  Re-zeroes the cell counters and the next pass's counters.
-static __global__ void __launch_bounds__(kScanThreads) route_scan_kernel(RouteBuffers R, int n_cells, int* __restrict__ seg_cell,
-                                                                  int* __restrict__ seg_start,
-                                                                  int* __restrict__ n_seg_out) {
-  __shared__ int s_warp[96];
+__device__ __forceinline__ void route_scan_body(const RouteBuffers& R, int n_cells, int* __restrict__ seg_cell, int* __restrict__ seg_start,
+                                                int* __restrict__ n_seg_out, int* s_warp) {
   const int tid = threadIdx.x;
   const int per = (n_cells + kScanThreads - 1) / kScanThreads;
   const int c0 = min(tid * per, n_cells);
@@ -196,9 +194,20 @@ static __global__ void __launch_bounds__(kScanThreads) route_scan_kernel(RouteBu
     }
   }
 }
+static __global__ void __launch_bounds__(kScanThreads) route_scan_kernel(RouteBuffers R, int n_cells, int* __restrict__ seg_cell,
+                                                                  int* __restrict__ seg_start,
+                                                                  int* __restrict__ n_seg_out) {
+  __shared__ int s_warp[96];
+  route_scan_body(R, n_cells, seg_cell, seg_start, n_seg_out, s_warp);
+}
+// The two queues of a march wavefront (filter, exact) in one launch: CTA 0 scans the first, CTA 1 the second.
+static __global__ void __launch_bounds__(kScanThreads) route_scan2_kernel(RouteBuffers Ra, RouteBuffers Rb, int n_cells) {
+  __shared__ int s_warp[96];
+  route_scan_body(blockIdx.x == 0 ? Ra : Rb, n_cells, nullptr, nullptr, nullptr, s_warp);
+}
 
 // perm[offset[cell] + rank] = request slot, and (in the same launch) the tile descriptors of every cell.
-static __global__ void route_scatter_kernel(RouteBuffers R, int n_cells) {
+__device__ __forceinline__ void route_scatter_body(const RouteBuffers& R, int n_cells) {
   const int n = R.ctr->n_requests;
   const int stride = gridDim.x * blockDim.x;
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -260,6 +269,11 @@ static __global__ void route_scatter_kernel(RouteBuffers R, int n_cells) {
     t.pad = 0;
     R.tiles[ti] = t;
   }
+}
+static __global__ void route_scatter_kernel(RouteBuffers R, int n_cells) { route_scatter_body(R, n_cells); }
+static __global__ void route_scatter2_kernel(RouteBuffers Ra, RouteBuffers Rb, int n_cells) {
+  route_scatter_body(Ra, n_cells);
+  route_scatter_body(Rb, n_cells);
 }
 
 }  // namespace knf
