@@ -222,6 +222,8 @@ int begin_call(Field& F, cudaStream_t st) {
     KNF_CUDA(cudaFuncSetAttribute(sdf_mma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<2>)));
     KNF_CUDA(cudaFuncSetAttribute(march_tc5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Tc5MarchSmem)));
     KNF_CUDA(cudaFuncSetAttribute(march_tc5_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));  // several 40 KB CTAs per SM
+    KNF_CUDA(cudaFuncSetAttribute(sdf_tc5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Tc5FwdSmem)));
+    KNF_CUDA(cudaFuncSetAttribute(sdf_tc5_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     if (!F.host_poll) KNF_CUDA(cudaMallocHost(&F.host_poll, 64));
     if (!F.side_stream) {
       KNF_CUDA(cudaStreamCreateWithFlags(&F.side_stream, cudaStreamNonBlocking));
@@ -332,6 +334,11 @@ static inline int mlp_grid(const Field& F, size_t n_upper, int ctas_per_sm = kWa
   return (int)std::max<size_t>(1, std::min<size_t>(tiles_upper, (size_t)148 * ctas_per_sm));
 }
 
+// tile shape of the batched SDF forward: 128-request tiles for the tcgen05 kernel of KNF_PRECISION_TENSOR_FP16X2
+static inline int sdf_forward_tile_mode(const Field& F) {
+  return (F.precision == KNF_PRECISION_TENSOR_FP16X2 && F.sdf_tc5_blobs && F.filter_kernel == 1) ? 3 : 0;
+}
+
 int launch_sdf_mlp(Field& F, const RouteBuffers& R, size_t n_upper, float* out_first, float* out_full, cudaStream_t st) {
   MlpParams P{};
   P.blobs = F.sdf_blobs;
@@ -345,6 +352,11 @@ int launch_sdf_mlp(Field& F, const RouteBuffers& R, size_t n_upper, float* out_f
   if (F.precision == KNF_PRECISION_TENSOR_BF16X3) {
     P.blobs = reinterpret_cast<const float*>(F.sdf_mma_blobs);
     sdf_mma_kernel<3><<<mlp_grid(F, n_upper, kMmaCtasPerSm), 32, sizeof(MmaSmemT<3>), st>>>(P);
+  } else if (F.precision == KNF_PRECISION_TENSOR_FP16X2 && R.small_tiles == 3) {
+    // routed in tiles of <= 128 (launch_scan_scatter callers pass small_tiles = 3 for this mode): tcgen05 / TMEM kernel
+    P.blobs = reinterpret_cast<const float*>(F.sdf_tc5_blobs);
+    const size_t tiles_upper = n_upper / 64 + std::min<size_t>(n_upper, (size_t)F.geom.n_cells) + 1;
+    sdf_tc5_kernel<<<(int)std::max<size_t>(1, std::min<size_t>(tiles_upper, (size_t)148 * kTc5CtasPerSm)), kTc5Tile, sizeof(Tc5FwdSmem), st>>>(P);
   } else if (F.precision == KNF_PRECISION_TENSOR_FP16X2) {
     P.blobs = reinterpret_cast<const float*>(F.sdf_mmah_blobs);
     sdf_mma_kernel<2><<<mlp_grid(F, n_upper, kMmaCtasPerSm), 32, sizeof(MmaSmemT<2>), st>>>(P);
@@ -383,6 +395,7 @@ int sdf_forward_device(Field& F, const float* pts, int64_t n, float* out_full, f
   KNF_TRY(ensure_requests(F, (size_t)n));
   RouteBuffers R = route_buffers(F, 2, -1);
   R.eval_counter = stat_counter(F, 0);
+  R.small_tiles = sdf_forward_tile_mode(F);
   route_emit_points_kernel<<<blocks_for((size_t)n), 256, 0, st>>>(R, F.geom, pts, (int)n, cell_out);
   F.stats.kernel_launches += 1;
   KNF_TRY(launch_scan_scatter(F, R, (size_t)n, st));
@@ -617,6 +630,7 @@ static int shade_common(Field& F, ShadePoints S, int64_t m, const ShadeTargets& 
   S.count = nullptr;
   RouteBuffers R = route_buffers(F, 2, -1);
   R.eval_counter = stat_counter(F, 0);
+  R.small_tiles = sdf_forward_tile_mode(F);
   shade_emit_kernel<<<blocks_for(nreq), 256, 0, st>>>(R, F.geom, S, np);
   F.stats.kernel_launches += 1;
   KNF_TRY(launch_scan_scatter(F, R, nreq, st));

@@ -451,6 +451,131 @@ static __global__ void __launch_bounds__(kTc5Tile, kTc5CtasPerSm) march_tc5_kern
   if (warp == 0) tc5_dealloc(tmem, kTc5TmemCols);
 }
 
+
+// ---- batched forward on tcgen05 (grid.sdf_query / sdf_values in KNF_PRECISION_TENSOR_FP16X2) -------------------------
+// Same tile, same operand pieces, an accurate polynomial softplus (softplus_f2xN: 0.42 ulp mean against float64, like
+// NumPy's) instead of the filter's MUFU one, and all nine outputs: out[j] = sum_k h2[k] W3[j][k] + b3[j] as in-thread fp32 FMAs in ascending k.
+struct Tc5FwdSmem {
+  alignas(128) uint8_t w[Tc5Blob::bytes];            // B1 | B2 | fp32 constants | W3t
+  alignas(128) uint8_t a[2 * kTc5AChunks * kTc5Tile * 16];
+  alignas(8) uint64_t bar_w;
+  alignas(8) uint64_t bar_mma;
+  uint32_t tmem_slot;
+  int tile_ix;
+};
+
+static __global__ void __launch_bounds__(kTc5Tile, kTc5CtasPerSm) sdf_tc5_kernel(MlpParams P) {
+  extern __shared__ __align__(128) unsigned char tc5_smem_raw[];
+  Tc5FwdSmem& S = *reinterpret_cast<Tc5FwdSmem*>(tc5_smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (tid == 0) {
+    mbar_init(&S.bar_w, 1);
+    mbar_init(&S.bar_mma, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tc5_alloc(&S.tmem_slot, kTc5TmemCols);
+  tc5_fence_before();
+  __syncthreads();
+  tc5_fence_after();
+  const uint32_t tmem = S.tmem_slot;
+  const uint32_t tmem_lane = tmem + ((uint32_t)(warp * 32) << 16);
+  const int n_tiles = P.ctr->n_tiles;
+  const uint8_t* blobs = reinterpret_cast<const uint8_t*>(P.blobs);
+  const float* F32 = reinterpret_cast<const float*>(S.w + Tc5Blob::off_f32);
+  uint32_t par_w = 0, par_mma = 0;
+
+  for (;;) {
+    if (tid == 0) S.tile_ix = atomicAdd(&P.ctr->tile_cursor, 1);
+    __syncthreads();  // also: every thread is done with the previous tile's shared memory
+    const int tix = S.tile_ix;
+    if (tix >= n_tiles) break;
+    const Tile tile = P.tiles[tix];
+    if (tid == 0) {
+      fence_proxy_async();
+      mbar_expect_tx(&S.bar_w, Tc5Blob::bytes);
+      bulk_copy_g2s(S.w, blobs + (size_t)tile.cell * Tc5Blob::bytes, Tc5Blob::bytes, &S.bar_w);
+    }
+    int slot = -1;
+    float4 pt = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (tid < tile.count) {
+      slot = P.perm[tile.start + tid];
+      pt = P.req_pt[slot];
+    }
+    const bool warp_active = __any_sync(0xffffffffu, slot >= 0);
+    if (warp_active) tc5_encode_store(S.a, tid, pt.x, pt.y, pt.z);
+    fence_proxy_async();
+    tc5_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      mbar_wait(&S.bar_w, par_w);
+      tc5_fence_after();
+      tc5_issue_layer<3>(tmem, smem_u32(S.a), smem_u32(S.w + Tc5Blob::off_b1), &S.bar_mma);
+    }
+    tc5_mbar_wait(&S.bar_mma, par_mma);
+    par_mma ^= 1;
+    tc5_fence_after();
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      float2 z[8];
+      tc5_load_half(tmem_lane, h, nullptr, z);
+      if (warp_active) {
+        softplus_f2xN<8>(z);  // 24 packed steps per pair; as accurate against float64 as NumPy's own (knf_common.cuh), not bit-equal to it
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+          const float v[8] = {z[4 * c].x, z[4 * c].y, z[4 * c + 1].x, z[4 * c + 1].y, z[4 * c + 2].x, z[4 * c + 2].y, z[4 * c + 3].x, z[4 * c + 3].y};
+          tc5_store_chunk(S.a, 2 * h + c, tid, v);
+        }
+      }
+    }
+    fence_proxy_async();
+    tc5_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc5_fence_after();
+      tc5_issue_layer<2>(tmem, smem_u32(S.a), smem_u32(S.w + Tc5Blob::off_b2), &S.bar_mma);
+    }
+    mbar_wait(&S.bar_w, par_w);  // (long complete: the fp32 constants are read below by every thread)
+    par_w ^= 1;
+    tc5_mbar_wait(&S.bar_mma, par_mma);
+    par_mma ^= 1;
+    tc5_fence_after();
+    // outputs 0..8 (+ 3 pad columns) as six packed accumulators, ascending k
+    float2 acc[6];
+#pragma unroll
+    for (int j = 0; j < 6; j++) acc[j] = *reinterpret_cast<const float2*>(F32 + Tc5Blob::f_b3 + 2 * j);
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      float2 z[8];
+      tc5_load_half(tmem_lane, h, F32 + Tc5Blob::f_b2, z);
+      if (warp_active) {
+        softplus_f2xN<8>(z);  // 24 packed steps per pair; as accurate against float64 as NumPy's own (knf_common.cuh), not bit-equal to it
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+          const float hv = (i & 1) ? z[i >> 1].y : z[i >> 1].x;
+          const float4* wrow = reinterpret_cast<const float4*>(F32 + Tc5Blob::f_w3t + (16 * h + i) * kSdfOutPad);
+          const float4 w0 = wrow[0], w1 = wrow[1], w2 = wrow[2];
+          acc[0] = __ffma2_rn(splat(hv), make_float2(w0.x, w0.y), acc[0]);
+          acc[1] = __ffma2_rn(splat(hv), make_float2(w0.z, w0.w), acc[1]);
+          acc[2] = __ffma2_rn(splat(hv), make_float2(w1.x, w1.y), acc[2]);
+          acc[3] = __ffma2_rn(splat(hv), make_float2(w1.z, w1.w), acc[3]);
+          acc[4] = __ffma2_rn(splat(hv), make_float2(w2.x, w2.y), acc[4]);
+        }
+      }
+    }
+    if (slot >= 0) {
+      if (P.out_first) P.out_first[slot] = acc[0].x;
+      if (P.out_full) {
+        float* o = P.out_full + (size_t)slot * kSdfOut;
+        o[0] = acc[0].x; o[1] = acc[0].y; o[2] = acc[1].x; o[3] = acc[1].y; o[4] = acc[2].x;
+        o[5] = acc[2].y; o[6] = acc[3].x; o[7] = acc[3].y; o[8] = acc[4].x;
+      }
+    }
+  }
+  tc5_fence_before();
+  __syncthreads();
+  if (warp == 0) tc5_dealloc(tmem, kTc5TmemCols);
+}
+
 #endif  // KNF_TC5_LAYOUT_ONLY
 
 }  // namespace knf
