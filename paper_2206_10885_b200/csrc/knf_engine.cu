@@ -12,6 +12,7 @@
 #include "knf_mlp.cuh"
 #include "knf_mma.cuh"
 #include "knf_rays.cuh"
+#include "knf_tail.cuh"
 #include "knf_tc5.cuh"
 
 namespace knf {
@@ -52,7 +53,7 @@ void DevBuf::release() {
 }
 
 void Workspace::release_all() {
-  DevBuf* all[] = {&sorted_f, &tiles_f, &cell_offset_f, &tile_base_f, &req_pt2, &req_cell2, &req_rank2, &req_pt3, &req_cell3, &req_rank3, &cell_count_f, &sorted, &live2, &live3, &tile_base, &req_pt1, &req_cell1, &req_rank1, &req_pt, &req_cell, &req_rank, &perm, &tiles, &cell_count, &cell_offset, &counters, &t, &t_prev,
+  DevBuf* all[] = {&tail_cursor, &sorted_f, &tiles_f, &cell_offset_f, &tile_base_f, &req_pt2, &req_cell2, &req_rank2, &req_pt3, &req_cell3, &req_rank3, &cell_count_f, &sorted, &live2, &live3, &tile_base, &req_pt1, &req_cell1, &req_rank1, &req_pt, &req_cell, &req_rank, &perm, &tiles, &cell_count, &cell_offset, &counters, &t, &t_prev,
                    &d_prev, &t_conv, &d_conv, &t_hit, &steps, &phase, &hit, &live0, &live1, &hit_list,
                    &hit_count, &sdf_out, &col_v, &col_n, &col_z, &rgb, &origins, &dirs, &t_near, &t_far, &normals64,
                    &colors64, &frame_color, &frame_depth, &frame_normal, &frame_hit};
@@ -135,6 +136,7 @@ int ensure_rays(Field& F, size_t n) {
   }
   KNF_TRY(W.hit_list.ensure(n * 4));
   KNF_TRY(W.hit_count.ensure(16));
+  KNF_TRY(W.tail_cursor.ensure(16));
   W.ray_cap = std::max(W.ray_cap, n);
   return ensure_requests(F, n);
 }
@@ -473,6 +475,8 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
   F.prof_last_end = (size_t)-1;
   size_t live_upper = (size_t)n;  // upper bound on the size of any queue from here on: sizes the routing and tile grids
   const int max_wavefronts = 2 * s.max_steps + 6;
+  // hand-over point to the one-warp-per-ray tail kernel: a fixed count for large marches, 1/16 of the rays for small ones
+  const int tail_at = F.tail_threshold > 0 ? (int)std::min<int64_t>(F.tail_threshold, std::max<int64_t>(n / 16, 2048)) : 0;
   for (int w = 0; w < max_wavefronts; w++) {
     const int cur = w & 1, nxt = cur ^ 1;
     const bool filter_pass = exact_mode && F.fp16_ok && F.filter_mode != 0 && !filter_drained && w > 0;
@@ -572,7 +576,9 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     }
     F.stats.kernel_launches += 1;
     F.stats.wavefronts += 1;
-    const bool poll = (w == 0 && probing) || (w == 1) || (w == 3) || (w % 8 == 7);
+    // (more often once the live count nears the tail threshold, so the hand-over is not missed by several wavefronts)
+    const bool near_tail = exact_mode && tail_at > 0 && live_upper <= (size_t)tail_at * 6 && w > 3;
+    const bool poll = (w == 0 && probing) || (w == 1) || (w == 3) || (w % 8 == 7) || (near_tail && (w & 1));
     if (poll && w + 1 < max_wavefronts) {
       // n_requests of the next exact queue and of the next filter queue
       KNF_CUDA(cudaMemcpyAsync(F.host_poll, &counters(F, nxt)->n_requests, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -585,6 +591,31 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
         seen_total = (size_t)n_exact + (size_t)n_filter;
       }
       if (n_exact == 0 && n_filter == 0) break;
+      if (exact_mode && tail_at > 0 && n_exact + n_filter <= tail_at) {
+        // few rays left: one warp per ray to completion instead of more global wavefronts (knf_tail.cuh)
+        MarchTailArgs T{};
+        T.blobs = F.sdf_blobs;
+        T.G = F.geom;
+        T.M = M;
+        for (int a = 0; a < 3; a++) T.cell_scale[a] = A.cell_scale[a];
+        const RouteBuffers Qa = route_buffers(F, nxt, -1, nxt), Qb = route_buffers(F, 4 + nxt, -1, 2 + nxt);
+        T.live_a = M.live[nxt]; T.pt_a = Qa.req_pt; T.cell_a = Qa.req_cell; T.ctr_a = Qa.ctr;
+        T.live_b = M.live[2 + nxt]; T.pt_b = Qb.req_pt; T.cell_b = Qb.req_cell; T.ctr_b = Qb.ctr;
+        T.cursor = W.tail_cursor.as<int>();
+        T.eval_counter = stat_counter(F, 0);
+        KNF_CUDA(cudaMemsetAsync(W.tail_cursor.p, 0, 16, st));
+        const int rays_left = n_exact + n_filter;
+        const int grid = std::max(1, std::min((rays_left + kTailWarps - 1) / kTailWarps, 148 * 8));
+        {
+          ProfScope prof(F, st, SPAN_SDF_MLP);
+          march_tail_kernel<<<grid, 32 * kTailWarps, 0, st>>>(T);
+        }
+        F.stats.kernel_launches += 1;
+        // the pending queues were consumed without a routing pass: leave their per-cell counts as a pass would
+        KNF_CUDA(cudaMemsetAsync(W.cell_count.p, 0, (size_t)F.geom.n_cells * sizeof(int), st));
+        KNF_CUDA(cudaMemsetAsync(W.cell_count_f.p, 0, (size_t)F.geom.n_cells * sizeof(int), st));
+        break;
+      }
       exact_sparse = (size_t)n_exact * (size_t)F.sparse_div < (size_t)n;
       live_upper = std::max<size_t>((size_t)n_exact + (size_t)n_filter, 1);  // rays only retire: an upper bound for every later queue
       if (probing && w == 0 && (size_t)n_filter * 8 < (size_t)(n_exact + n_filter)) use_filter = false;  // < 1/8 of the live rays crawl

@@ -50,6 +50,7 @@ struct Workspace {
   // march state
   DevBuf t, t_prev, d_prev, t_conv, d_conv, t_hit, steps, phase, hit, live0, live1;
   // shading
+  DevBuf tail_cursor;
   DevBuf hit_list, hit_count, sdf_out, col_v, col_n, col_z, rgb;
   // render-frame ray buffers
   DevBuf origins, dirs, t_near, t_far, normals64, colors64;
@@ -102,6 +103,7 @@ struct Field {
   int* host_poll = nullptr;  // pinned; early-out polling of the march loop
   cudaStream_t side_stream = nullptr;    // the exact queue's tile kernels run here, beside the filter kernel on the caller's stream
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int tail_threshold = 24576;            // hand the march to march_tail_kernel (one warp per ray) once this few rays are live; 0: never (KNF_TAIL)
   bool overlap_queues = true;            // KNF_OVERLAP=0: one stream, filter then exact (the round-1 schedule)
   cudaEvent_t last_call_done = nullptr;  // recorded at the end of every call (CallScope)
   void* last_call_stream = nullptr;
