@@ -277,19 +277,11 @@ def ncu_traffic(which: str):
     return None
 
 
+_FILTER_KERNEL = {"name": "march_tc5_kernel"}
+
+
 def filter_kernel_name():
-    try:
-        from paper_2206_10885_b200 import _native as N
-
-        fn = getattr(N.load(), "knf_filter_kernel_name", None)
-        if fn is not None:
-            import ctypes
-
-            fn.restype = ctypes.c_char_p
-            return fn().decode()
-    except Exception:
-        pass
-    return "march_mma_kernel<2, true>"
+    return _FILTER_KERNEL["name"]
 
 
 def _event_ms(fn, warm=1, it=3):
@@ -349,16 +341,22 @@ def other_configs(fs, field, peaks, ffma_peak, tensor_peak):
     ms = _event_ms(lambda: orbit(fs), warm=1, it=1)
     out["config2_orbit_800x800_random_init_16"] = {"views": 25, "ms_total": ms, "fps": 25e3 / ms, "mrays_per_s": 25 * 640000 / ms / 1e3}
     trained = {}
-    for name in ("sphere_stripes_r16_distilled.knf", "sphere_stripes_r8_distilled.knf", "sphere_r4_distilled.knf"):
-        path = os.path.join(ROOT, "tests", "golden", name)
-        if os.path.exists(path):
-            trained[name] = surface.FieldSurface(load_model(path))
+    r8 = os.path.join(ROOT, "tests", "golden", "sphere_stripes_r8_distilled.knf")
+    if os.path.exists(r8):
+        f8 = load_model(r8)
+        # the 12 000-step distilled 8^3 field refined onto the 16^3 grid of the BASELINE configs (same function, 4096 MLPs)
+        trained["trained_16_refined_from_r8_distilled"] = surface.FieldSurface(grid.refine_field(f8, 2))
+        trained["trained_8_distilled_12k"] = surface.FieldSurface(f8)
     for name, surf in trained.items():
         ms = _event_ms(lambda: orbit(surf), warm=1, it=1)
         out[f"config2_orbit_800x800_{name}"] = {"views": 25, "ms_total": ms, "fps": 25e3 / ms, "mrays_per_s": 25 * 640000 / ms / 1e3}
         pose = orbit_view(3, 1920, 1080)
+        surf.dev.reset_stats()
         ms = _event_ms(lambda: surface.render_rows(surf, pose, settings, (1, 1, 1), 1, 0, 1080, device_out=True), warm=2, it=5)
-        out[f"config3_1920x1080_{name}"] = {"ms": ms, "fps": 1e3 / ms, "note": "trained field: the decision filter switches itself off, this is the exact FP32 path"}
+        st = surf.dev.stats()
+        out[f"config3_1920x1080_{name}"] = {"ms": ms, "fps": 1e3 / ms, "sdf_evals_per_ray": st["sdf_evals"] / max(st["rays"], 1),
+                                            "hit_fraction": st["hits"] / max(st["rays"], 1),
+                                            "note": "trained field: rays never crawl, the decision filter switches itself off -- this is the exact FP32 path"}
     # config 5: 3840x2160 path tracing, floor quad + neural object, 1 spp, 8 bounces
     pose = cameras.look_at_pose((0.5, 0.8, 3.2), (0, -0.2, 0), (0, 1, 0), np.deg2rad(45), 3840, 2160)
     quad = pathtrace.QuadObj((-3, -1.0, -3), (6, 0, 0), (0, 0, 6), pathtrace.Lambertian((0.7, 0.7, 0.7)))
@@ -413,6 +411,7 @@ def main():
     W, H = args.width, args.height
     field = grid.field_init(grid.GridConfig(resolution=16), seed=0)
     fs = surface.FieldSurface(field, device=local)
+    _FILTER_KERNEL["name"] = fs.dev.filter_kernel()
     settings = surface.RenderSettings()
     dev = torch.device("cuda", local)
     rows_mode = args.shard == "rows" and world > 1
@@ -518,33 +517,44 @@ def main():
         route_gbs = route_bytes / (stats["route_ms"] * 1e-3) / 1e9 if stats["route_ms"] > 0 else None
         # what the reference evaluates for the same frames: every crawl step the filter decided or certified counts once
         ref_evals = stats["sdf_evals"] + stats["filter_evals"] - stats["filter_deferred"] + stats["filter_skipped"]
+        clock_hz = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
         roof_exact = {
-            "kernel": "march_warp_kernel + march_small_kernel / mlp_warp_kernel (fused encode + 3-layer SDF MLP as k-ordered fp32 FMA chains + NumPy-exact softplus + sphere-trace step)",
+            "kernel": "march_warp_kernel / march_small_kernel / march_tail_kernel / mlp_warp_kernel (fused encode + 3-layer SDF MLP as k-ordered fp32 FMA chains + NumPy-exact softplus + sphere-trace step)",
             "bound": "fp32", "achieved": exact_tflops, "peak": ffma_peak, "unit": "TFLOP/s", "frac": (exact_tflops / ffma_peak) if exact_tflops else None,
             "peak_source": f"derived: {SM_COUNT} SMs x {FFMA_LANES_PER_SM} FFMA lanes x 2 x sm_max_mhz ({peak_src} MEASURED_PEAKS.json holds HBM and bf16-tensor "
                            "peaks only); measured attainable FP32 rates on this pool: 71.0 TFLOP/s packed FFMA2, 52.0 with one LDS.128 per 16 FFMA2 (profiles/ffma_peak_micro_r1.txt)",
             "evals": int(stats["sdf_evals"]), "launches": int(stats["sdf_mlp_launches"]), "avg_launch_ms": stats["sdf_mlp_ms"] / max(stats["sdf_mlp_launches"], 1),
-            "share_of_step": stats["sdf_mlp_ms"] / ms, "tile_fill": stats["sdf_evals"] / max(stats["march_lane_slots"], 1),
-            "note": "after the decision filter only ~3 % of the evaluations reach these kernels, mostly in sparse <= 16-request tiles (tile_fill): achieved counts useful evaluations only",
+            "elapsed_share_of_step": stats["sdf_mlp_ms"] / ms, "tile_fill": stats["sdf_evals"] / max(stats["march_lane_slots"], 1),
+            "note": "these launches run on a side stream CONCURRENTLY with the filter kernel (sparse, latency-bound tiles): their summed elapsed time overlaps the filter's and "
+                    "is not a share of the step; achieved = useful evaluations x 5120 flop over that elapsed time, so it understates the kernels alone "
+                    "(dense batched forward, config 4: see configs.config4_batched_forward)",
         }
+        tc5 = filter_kernel_name() == "march_tc5_kernel"
+        filter_evals_per_s = stats["filter_evals"] / (stats["filter_ms"] * 1e-3) if stats["filter_ms"] > 0 else None
+        xu_peak_evals = SM_COUNT * 16 * clock_hz / 128.0  # 128 MUFU (64 softplus x ex2 + lg2) per evaluation, 16 MUFU lanes per SM and clock
         roof_filter = {
-            "kernel": "march_mma_kernel<2, filter> (decision filter: Fourier recurrence + fp16x2 split mma.sync.m16n8k16 layers chained in registers + MUFU softplus "
-                      "+ sphere-trace crawl step + certified skipping)",
+            "kernel": ("march_tc5_kernel (decision filter: Fourier features + fp16x2 operand split in the threads, tcgen05.mma M128 N64/N32 K16 issued by one thread, "
+                       "accumulators in TMEM read back with tcgen05.ld, MUFU softplus, sphere-trace crawl step + certified skipping)") if tc5 else
+                      "march_mma_kernel<2, filter> (decision filter on mma.sync.m16n8k16)",
             "bound": "tensor", "achieved": filter_tflops, "peak": tensor_peak, "unit": "TFLOP/s", "frac": (filter_tflops / tensor_peak) if filter_tflops else None,
             "traffic": ncu_traffic("filter"),
-            "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch of the filter kernel, read from the committed ncu --set full capture "
-                            "profiles/ncu_traffic.json (null when that file has no entry for the kernel this build runs); weights and ray state are L2-resident",
-            "peak_source": f"{peak_src} MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS, tcgen05 path); mma.sync (HMMA.16816) issue peak measured on this pool: "
-                           "553 TFLOP/s (profiles/hmma_split_r1.txt)",
+            "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum per dense launch of the filter kernel, from the committed ncu --set full capture "
+                            "(profiles/ncu_traffic.json; null when that file holds another kernel than the one this build runs); weights and ray state are L2-resident",
+            "peak_source": f"{peak_src} MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS, tcgen05 path)",
             "algorithmic_flop_per_launch": stats["filter_evals"] * FLOP_PER_SDF_EVAL / max(stats["filter_launches"], 1),
             "avg_launch_ms": stats["filter_ms"] / max(stats["filter_launches"], 1), "launches": int(stats["filter_launches"]),
             "share_of_step": stats["filter_ms"] / ms,
-            "hmma_flop_per_eval": 15360,
-            "hmma_issued_tflops": (stats["filter_evals"] * 15360 / (stats["filter_ms"] * 1e-3) / 1e12) if stats["filter_ms"] > 0 else None,
-            "note": "achieved = filter evaluations x 5120 algorithmic flop; each evaluation issues 3 fp16 piece products over K padded to 48 + 32 "
-                    "(15360 tensor flop).  The kernel is co-limited by issue slots (57 %), the MUFU pipe (45 %) and the tensor pipe (38 %), see profiles/",
+            "tensor_flop_issued_per_eval": 15360,
+            "tensor_issued_tflops": (stats["filter_evals"] * 15360 / (stats["filter_ms"] * 1e-3) / 1e12) if stats["filter_ms"] > 0 else None,
+            "evals_per_s": filter_evals_per_s,
+            "binding_pipe": {"name": "XU (MUFU ex2 / lg2 of the 64 softplus per evaluation)", "peak_evals_per_s": xu_peak_evals,
+                             "frac": (filter_evals_per_s / xu_peak_evals) if filter_evals_per_s else None,
+                             "note": "ncu (profiles/ncu_r2_tc5_filter.summary.txt): XU pipe 55 %, issue slots 57 %, tensor pipe 12 % busy in a dense launch -- the tensor "
+                                     "cores wait for the CUDA-core activation math, so the fraction of tensor peak is not what limits this kernel"},
+            "note": "achieved = filter evaluations x 5120 algorithmic flop / summed CUDA-event time of the filter launches; each evaluation issues 3 fp16 piece products "
+                    "over K padded to 48 + 32 (15360 tensor flop)",
         }
-        dominant = roof_filter if stats["filter_ms"] >= stats["sdf_mlp_ms"] else roof_exact
+        dominant = roof_filter if stats["filter_ms"] >= 0.3 * ms else roof_exact  # the exact launches overlap the filter's: their elapsed sum is not a share
         line = {
             "metric": f"fps_{W}x{H}_sphere_traced", "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong" if rows_mode else "weak",

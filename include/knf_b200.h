@@ -163,6 +163,9 @@ double knf_field_filter_delta(knf_field_t f);
 /* number of cells the filter is switched off for (bound = +inf): cells whose hidden activations could leave the
  * fp16 range of the tensor-core operand pieces (very large weights); their samples all go to the exact kernel */
 int knf_field_filter_cells_off(knf_field_t f);
+/* name of the decision-filter kernel this handle launches: "march_tc5_kernel" (tcgen05.mma, accumulators in tensor
+ * memory; the default) or "march_mma_kernel<2, true>" (mma.sync; environment KNF_FILTER_KERNEL=mma).  For reports. */
+const char* knf_field_filter_kernel(knf_field_t f);
 
 /* ---- routing: grid.py:176-213 ------------------------------------------------------------ */
 /* grid.cell_index_flat (grid.py:182-185) on fp32 points (fp64 arithmetic, bit-exact). */

@@ -132,6 +132,7 @@ _SIGNATURES = {
     "knf_field_set_filter": [_P, _I32],
     "knf_field_filter_delta": [_P],
     "knf_field_filter_cells_off": [_P],
+    "knf_field_filter_kernel": [_P],
     "knf_cell_index": [_P, _P, _I64, _P, _I32, _P],
     "knf_cell_index_f64": [_P, _P, _I64, _P, _I32, _P],
     "knf_route": [_P, _P, _I64, _P, _P, _P, _P, _P, _I32, _P],
@@ -189,6 +190,7 @@ def load():
             fn.argtypes = args
             fn.restype = C.c_int
         lib.knf_field_filter_delta.restype = C.c_double
+        lib.knf_field_filter_kernel.restype = C.c_char_p
         lib.knf_last_error.argtypes = []
         lib.knf_last_error.restype = C.c_char_p
         if lib.knf_abi_version() != 2:

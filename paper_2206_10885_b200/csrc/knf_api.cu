@@ -873,6 +873,11 @@ double knf_field_filter_delta(knf_field_t f) {
   return f->f.filter_delta_max;
 }
 
+const char* knf_field_filter_kernel(knf_field_t f) {
+  if (check_field(f) != 0) return "";
+  return (f->f.filter_kernel == 1 && f->f.sdf_tc5_blobs) ? "march_tc5_kernel" : "march_mma_kernel<2, true>";
+}
+
 int knf_field_filter_cells_off(knf_field_t f) {
   KNF_TRY(check_field(f));
   return f->f.fp16_ok ? f->f.filter_cells_off : f->f.geom.n_cells;

@@ -126,6 +126,26 @@ def field_init(cfg: GridConfig, seed: int, dtype=np.float32, init_s: float = 20.
     return KiloField(cfg, sdf, col, np.array(np.log(init_s), dtype=dtype))
 
 
+def refine_field(field: KiloField, factor: int = 2) -> KiloField:
+    """The same field on a grid `factor` times finer per axis: every child cell inherits its parent's networks, which
+    take GLOBAL coordinates (grid.py:373-380 encodes the point, not a cell-local offset), so the SDF / colour functions
+    are unchanged -- bit for bit, since a point is evaluated by identical weights with identical arithmetic.  Gives a
+    trained 16^3-cell (4096-MLP) workload from the committed 8^3 fixture without shipping an 84 MB model file."""
+    if factor < 1:
+        raise ValueError("factor must be >= 1")
+    cfg = field.config
+    n, m = int(cfg.resolution), int(cfg.resolution) * int(factor)
+    idx = np.arange(m) // factor
+    parent = ((idx[:, None, None] * n + idx[None, :, None]) * n + idx[None, None, :]).reshape(-1)
+    fine = GridConfig(m, tuple(cfg.bbox_min), tuple(cfg.bbox_max), cfg.sdf_freqs, cfg.dir_freqs, cfg.feature_dim, cfg.fd_step)
+
+    def fam(g):
+        return MlpGrid(list(g.layer_dims), list(g.activations), [np.ascontiguousarray(w[parent]) for w in g.weights],
+                       [np.ascontiguousarray(b[parent]) for b in g.biases])
+
+    return KiloField(fine, fam(field.sdf), fam(field.color), np.array(field.inv_std_param))
+
+
 # ---------------------------------------------------------------------------------------------
 # device residency
 
@@ -252,6 +272,10 @@ class DeviceField:
 
     def filter_delta(self) -> float:
         return float(N.load().knf_field_filter_delta(self.handle))
+
+    def filter_kernel(self) -> str:
+        """Which decision-filter kernel this handle launches (include/knf_b200.h knf_field_filter_kernel)."""
+        return N.load().knf_field_filter_kernel(self.handle).decode()
 
     def filter_cells_off(self) -> int:
         """Cells whose activations could leave the fp16 range: the decision filter leaves them to the exact kernel."""

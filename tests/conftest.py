@@ -59,3 +59,11 @@ def small_field():
     from paper_2206_10885_b200.grid import GridConfig, field_init
 
     return field_init(GridConfig(resolution=4), seed=7)
+
+
+@pytest.fixture(scope="session")
+def trained_field():
+    """8^3 field distilled for 12 000 steps with the reference's own training code (tests/golden/make_trained.py)."""
+    from paper_2206_10885_b200.modelio import load_model
+
+    return load_model(os.path.join(GOLDEN, "sphere_stripes_r8_distilled.knf"))
