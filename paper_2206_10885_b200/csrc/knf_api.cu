@@ -191,10 +191,10 @@ static inline void split_fp16x2(float w, uint16_t p[2]) {
 // Inputs are bounded by 1 (sin / cos) and by the box (raw coordinates).
 constexpr double kFp16Safe = 60000.0;  // below the largest finite fp16 (65504) with room for the rounding of a piece
 static double filter_delta(int pieces, const float* w1, const float* b1, const float* w2, const float* b2, const float* w3,
-                           const float* b3, double x_raw, bool bias1_in_mma = false) {
+                           const float* b3, double x_raw, bool bias1_in_mma = false, double softplus_abs_err = (double)kFastSoftplusErr) {
   const double e_rep = pieces == 2 ? 3.1 * std::ldexp(1.0, -22) : 0.0;
   const double e = e_rep + 155.0 * std::ldexp(1.0, -24) + std::ldexp(1.0, -18);
-  const double sp_rel = 2.0 * std::ldexp(1.0, -22), sp_abs = (double)kFastSoftplusErr;
+  const double sp_rel = 2.0 * std::ldexp(1.0, -22), sp_abs = softplus_abs_err;
   auto softplus = [](double z) { return std::log1p(std::exp(-std::fabs(z))) + std::max(z, 0.0); };
   double eh1[kHidden], H1[kHidden], eh2[kHidden], H2[kHidden];
   for (int n = 0; n < kHidden; n++) {
@@ -394,7 +394,7 @@ void pack_sdf_tc5(int n_cells, const float* const w[3], const float* const b[3],
     std::memcpy(f + Tc5Blob::f_b3, b3, kSdfOut * sizeof(float));
     for (int j = 0; j < kSdfOut; j++)
       for (int k = 0; k < kHidden; k++) f[Tc5Blob::f_w3t + k * kSdfOutPad + j] = w3[j * kHidden + k];
-    const double delta = filter_delta(2, w1, b1, w2, b2, w3, b3, x_raw, true);
+    const double delta = filter_delta(2, w1, b1, w2, b2, w3, b3, x_raw, true, (double)kTc5SoftplusErr);
     const float delta_f = delta < 1e30 ? std::nextafter((float)delta, INFINITY) : INFINITY;
     f[Tc5Blob::f_delta] = delta_f;
     if (delta_max && std::isfinite(delta_f)) *delta_max = std::max(*delta_max, (double)delta_f);

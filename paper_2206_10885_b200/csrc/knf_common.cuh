@@ -332,6 +332,31 @@ __device__ __forceinline__ void softplus_fast_f2xN(float2 (&x)[N]) {
   }
 }
 
+// One-MUFU variant for the tcgen05 filter (knf_tc5.cuh), where the XU pipe (ex2 + lg2 of 64 activations per evaluation) is
+// the busiest pipe: e = 2^(-|x| log2 e) by MUFU.EX2 as above, ln(1 + e) on [0, 1] by a degree-5 minimax polynomial on the
+// FMA pipe (packed) instead of MUFU.LG2.  Polynomial fitted in float64, evaluated here in fp32 Horner form: max |error|
+// 8.8e-6 on 200 001 grid points of [0, 1] (scripts/fit_log1p.py), + 2^-22 e from ex2.approx + three fp32 roundings <= 1:
+// kFastSoftplusPolyErr covers it with margin.  Like softplus_fast it only ever feeds the filter's predicate.
+constexpr float kFastSoftplusPolyErr = 1.0e-5f;  // + 2^-22 * y, accounted for in the filter bound
+template <int N>
+__device__ __forceinline__ void softplus_fast_poly_f2xN(float2 (&x)[N]) {
+#define KNF_C2(v) make_float2(v, v)
+#pragma unroll
+  for (int i = 0; i < N; i++) {
+    const float2 u = __fmul2_rn(x[i], KNF_C2(1.4426950408889634f));
+    float2 e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(-fabsf(u.x)));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(-fabsf(u.y)));
+    float2 p = __ffma2_rn(KNF_C2(0.0311028603464365f), e, KNF_C2(-0.1332147866487503f));
+    p = __ffma2_rn(p, e, KNF_C2(0.28669968247413635f));
+    p = __ffma2_rn(p, e, KNF_C2(-0.4907394051551819f));
+    p = __ffma2_rn(p, e, KNF_C2(0.9992988109588623f));
+    p = __ffma2_rn(p, e, KNF_C2(8.732203241379466e-06f));
+    x[i] = __fadd2_rn(p, make_float2(fmaxf(x[i].x, 0.0f), fmaxf(x[i].y, 0.0f)));
+  }
+#undef KNF_C2
+}
+
 // Which softplus the tile kernels run: 1 = softplus_np (NumPy bit-exact, 34 packed FMA-pipe steps per pair),
 // 0 = softplus_f2 (same accuracy against float64, 24 steps, agrees with NumPy on 64 % of arguments).
 #ifndef KNF_SOFTPLUS_EXACT

@@ -39,10 +39,16 @@
 
 namespace knf {
 
+// Activation of the filter kernel: 1 = one MUFU (ex2) + degree-5 polynomial ln(1 + e) (softplus_fast_poly_f2xN), 0 = two MUFU
+// (ex2 + lg2, softplus_fast_f2xN).  The blob's bound delta is computed for the matching error constant (kTc5SoftplusErr).
+#ifndef KNF_TC5_SOFTPLUS_POLY
+#define KNF_TC5_SOFTPLUS_POLY 1
+#endif
 constexpr int kTc5Tile = 128;     // requests per tile = threads per CTA = TMEM lanes
 constexpr int kTc5K1 = 48;        // layer-1 K: 39 features + the constant-1 bias feature + 8 zero columns
 constexpr int kTc5BiasK = kSdfIn; // index of the constant-1 feature
 constexpr int kTc5TmemCols = 64;  // D: big (0..31) | small (32..63)
+constexpr float kTc5SoftplusErr = KNF_TC5_SOFTPLUS_POLY ? kFastSoftplusPolyErr : kFastSoftplusErr;
 constexpr int kTc5AChunks = 5;    // K chunks (8 fp16 each) of an A piece the threads write: k = 0..39 (chunk 5 meets zero weights, see tc5_issue_layer)
 
 // ---- per-cell blob ----------------------------------------------------------------------------------------------
@@ -202,6 +208,14 @@ __device__ __forceinline__ void tc5_load_half(uint32_t taddr_lane, int h, const 
   }
 }
 
+#ifndef KNF_TC5_LAYOUT_ONLY
+template <int N>
+__device__ __forceinline__ void tc5_softplus(float2 (&z)[N]) {
+  if (KNF_TC5_SOFTPLUS_POLY) softplus_fast_poly_f2xN<N>(z);
+  else softplus_fast_f2xN<N>(z);
+}
+#endif
+
 #ifndef KNF_TC5_CTAS_PER_SM
 #define KNF_TC5_CTAS_PER_SM 6
 #endif
@@ -307,7 +321,7 @@ static __global__ void __launch_bounds__(kTc5Tile, kTc5CtasPerSm) march_tc5_kern
         float2 z[8];
         tc5_load_half(tmem_lane, h, nullptr, z);  // the bias came in through feature 39
         if (warp_active) {
-          softplus_fast_f2xN<8>(z);
+          tc5_softplus<8>(z);
 #pragma unroll
           for (int c = 0; c < 2; c++) {
             const float v[8] = {z[4 * c].x, z[4 * c].y, z[4 * c + 1].x, z[4 * c + 1].y, z[4 * c + 2].x, z[4 * c + 2].y, z[4 * c + 3].x, z[4 * c + 3].y};
@@ -334,7 +348,7 @@ static __global__ void __launch_bounds__(kTc5Tile, kTc5CtasPerSm) march_tc5_kern
           float2 z[8];
           tc5_load_half(tmem_lane, h, F32 + Tc5Blob::f_b2, z);
           if (warp_active) {
-            softplus_fast_f2xN<8>(z);
+            tc5_softplus<8>(z);
 #pragma unroll
             for (int i = 0; i < 8; i++) acc = __ffma2_rn(z[i], *reinterpret_cast<const float2*>(F32 + Tc5Blob::f_w3d + 16 * h + 2 * i), acc);
           }
