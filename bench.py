@@ -404,6 +404,8 @@ def main():
     torch.cuda.set_device(local)
     use_dist = world > 1 or "RANK" in os.environ  # under torchrun even a single rank goes through NCCL
     if use_dist:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # the communicator / rank log (stdout, before the JSON line, which stays last)
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))

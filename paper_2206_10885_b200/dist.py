@@ -137,3 +137,25 @@ def render_frame_sharded(surface, pose, settings=None, background=(1.0, 1.0, 1.0
         bands = render_rows(0, 1)
         bands = tuple(b[:0] for b in bands)
     return tuple(gather_row_bands(b, H, group) for b in bands)
+
+
+def render_pathtraced_sharded(scene, pose, spp: int, seed: int, max_bounces: int = 8, sample_offset: int = 0, group=None,
+                              interleave: int = 64, pathtrace_rows=None):
+    """BASELINE config 5: one path-traced frame split into interleaved row bands across the ranks of `group` (the per-pixel
+    counter RNG makes every pixel independent of the banding, pathtrace.py:439-442), hdr radiance assembled on every rank
+    with one all_gather.  Returns the (H, W, 3) float64 hdr tensor on the rank's device; `pathtrace_rows(r0, r1)` is
+    injectable so the host logic can be tested without a GPU."""
+    import torch
+    import torch.distributed as dist
+
+    from . import pathtrace as P
+
+    pathtrace_rows = pathtrace_rows or (lambda r0, r1: P.pathtrace_rows(scene, pose, spp, seed, max_bounces, sample_offset, r0, r1,
+                                                                        device_out=True))
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    H = int(pose.height)
+    mine = shard_rows_interleaved(H, rank, world, interleave)
+    parts = [pathtrace_rows(r0, r1) for r0, r1 in mine]
+    local = torch.cat(parts, dim=0) if parts else pathtrace_rows(0, 1)[:0]
+    return gather_interleaved_bands(local, H, interleave, group)

@@ -76,9 +76,11 @@ def _worker(rank, world, port, height, width, out_dir):
         color, depth, normal, hit = kd.render_frame_sharded(None, pose, settings=object(), render_rows=_fake_bands(width))
         views = kd.gather_views(torch.full((2, 3), float(rank)))
         inter = kd.render_frame_sharded(None, pose, settings=object(), render_rows=_fake_bands(width), interleave=2)
+        hdr = kd.render_pathtraced_sharded(None, pose, spp=1, seed=0, interleave=3,
+                                           pathtrace_rows=lambda r0, r1: _fake_bands(width)(r0, r1)[0].double())
         np.savez(os.path.join(out_dir, f"r{rank}.npz"), color=color.numpy(), depth=depth.numpy(), normal=normal.numpy(),
                  hit=hit.numpy(), views=views.numpy(), icolor=inter[0].numpy(), idepth=inter[1].numpy(), inormal=inter[2].numpy(),
-                 ihit=inter[3].numpy())
+                 ihit=inter[3].numpy(), hdr=hdr.numpy())
     finally:
         dist.destroy_process_group()
 
@@ -98,3 +100,4 @@ def test_sharded_frame_equals_single_process(tmp_path, height):
         # bands of 2 rows dealt round-robin, reassembled in image order
         assert np.array_equal(got["icolor"], want[0].numpy()) and np.array_equal(got["idepth"], want[1].numpy())
         assert np.array_equal(got["inormal"], want[2].numpy()) and np.array_equal(got["ihit"], want[3].numpy())
+        assert np.array_equal(got["hdr"], want[0].double().numpy())  # path-traced bands of 3 rows
