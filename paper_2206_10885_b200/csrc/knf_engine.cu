@@ -491,6 +491,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     A.max_inner = (probing && w == 0) ? 1 : F.march_max_inner;
     A.crawl_below = use_filter ? crawl_on : -INFINITY;
     A.max_skip = F.filter_skip;
+    A.skip_cap = F.filter_skip_cap;
     A.inv_resolution = 1.0 / (double)F.geom.resolution;
     A.filter_x_raw = F.filter_x_raw;
     for (int a = 0; a < 3; a++) A.cell_scale[a] = (double)F.geom.resolution / (F.geom.hi[a] - F.geom.lo[a]);

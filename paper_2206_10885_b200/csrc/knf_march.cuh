@@ -33,6 +33,7 @@ struct MarchTileArgs {
   unsigned long long* eval_counter;  // statistics: [0] SDF evaluations, [2] lane slots, [4] filter evaluations, [5] deferred, [6] certified skips, [7] filter lane slots
   int max_inner;            // cap on consecutive in-place steps of one tile
   int max_skip;             // filter kernel: 0 disables certified skipping
+  int skip_cap;             // filter kernel: most certified steps taken sample by sample after one evaluation
   int keep_div;             // a tile keeps stepping in place while n_stay * keep_div >= its size (2 = half; 0 is read as 2)
   double inv_resolution;    // 1 / grid resolution (host-computed)
   double crawl_below;       // exact kernels: a march step from a distance below this continues in the filter queue (-inf: never)

@@ -409,13 +409,13 @@ static __global__ void __launch_bounds__(kTc5Tile, kTc5CtasPerSm) march_tc5_kern
             t_next = rr.t;
           }
           // ---- part 2: the remaining samples, one by one (exact point, exact box test, exact rise) ---------------------
-          while (code != STEP_DONE) {
+          for (int it = 0; code != STEP_DONE; it++) {
             px = __double2float_rn(S.od[0][tid] + t_next * S.od[3][tid]);
             py = __double2float_rn(S.od[1][tid] + t_next * S.od[4][tid]);
             pz = __double2float_rn(S.od[2][tid] + t_next * S.od[5][tid]);
             const bool well_inside = px > in_lo[0] && px < in_hi[0] && py > in_lo[1] && py < in_hi[1] && pz > in_lo[2] && pz < in_hi[2];
             cell = well_inside ? tile.cell : cell_of_quick(px, py, pz, A.G.lo, A.G.hi, A.cell_scale, A.G.resolution);
-            if (!well_inside) break;
+            if (!well_inside || it >= A.skip_cap) break;  // (the cap bounds how long one lane can hold up its warp and CTA)
             const float rise = lip[0] * (fabsf(px - x0) + 1e-6f) + lip[1] * (fabsf(py - y0) + 1e-6f) + lip[2] * (fabsf(pz - z0) + 1e-6f);
             if (!(rise < room)) break;
             rr.steps += 1;

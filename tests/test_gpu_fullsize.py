@@ -119,8 +119,9 @@ def test_full_hd_parity_bands(field16):
           f"depth<=1e-4 {tot['d_ok'] / max(tot['both'], 1):.4%} (max {worst['d']:.1e}), normal<=1e-3 {tot['n_ok'] / max(tot['both'], 1):.4%} "
           f"(max {worst['n']:.1e}), rgb<=1e-3 {tot['c_ok'] / max(tot['both'], 1):.4%} (max {worst['c']:.1e})")
     assert tot["both"] >= 1000  # the centre band carries the surface
-    assert agree >= 0.999
-    assert tot["d_ok"] >= 0.999 * tot["both"] and tot["n_ok"] >= 0.999 * tot["both"] and tot["c_ok"] >= 0.999 * tot["both"]
+    assert agree >= 0.9995  # measured 99.9886 % (21 flips of 184 320 rays)
+    # every both-hit pixel inside the depth and RGB bars (measured max 2.7e-5 / 6.7e-5); FD normals on >= 99.95 % (measured 99.986 %)
+    assert tot["d_ok"] == tot["both"] and tot["c_ok"] == tot["both"] and tot["n_ok"] >= 0.9995 * tot["both"]
 
 
 def test_frame_256_matches_oracle_statistics(field16):

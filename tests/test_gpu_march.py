@@ -301,5 +301,8 @@ def test_frame_random_init_256_parity(S, cams):
     cerr = np.abs(fb.color - ref.color)[both].max(axis=1)
     print(f"256^2 random-init: hit agreement {agree:.4%} ({int((fb.hit != ref.hit).sum())} flips), depth<=1e-4 {np.mean(rel <= 1e-4):.4%}, "
           f"normal<=1e-3 {np.mean(nerr <= 1e-3):.4%}, rgb<=1e-3 {np.mean(cerr <= 1e-3):.4%}")
-    assert agree >= 0.999
-    assert np.mean(rel <= 1e-4) >= 0.999 and np.mean(nerr <= 1e-3) >= 0.995 and np.mean(cerr <= 1e-3) >= 0.999
+    # north_star bars, asserted at what is achieved: hit masks >= 99.9 % (measured 99.963 %: 24 flips; the
+    # reference against itself across band sizes flips 6, tests/golden/reference_noise.json); EVERY both-hit pixel inside the
+    # depth 1e-4 and RGB 1e-3 bars; normals (FD: SDF ulps x 500) inside 1e-3 on >= 99.95 % (measured 100 %)
+    assert agree >= 0.9995
+    assert np.all(rel <= 1e-4) and np.all(cerr <= 1e-3) and np.mean(nerr <= 1e-3) >= 0.9995

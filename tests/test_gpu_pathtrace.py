@@ -84,7 +84,7 @@ def test_analytic_scene_matches_reference_golden(PT):
     out = PT.render_pathtraced(_scenes(PT), _pose(), spp=3, seed=11, max_bounces=8, sample_offset=2)
     err = np.abs(out.hdr - g["hdr"]).max(axis=2)
     print(f"analytic path trace: max err {err.max():.2e}, pixels within 1e-9: {(err <= 1e-9).mean():.4%}")
-    assert (err <= 1e-9).mean() >= 0.995
+    assert (err <= 1e-9).mean() >= 0.9995  # measured: max error 0.0
     assert np.abs(out.ldr - np.clip(out.hdr, 0, 1) ** (1 / 2.2)).max() == 0
 
 
@@ -130,7 +130,7 @@ def test_neural_object_scene(PT, distilled_field, distilled_oracle):
     out = PT.render_pathtraced(scene, _pose(), spp=2, seed=7, max_bounces=8)
     err = np.abs(out.hdr - g["hdr"]).max(axis=2)
     print(f"neural path trace vs reference golden: pixels within 1e-3: {(err <= 1e-3).mean():.4%}, max {err.max():.2e}")
-    assert (err <= 1e-3).mean() >= 0.97  # secondary bounces off FD normals amplify SDF ulps; see DESIGN.md
+    assert (err <= 1e-3).mean() >= 0.999  # measured: 100 % of pixels, max 4.8e-5 (a last-ulp difference in a bounce direction could move isolated pixels)
     t, obj, _ = PT.intersect_scene(scene, np.array([[0.5, 0.8, 3.2]]), np.array([[-0.1, -0.25, -1.0]]) / np.linalg.norm([-0.1, -0.25, -1.0]))
     ot, oobj, _ = oracle.nearest_hit(_oracle_scene(oracle.FieldTraceable(distilled_oracle)), np.array([[0.5, 0.8, 3.2]]),
                                      np.array([[-0.1, -0.25, -1.0]]) / np.linalg.norm([-0.1, -0.25, -1.0]))
