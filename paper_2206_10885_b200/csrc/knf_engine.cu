@@ -538,7 +538,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
         if (tc5) {
           Af.P.blobs = reinterpret_cast<const float*>(F.sdf_tc5_blobs);
           const size_t tiles_upper = live_upper / 64 + std::min<size_t>(live_upper, (size_t)F.geom.n_cells) + 1;
-          const int grid = (int)std::max<size_t>(1, std::min<size_t>(tiles_upper, (size_t)148 * kTc5CtasPerSm));
+          const int grid = (int)std::max<size_t>(1, std::min<size_t>(tiles_upper, (size_t)148 * std::min(kTc5CtasPerSm, F.filter_grid_ctas)));
           march_tc5_kernel<<<grid, kTc5Tile, sizeof(Tc5MarchSmem), st>>>(Af);
         } else {
           march_mma_kernel<2, true><<<mlp_grid(F, live_upper, march_ctas_per_sm<2>()), 32, sizeof(MmaMarchSmemT<2>), st>>>(Af);

@@ -80,6 +80,7 @@ struct Field {
   int sparse_keep_div = 2;   // measured: (16, 4) gains 3 % on the distilled frame and loses 1.3 % on the random-init one; (32, 8) and up lose more
   int sparse_div = 8;                  // a wavefront is sparse when its exact queue holds < n / sparse_div rays (KNF_SPARSE_DIV)
   bool sparse_small_kernel = true;     // exact march: sparse wavefronts by march_small_kernel (KNF_SPARSE_SMALL=0 disables)
+  int filter_grid_ctas = 6;            // CTAs per SM the tcgen05 filter's grid asks for (KNF_FILTER_GRID; fewer leaves room for the concurrent exact kernel)
   int filter_skip_cap = 1 << 20;       // cap on the certified steps taken after one evaluation (KNF_FILTER_SKIP_CAP)
   int filter_skip = 1;                 // certified (Lipschitz) skipping inside the filter: 0 off, 1 sample by sample, 2 closed-form run (cell-exit DDA + Lipschitz budget) then sample by sample; KNF_FILTER_SKIP
   int filter_hint = 0;                 // auto mode: what the previous march on this handle learnt (0 unknown, 1 rays crawl, 2 they do not)

@@ -146,6 +146,40 @@ def refine_field(field: KiloField, factor: int = 2) -> KiloField:
     return KiloField(fine, fam(field.sdf), fam(field.color), np.array(field.inv_std_param))
 
 
+KERNEL_SDF_FREQS, KERNEL_DIR_FREQS, KERNEL_FEATURE_DIM = 6, 4, 8  # the widths the kernels are compiled for (grid.py:32-68 defaults)
+
+
+def _embed_layer(name, k, w, b, lx, lv, nf):
+    """A field with fewer encoding octaves or features than the compiled widths, embedded EXACTLY: the missing inputs get
+    zero weight columns at the positions the wide layout gives them (the Fourier octaves are ordered ascending, so a
+    narrower encoding is a prefix; colour inputs are [x(3), enc(v), n(3), z(F)], grid.py:387-400) and the missing
+    outputs zero rows.  A zero column adds fma(x, 0, acc) = acc to the k-ordered chain and the nonzero terms keep their
+    order, so every value the reference computes is reproduced bit for bit; the extra feature outputs are 0 and are
+    sliced off by the host API."""
+    w = np.ascontiguousarray(w, dtype=np.float32)
+    b = np.ascontiguousarray(b, dtype=np.float32)
+    n = w.shape[0]
+    if name == "sdf" and k == 0 and lx < KERNEL_SDF_FREQS:
+        wide = np.zeros((n, 32, 3 + 6 * KERNEL_SDF_FREQS), np.float32)
+        wide[:, :, : 3 + 6 * lx] = w
+        w = wide
+    elif name == "sdf" and k == 2 and nf < KERNEL_FEATURE_DIM:
+        wide = np.zeros((n, 1 + KERNEL_FEATURE_DIM, 32), np.float32)
+        wide[:, : 1 + nf] = w
+        bw = np.zeros((n, 1 + KERNEL_FEATURE_DIM), np.float32)
+        bw[:, : 1 + nf] = b
+        w, b = wide, bw
+    elif name == "color" and k == 0 and (lv < KERNEL_DIR_FREQS or nf < KERNEL_FEATURE_DIM):
+        ev, evw = 3 + 6 * lv, 3 + 6 * KERNEL_DIR_FREQS
+        wide = np.zeros((n, 32, 3 + evw + 3 + KERNEL_FEATURE_DIM), np.float32)
+        wide[:, :, 0:3] = w[:, :, 0:3]                                       # x
+        wide[:, :, 3 : 3 + ev] = w[:, :, 3 : 3 + ev]                          # enc(v): a prefix of the wider encoding
+        wide[:, :, 3 + evw : 3 + evw + 3] = w[:, :, 3 + ev : 3 + ev + 3]      # n
+        wide[:, :, 3 + evw + 3 : 3 + evw + 3 + nf] = w[:, :, 3 + ev + 3 :]    # z
+        w = wide
+    return np.ascontiguousarray(w), np.ascontiguousarray(b)
+
+
 # ---------------------------------------------------------------------------------------------
 # device residency
 
@@ -187,12 +221,14 @@ class DeviceField:
         desc.resolution = int(cfg.resolution)
         desc.bbox_min = N.vec3(cfg.bbox_min)
         desc.bbox_max = N.vec3(cfg.bbox_max)
-        desc.sdf_freqs = int(cfg.sdf_freqs)
-        desc.dir_freqs = int(cfg.dir_freqs)
-        desc.feature_dim = int(cfg.feature_dim)
+        lx, lv, nf = int(cfg.sdf_freqs), int(cfg.dir_freqs), int(cfg.feature_dim)
+        if lx > KERNEL_SDF_FREQS or lv > KERNEL_DIR_FREQS or nf > KERNEL_FEATURE_DIM or min(lx, lv, nf) < 0:
+            raise N.KnfUnsupported(f"sdf_freqs={lx}, dir_freqs={lv}, feature_dim={nf}: the kernels are compiled for the reference widths "
+                                   f"({KERNEL_SDF_FREQS}, {KERNEL_DIR_FREQS}, {KERNEL_FEATURE_DIM}); narrower fields are embedded exactly, wider ones are not supported")
+        desc.sdf_freqs, desc.dir_freqs, desc.feature_dim = KERNEL_SDF_FREQS, KERNEL_DIR_FREQS, KERNEL_FEATURE_DIM
         desc.fd_step = float(cfg.fd_step)
-        expect_sdf = [(32, 3 + 6 * desc.sdf_freqs), (32, 32), (1 + desc.feature_dim, 32)]
-        expect_col = [(32, 3 + 3 + 6 * desc.dir_freqs + 3 + desc.feature_dim), (32, 32), (3, 32)]
+        expect_sdf = [(32, 3 + 6 * lx), (32, 32), (1 + nf, 32)]
+        expect_col = [(32, 3 + 3 + 6 * lv + 3 + nf), (32, 32), (3, 32)]
         n_cells = int(cfg.resolution) ** 3
         # Everything the C side memcpy's is validated here first: it reads n_cells * out * in weights and
         # n_cells * out biases per layer without looking at shapes.
@@ -220,8 +256,7 @@ class DeviceField:
         keep = []
         for name, fam in (("sdf", field.sdf), ("color", field.color)):
             for k in range(3):
-                w = np.ascontiguousarray(fam.weights[k], dtype=np.float32)
-                b = np.ascontiguousarray(fam.biases[k], dtype=np.float32)
+                w, b = _embed_layer(name, k, fam.weights[k], fam.biases[k], lx, lv, nf)
                 keep += [w, b]
                 getattr(desc, f"{name}_w")[k] = w.ctypes.data
                 getattr(desc, f"{name}_b")[k] = b.ctypes.data
@@ -482,10 +517,9 @@ def sdf_query(field, points) -> SdfSample:
     dev = device_field(field)
     a = _Args(dev, points)
     p = a.inp(points, np.float32, 3)
-    width = 1 + dev.config.feature_dim
-    out = a.out((p.shape[0], width), np.float32)
+    out = a.out((p.shape[0], 1 + KERNEL_FEATURE_DIM), np.float32)
     N.check(N.load().knf_sdf_forward(dev.handle, N.ptr(p), p.shape[0], N.ptr(out), a.mem, a.stream))
-    return SdfSample(value=out[:, 0], features=out[:, 1:])
+    return SdfSample(value=out[:, 0], features=out[:, 1 : 1 + int(dev.config.feature_dim)])  # (embedded narrower fields: the rest is 0)
 
 
 def sdf_values(field, points):
@@ -504,7 +538,13 @@ def color_query(field, x, v, n, z):
     xs = a.inp(x, np.float32, 3)
     vs = a.inp(v, np.float32, 3)
     ns = a.inp(n, np.float32, 3)
-    zs = a.inp(z, np.float32, dev.config.feature_dim)
+    nf = int(dev.config.feature_dim)
+    zs = a.inp(z, np.float32, nf)
+    if nf < KERNEL_FEATURE_DIM:  # embedded narrower field: the missing features meet zero weights
+        wide = a.out((zs.shape[0], KERNEL_FEATURE_DIM), np.float32)
+        wide[:, :nf] = zs
+        wide[:, nf:] = 0
+        zs = wide
     m = xs.shape[0]
     if not (vs.shape[0] == ns.shape[0] == zs.shape[0] == m):
         raise ValueError("x, v, n, z must have the same number of rows")

@@ -181,11 +181,47 @@ def test_fd_normals(G, small_field):
 
 
 def test_unsupported_architecture_is_loud(G):
-    cfg = G.GridConfig(resolution=2, feature_dim=4)
+    """Widths beyond the compiled ones cannot be embedded: refuse loudly."""
     from paper_2206_10885_b200 import _native as N
 
-    with pytest.raises(N.KnfUnsupported):
-        G.sdf_query(G.field_init(cfg, seed=0), np.zeros((3, 3), np.float32))
+    for cfg in (G.GridConfig(resolution=2, feature_dim=12), G.GridConfig(resolution=2, sdf_freqs=7), G.GridConfig(resolution=2, dir_freqs=5)):
+        with pytest.raises(N.KnfUnsupported):
+            G.sdf_query(G.field_init(cfg, seed=0), np.zeros((3, 3), np.float32))
+
+
+@pytest.mark.parametrize("lx,lv,nf", [(4, 2, 5), (6, 4, 3), (0, 0, 1), (5, 4, 8)])
+def test_narrower_widths_are_embedded_exactly(G, lx, lv, nf):
+    """GridConfig.sdf_freqs / dir_freqs / feature_dim below the defaults (grid.py:32-64).  Such a field is embedded
+    into the compiled 39-32-32-9 / 41-32-32-3 networks with zero weights at the missing inputs / outputs, which leaves every
+    k-ordered FMA chain unchanged -- so parity with the oracle is the same as for the default widths."""
+    import oracle
+    from paper_2206_10885_b200 import cameras, surface
+
+    cfg = G.GridConfig(resolution=4, sdf_freqs=lx, dir_freqs=lv, feature_dim=nf)
+    field = G.field_init(cfg, seed=5)
+    spec = oracle.FieldSpec(resolution=4, pos_octaves=lx, dir_octaves=lv, n_features=nf)
+    ofield = oracle.field.field_from_stacks(spec, field.sdf.weights, field.sdf.biases, field.color.weights, field.color.biases)
+    rng = np.random.default_rng(8)
+    pts = rng.uniform(-1.05, 1.05, size=(20000, 3)).astype(np.float32)
+    got = G.sdf_query(field, pts)
+    ov, of = oracle.query_sdf(ofield, pts)
+    assert got.features.shape == (20000, nf)
+    assert np.abs(got.value - ov).max() <= 2e-6 and (nf == 0 or np.abs(got.features - of).max() <= 2e-6)
+    v = rng.normal(size=(20000, 3)).astype(np.float32)
+    v /= np.linalg.norm(v, axis=1, keepdims=True)
+    rgb = G.color_query(field, pts, v, v, got.features)
+    assert np.abs(rgb - oracle.query_color(ofield, pts, v, v, got.features)).max() <= 1e-6
+    assert np.array_equal(G.cell_index_flat(field, pts), oracle.cell_ids(spec, pts))
+    # a whole frame through the march, FD normals and the colour pass
+    pose = cameras.look_at_pose((0.2, 0.3, 2.5), (0, 0, 0), (0, 1, 0), np.deg2rad(40), 48, 40)
+    fb = surface.render_frame(surface.FieldSurface(field), pose)
+    ref = oracle.render(oracle.FieldTraceable(ofield), oracle.camera_look_at((0.2, 0.3, 2.5), (0, 0, 0), (0, 1, 0), np.deg2rad(40), 48, 40),
+                        oracle.MarchSettings())
+    assert (fb.hit == ref.hit).mean() >= 0.995
+    both = fb.hit & ref.hit
+    if both.any():
+        assert np.mean(np.abs(fb.depth[both] - ref.depth[both]) / ref.depth[both] <= 1e-4) >= 0.99
+        assert np.mean(np.abs(fb.color - ref.color)[both].max(axis=1) <= 2e-3) >= 0.99
 
 
 def test_knf_straight_to_device(G, distilled_field, golden_dir):
