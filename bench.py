@@ -505,6 +505,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
+    final_line = None
     if rank == 0:
         peaks, peak_src = measured_peaks()
         frames_per_step = 1 if rows_mode else world
@@ -533,7 +534,8 @@ def main():
         }
         tc5 = filter_kernel_name() == "march_tc5_kernel"
         filter_evals_per_s = stats["filter_evals"] / (stats["filter_ms"] * 1e-3) if stats["filter_ms"] > 0 else None
-        xu_peak_evals = SM_COUNT * 16 * clock_hz / 128.0  # 128 MUFU (64 softplus x ex2 + lg2) per evaluation, 16 MUFU lanes per SM and clock
+        mufu_per_eval = 64.0 if tc5 else 128.0  # tcgen05 filter: one MUFU.EX2 per softplus (ln(1 + e) is a polynomial); mma.sync filter: ex2 + lg2
+        xu_peak_evals = SM_COUNT * 16 * clock_hz / mufu_per_eval  # 16 MUFU lanes per SM and clock
         roof_filter = {
             "kernel": ("march_tc5_kernel (decision filter: Fourier features + fp16x2 operand split in the threads, tcgen05.mma M128 N64/N32 K16 issued by one thread, "
                        "accumulators in TMEM read back with tcgen05.ld, MUFU softplus, sphere-trace crawl step + certified skipping)") if tc5 else
@@ -549,10 +551,11 @@ def main():
             "tensor_flop_issued_per_eval": 15360,
             "tensor_issued_tflops": (stats["filter_evals"] * 15360 / (stats["filter_ms"] * 1e-3) / 1e12) if stats["filter_ms"] > 0 else None,
             "evals_per_s": filter_evals_per_s,
-            "binding_pipe": {"name": "XU (MUFU ex2 / lg2 of the 64 softplus per evaluation)", "peak_evals_per_s": xu_peak_evals,
-                             "frac": (filter_evals_per_s / xu_peak_evals) if filter_evals_per_s else None,
-                             "note": "ncu (profiles/ncu_r2_tc5_filter.summary.txt): XU pipe 55 %, issue slots 57 %, tensor pipe 12 % busy in a dense launch -- the tensor "
-                                     "cores wait for the CUDA-core activation math, so the fraction of tensor peak is not what limits this kernel"},
+            "binding_pipe": {"name": "instruction issue / FMA pipe (CUDA-core work around the MMAs: 64 softplus, 71 operand splits, 39 Fourier features, fp64 march step)",
+                             "issue_slots_busy_ncu": 0.63, "fma_pipe_busy_ncu": 0.51, "xu_pipe_busy_ncu": 0.32, "tensor_pipe_busy_ncu": 0.13,
+                             "xu_roof_evals_per_s": xu_peak_evals, "frac_of_xu_roof": (filter_evals_per_s / xu_peak_evals) if filter_evals_per_s else None,
+                             "note": "ncu --set full of a dense launch (profiles/ncu_r2_tc5_filter.summary.txt): ~1200 CUDA-core instructions per evaluation surround 10 "
+                                     "tcgen05.mma per 128 evaluations -- the tensor cores wait for the activation math, so the fraction of tensor peak is not what limits this kernel"},
             "note": "achieved = filter evaluations x 5120 algorithmic flop / summed CUDA-event time of the filter launches; each evaluation issues 3 fp16 piece products "
                     "over K padded to 48 + 32 (15360 tensor flop)",
         }
@@ -604,9 +607,13 @@ def main():
                                                    f"{dt1:.1f} s at KNF_THREADS=1, {dtn:.1f} s at KNF_THREADS={ncpu}; scaled per ray to {W}x{H} "
                                                    "(bench.py --impl reference renders the full frame un-extrapolated)",
                                          "krays_per_s_1_thread": w * h / dt1 / 1e3, "krays_per_s_all_threads": w * h / dtn / 1e3}, **host_description())
-        print(json.dumps(line), flush=True)
+        final_line = json.dumps(line)
     if use_dist:
+        dist.barrier()
         dist.destroy_process_group()
+    if rank == 0:
+        sys.stdout.flush()
+        print(final_line, flush=True)  # after the process group is gone: the JSON line is the last thing on stdout (NCCL's INFO log comes before)
     return 0
 
 

@@ -53,7 +53,7 @@ void DevBuf::release() {
 }
 
 void Workspace::release_all() {
-  DevBuf* all[] = {&tail_cursor, &sorted_f, &tiles_f, &cell_offset_f, &tile_base_f, &req_pt2, &req_cell2, &req_rank2, &req_pt3, &req_cell3, &req_rank3, &cell_count_f, &sorted, &live2, &live3, &tile_base, &req_pt1, &req_cell1, &req_rank1, &req_pt, &req_cell, &req_rank, &perm, &tiles, &cell_count, &cell_offset, &counters, &t, &t_prev,
+  DevBuf* all[] = {&scan_part, &tail_cursor, &sorted_f, &tiles_f, &cell_offset_f, &tile_base_f, &req_pt2, &req_cell2, &req_rank2, &req_pt3, &req_cell3, &req_rank3, &cell_count_f, &sorted, &live2, &live3, &tile_base, &req_pt1, &req_cell1, &req_rank1, &req_pt, &req_cell, &req_rank, &perm, &tiles, &cell_count, &cell_offset, &counters, &t, &t_prev,
                    &d_prev, &t_conv, &d_conv, &t_hit, &steps, &phase, &hit, &live0, &live1, &hit_list,
                    &hit_count, &sdf_out, &col_v, &col_n, &col_z, &rgb, &origins, &dirs, &t_near, &t_far, &normals64,
                    &colors64, &frame_color, &frame_depth, &frame_normal, &frame_hit};
@@ -311,9 +311,24 @@ int finish_stats(Field& F, cudaStream_t st) {
   return 0;
 }
 
+// grids beyond scan_split cells: the scan runs over <= 1024 chunks of >= 4096 cells in two launches (knf_route.cuh)
+static inline void scan_chunks(const Field& F, int& chunks, int& chunk) {
+  const int n = F.geom.n_cells;
+  chunk = std::max(std::min(4096, F.scan_split > 0 ? F.scan_split : 4096), (n + kScanThreads - 1) / kScanThreads);
+  chunks = (n + chunk - 1) / chunk;
+}
+
 int launch_scan_scatter(Field& F, const RouteBuffers& R, size_t n_upper, cudaStream_t st, int* seg_cell, int* seg_start,
                         int* n_seg) {
   ProfScope prof(F, st, SPAN_ROUTE);
+  if (F.geom.n_cells > F.scan_split) {
+    int chunks, chunk;
+    scan_chunks(F, chunks, chunk);
+    KNF_TRY(F.ws.scan_part.ensure(2 * (size_t)chunks * sizeof(ScanPart)));
+    route_scan_part_kernel<<<dim3(chunks, 1), kScanThreads, 0, st>>>(R, R, F.geom.n_cells, chunk, F.ws.scan_part.as<ScanPart>());
+    route_scan_apply_kernel<<<dim3(chunks, 1), kScanThreads, 0, st>>>(R, R, F.geom.n_cells, chunk, F.ws.scan_part.as<ScanPart>(), seg_cell, seg_start, n_seg);
+    F.stats.kernel_launches += 1;
+  } else
   route_scan_kernel<<<1, kScanThreads, 0, st>>>(R, F.geom.n_cells, seg_cell, seg_start, n_seg);
   route_scatter_kernel<<<blocks_for(std::max<size_t>(n_upper, (size_t)F.geom.n_cells)), 256, 0, st>>>(R, F.geom.n_cells);
   F.stats.kernel_launches += 2;
@@ -324,6 +339,14 @@ int launch_scan_scatter(Field& F, const RouteBuffers& R, size_t n_upper, cudaStr
 // scan + scatter of the two queues of one march wavefront in two launches instead of four
 static int launch_scan_scatter2(Field& F, const RouteBuffers& Ra, const RouteBuffers& Rb, size_t n_upper, cudaStream_t st) {
   ProfScope prof(F, st, SPAN_ROUTE);
+  if (F.geom.n_cells > F.scan_split) {
+    int chunks, chunk;
+    scan_chunks(F, chunks, chunk);
+    KNF_TRY(F.ws.scan_part.ensure(2 * (size_t)chunks * sizeof(ScanPart)));
+    route_scan_part_kernel<<<dim3(chunks, 2), kScanThreads, 0, st>>>(Ra, Rb, F.geom.n_cells, chunk, F.ws.scan_part.as<ScanPart>());
+    route_scan_apply_kernel<<<dim3(chunks, 2), kScanThreads, 0, st>>>(Ra, Rb, F.geom.n_cells, chunk, F.ws.scan_part.as<ScanPart>(), nullptr, nullptr, nullptr);
+    F.stats.kernel_launches += 1;
+  } else
   route_scan2_kernel<<<2, kScanThreads, 0, st>>>(Ra, Rb, F.geom.n_cells);
   route_scatter2_kernel<<<blocks_for(std::max<size_t>(n_upper, (size_t)F.geom.n_cells)), 256, 0, st>>>(Ra, Rb, F.geom.n_cells);
   F.stats.kernel_launches += 2;

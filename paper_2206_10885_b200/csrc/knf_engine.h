@@ -50,7 +50,7 @@ struct Workspace {
   // march state
   DevBuf t, t_prev, d_prev, t_conv, d_conv, t_hit, steps, phase, hit, live0, live1;
   // shading
-  DevBuf tail_cursor;
+  DevBuf tail_cursor, scan_part;
   DevBuf hit_list, hit_count, sdf_out, col_v, col_n, col_z, rgb;
   // render-frame ray buffers
   DevBuf origins, dirs, t_near, t_far, normals64, colors64;
@@ -80,6 +80,7 @@ struct Field {
   int sparse_keep_div = 2;   // measured: (16, 4) gains 3 % on the distilled frame and loses 1.3 % on the random-init one; (32, 8) and up lose more
   int sparse_div = 8;                  // a wavefront is sparse when its exact queue holds < n / sparse_div rays (KNF_SPARSE_DIV)
   bool sparse_small_kernel = true;     // exact march: sparse wavefronts by march_small_kernel (KNF_SPARSE_SMALL=0 disables)
+  int scan_split = 65536;              // grids with more cells scan in chunks over many CTAs (two launches) instead of one CTA per queue (KNF_SCAN_SPLIT)
   int filter_grid_ctas = 6;            // CTAs per SM the tcgen05 filter's grid asks for (KNF_FILTER_GRID; fewer leaves room for the concurrent exact kernel)
   int filter_skip_cap = 1 << 20;       // cap on the certified steps taken after one evaluation (KNF_FILTER_SKIP_CAP)
   int filter_skip = 1;                 // certified (Lipschitz) skipping inside the filter: 0 off, 1 sample by sample, 2 closed-form run (cell-exit DDA + Lipschitz budget) then sample by sample; KNF_FILTER_SKIP

@@ -148,15 +148,16 @@ __device__ __forceinline__ void block_scan3(int& a, int& b, int& c, int* s_warp 
   c = pc + ic - c;
 }
 
-// One CTA: per-cell request offsets and per-cell tile bases (the tile descriptors themselves are
-// written in parallel by route_scatter_kernel).  Optionally emits grid.route's occupied segments
-// (cells ascending, starts).  Re-zeroes the cell counters and the next pass's counters.
-__device__ __forceinline__ void route_scan_body(const RouteBuffers& R, int n_cells, int* __restrict__ seg_cell, int* __restrict__ seg_start,
-                                                int* __restrict__ n_seg_out, int* s_warp) {
+// Per-cell request offsets and per-cell tile bases of cells [c_begin, c_end) given the totals of all cells before them
+// (the tile descriptors themselves are written in parallel by route_scatter_kernel).  Optionally emits grid.route's
+// occupied segments (cells ascending, starts).  Re-zeroes the cell counters; the chunk that ends at n_cells also writes
+// the totals and resets the next pass's counters.
+__device__ __forceinline__ void route_scan_chunk(const RouteBuffers& R, int c_begin, int c_end, int n_cells, int base_p, int base_t, int base_g,
+                                                 int* __restrict__ seg_cell, int* __restrict__ seg_start, int* __restrict__ n_seg_out, int* s_warp) {
   const int tid = threadIdx.x;
-  const int per = (n_cells + kScanThreads - 1) / kScanThreads;
-  const int c0 = min(tid * per, n_cells);
-  const int c1 = min(c0 + per, n_cells);
+  const int per = (c_end - c_begin + kScanThreads - 1) / kScanThreads;
+  const int c0 = min(c_begin + tid * per, c_end);
+  const int c1 = min(c0 + per, c_end);
   int pts = 0, tl = 0, sg = 0;
   for (int c = c0; c < c1; c++) {
     int k = R.cell_count[c];
@@ -166,6 +167,9 @@ __device__ __forceinline__ void route_scan_body(const RouteBuffers& R, int n_cel
   }
   int p_base = pts, t_base = tl, g_base = sg, tot_p, tot_t, tot_g;
   block_scan3(p_base, t_base, g_base, s_warp, tot_p, tot_t, tot_g);
+  p_base += base_p;
+  t_base += base_t;
+  g_base += base_g;
   for (int c = c0; c < c1; c++) {
     int k = R.cell_count[c];
     R.cell_offset[c] = p_base;
@@ -179,7 +183,10 @@ __device__ __forceinline__ void route_scan_body(const RouteBuffers& R, int n_cel
     t_base += tiles_of_cell(k, R.small_tiles);
     p_base += k;
   }
-  if (tid == kScanThreads - 1) {
+  if (c_end == n_cells && tid == kScanThreads - 1) {
+    tot_p += base_p;
+    tot_t += base_t;
+    tot_g += base_g;
     R.cell_offset[n_cells] = tot_p;
     R.tile_base[n_cells] = tot_t;
     R.ctr->n_tiles = tot_t;
@@ -194,16 +201,58 @@ __device__ __forceinline__ void route_scan_body(const RouteBuffers& R, int n_cel
     }
   }
 }
+// One CTA per queue: the whole grid in one chunk (up to a few 10^4 cells).
 static __global__ void __launch_bounds__(kScanThreads) route_scan_kernel(RouteBuffers R, int n_cells, int* __restrict__ seg_cell,
                                                                   int* __restrict__ seg_start,
                                                                   int* __restrict__ n_seg_out) {
   __shared__ int s_warp[96];
-  route_scan_body(R, n_cells, seg_cell, seg_start, n_seg_out, s_warp);
+  route_scan_chunk(R, 0, n_cells, n_cells, 0, 0, 0, seg_cell, seg_start, n_seg_out, s_warp);
 }
 // The two queues of a march wavefront (filter, exact) in one launch: CTA 0 scans the first, CTA 1 the second.
 static __global__ void __launch_bounds__(kScanThreads) route_scan2_kernel(RouteBuffers Ra, RouteBuffers Rb, int n_cells) {
   __shared__ int s_warp[96];
-  route_scan_body(blockIdx.x == 0 ? Ra : Rb, n_cells, nullptr, nullptr, nullptr, s_warp);
+  route_scan_chunk(blockIdx.x == 0 ? Ra : Rb, 0, n_cells, n_cells, 0, 0, 0, nullptr, nullptr, nullptr, s_warp);
+}
+
+// ---- large grids: the scan in two launches over gridDim.x chunks of `chunk` cells (gridDim.y = queues) -------------------
+// part: per queue and chunk the totals (requests, tiles, occupied cells); apply: every CTA sums the parts before its chunk
+// (<= 1024 chunks: one block-wide scan) and runs the chunk scan from those bases.
+struct ScanPart {
+  int p, t, g, pad;
+};
+static __global__ void __launch_bounds__(kScanThreads) route_scan_part_kernel(RouteBuffers Ra, RouteBuffers Rb, int n_cells, int chunk,
+                                                                       ScanPart* __restrict__ part) {
+  __shared__ int s_warp[96];
+  const RouteBuffers& R = blockIdx.y == 0 ? Ra : Rb;
+  const int c_begin = min((int)blockIdx.x * chunk, n_cells), c_end = min(c_begin + chunk, n_cells);
+  const int per = (c_end - c_begin + kScanThreads - 1) / kScanThreads;
+  const int c0 = min(c_begin + (int)threadIdx.x * per, c_end), c1 = min(c0 + per, c_end);
+  int pts = 0, tl = 0, sg = 0;
+  for (int c = c0; c < c1; c++) {
+    int k = R.cell_count[c];
+    pts += k;
+    tl += tiles_of_cell(k, R.small_tiles);
+    sg += (k > 0);
+  }
+  int tp, tt, tg;
+  block_scan3(pts, tl, sg, s_warp, tp, tt, tg);
+  if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = ScanPart{tp, tt, tg, 0};
+}
+static __global__ void __launch_bounds__(kScanThreads) route_scan_apply_kernel(RouteBuffers Ra, RouteBuffers Rb, int n_cells, int chunk,
+                                                                        const ScanPart* __restrict__ part, int* __restrict__ seg_cell,
+                                                                        int* __restrict__ seg_start, int* __restrict__ n_seg_out) {
+  __shared__ int s_warp[96];
+  const RouteBuffers& R = blockIdx.y == 0 ? Ra : Rb;
+  const ScanPart* mine = part + blockIdx.y * gridDim.x;
+  int a = 0, b = 0, c = 0, base_p, base_t, base_g;
+  if ((int)threadIdx.x < (int)blockIdx.x) {
+    const ScanPart v = mine[threadIdx.x];
+    a = v.p; b = v.t; c = v.g;
+  }
+  block_scan3(a, b, c, s_warp, base_p, base_t, base_g);  // totals over the chunks before this one
+  __syncthreads();                                        // s_warp is reused by the chunk scan
+  const int c_begin = min((int)blockIdx.x * chunk, n_cells), c_end = min(c_begin + chunk, n_cells);
+  route_scan_chunk(R, c_begin, c_end, n_cells, base_p, base_t, base_g, seg_cell, seg_start, n_seg_out, s_warp);
 }
 
 // perm[offset[cell] + rank] = request slot, and (in the same launch) the tile descriptors of every cell.

@@ -332,3 +332,29 @@ def test_analytic_gradient(G, distilled_field, distilled_oracle):
     # ragged / empty
     assert G.grad_analytic(distilled_field, np.zeros((0, 3), np.float32)).shape == (0, 3)
     assert G.grad_analytic(distilled_field, pts[:1]).shape == (1, 3)
+
+
+def test_chunked_scan_equals_single_cta_scan(G, monkeypatch):
+    """Grids beyond 65 536 cells scan their per-cell counts in chunks over many CTAs (route_scan_part / _apply); forcing
+    that path on a 16^3 grid (KNF_SCAN_SPLIT, read when a handle is created) must reproduce the single-CTA scan: same
+    routing segments, bit-identical queries and frames."""
+    import copy
+
+    from paper_2206_10885_b200 import cameras, surface
+
+    field = G.field_init(G.GridConfig(resolution=16), seed=3)
+    pts = np.random.default_rng(2).uniform(-1.05, 1.05, size=(300_000, 3)).astype(np.float32)
+    pose = cameras.look_at_pose((0.3, 0.2, 2.5), (0, 0, 0), (0, 1, 0), np.deg2rad(40), 160, 120)
+    ref_route = G.route(field, pts[:50_000])
+    ref_q = G.sdf_query(field, pts)
+    ref_f = surface.render_frame(surface.FieldSurface(field), pose)
+    monkeypatch.setenv("KNF_SCAN_SPLIT", "64")
+    chunked = copy.deepcopy(field)  # a new object -> a new device handle, created under the environment variable
+    r = G.route(chunked, pts[:50_000])
+    assert np.array_equal(r.cells, ref_route.cells) and np.array_equal(r.starts, ref_route.starts) and np.array_equal(r.ends, ref_route.ends)
+    assert np.array_equal(np.sort(r.order), np.arange(50_000))
+    q = G.sdf_query(chunked, pts)
+    assert np.array_equal(q.value, ref_q.value) and np.array_equal(q.features, ref_q.features)
+    f = surface.render_frame(surface.FieldSurface(chunked), pose)
+    for k in ("color", "depth", "normal", "hit"):
+        assert np.array_equal(getattr(f, k), getattr(ref_f, k)), k
