@@ -54,7 +54,11 @@ constexpr int kTilePts = kWarpPts;
 #ifndef KNF_CTAS_PER_SM
 #define KNF_CTAS_PER_SM 8
 #endif
-constexpr int kWarpCtasPerSm = KNF_CTAS_PER_SM;  // 21.9 KB of shared memory each
+constexpr int kWarpCtasPerSm = KNF_CTAS_PER_SM;  // march_warp_kernel: 21.9 KB of shared memory each (192 registers: 8 is the measured optimum)
+#ifndef KNF_FWD_CTAS_PER_SM
+#define KNF_FWD_CTAS_PER_SM 10
+#endif
+constexpr int kFwdCtasPerSm = KNF_FWD_CTAS_PER_SM;  // mlp_warp_kernel (batched forward, 125 registers): 10 fit the shared memory; 16.8 M points 3.76 -> 4.19 Gq/s
 
 struct GridGeom {
   int resolution;

@@ -387,7 +387,7 @@ int launch_sdf_mlp(Field& F, const RouteBuffers& R, size_t n_upper, float* out_f
     sdf_mma_kernel<2><<<mlp_grid(F, n_upper, kMmaCtasPerSm), 32, sizeof(MmaSmemT<2>), st>>>(P);
   } else {
     mlp_warp_kernel<kSdfIn, kSdfOut, kSdfOutPad, ACT_SOFTPLUS, false>
-        <<<mlp_grid(F, n_upper), 32, sizeof(SdfKernelSmem), st>>>(P);
+        <<<mlp_grid(F, n_upper, kFwdCtasPerSm), 32, sizeof(SdfKernelSmem), st>>>(P);
   }
   F.stats.kernel_launches += 1;
   KNF_CUDA(cudaGetLastError());
@@ -408,7 +408,7 @@ int launch_col_mlp(Field& F, const RouteBuffers& R, size_t n_upper, const float*
   P.out_full = rgb;
   ProfScope prof(F, st, SPAN_COLOR_MLP);
   mlp_warp_kernel<kColIn, kColOut, kColOutPad, ACT_RELU, true>
-      <<<mlp_grid(F, n_upper), 32, sizeof(ColKernelSmem), st>>>(P);
+      <<<mlp_grid(F, n_upper, kFwdCtasPerSm), 32, sizeof(ColKernelSmem), st>>>(P);
   F.stats.kernel_launches += 1;
   KNF_CUDA(cudaGetLastError());
   return 0;

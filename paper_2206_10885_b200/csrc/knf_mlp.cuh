@@ -356,7 +356,7 @@ __device__ __forceinline__ int next_tile(RouteCounters* ctr, int lane) {
 // Batched-forward kernel (grid.sdf_query / color_query, shading probes): ONE WARP per CTA, each
 // warp a persistent worker that pulls 64-request tiles from the routing pass's tile list.
 template <int K1, int N3, int N3P, int HIDDEN_ACT, bool IS_COLOR>
-static __global__ void __launch_bounds__(32, kWarpCtasPerSm) mlp_warp_kernel(MlpParams P) {
+static __global__ void __launch_bounds__(32, kFwdCtasPerSm) mlp_warp_kernel(MlpParams P) {
   using Blob = BlobLayout<K1, N3P>;
   using Smem = MlpSmem<K1, N3P>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
