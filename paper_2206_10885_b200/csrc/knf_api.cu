@@ -498,6 +498,7 @@ int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
   if (const char* env = std::getenv("KNF_SPARSE_DIV")) F.sparse_div = std::max(1, std::atoi(env));
   if (const char* env = std::getenv("KNF_SPARSE_INNER")) F.sparse_max_inner = std::max(1, std::atoi(env));
   if (const char* env = std::getenv("KNF_SPARSE_KEEP")) F.sparse_keep_div = std::max(1, std::atoi(env));
+  if (const char* env = std::getenv("KNF_EXACT_MID")) F.exact_mid = std::atoi(env) != 0;
   if (const char* env = std::getenv("KNF_SCAN_SPLIT")) F.scan_split = std::max(64, std::atoi(env));
   if (const char* env = std::getenv("KNF_FILTER_GRID")) F.filter_grid_ctas = std::max(1, std::atoi(env));
   if (const char* env = std::getenv("KNF_FILTER_SKIP_CAP")) F.filter_skip_cap = std::max(0, std::atoi(env));

@@ -217,6 +217,8 @@ int begin_call(Field& F, cudaStream_t st) {
     KNF_CUDA(cudaFuncSetAttribute(march_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sizeof(SdfKernelSmem)));
     KNF_CUDA(cudaFuncSetAttribute(march_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SdfSmallSmem)));
+    KNF_CUDA(cudaFuncSetAttribute(march_mid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SdfMidSmem)));
+    KNF_CUDA(cudaFuncSetAttribute(march_mid_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     KNF_CUDA(cudaFuncSetAttribute(march_mma_kernel<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaMarchSmemT<3>)));
     KNF_CUDA(cudaFuncSetAttribute(sdf_mma_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaSmemT<3>)));
     KNF_CUDA(cudaFuncSetAttribute(march_mma_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(MmaMarchSmemT<2>)));
@@ -534,7 +536,8 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     R.sorted = W.sorted.as<float4>();
     R.live = M.live[cur];
     const bool small_only = exact_mode && exact_sparse && F.sparse_small_kernel;
-    R.small_tiles = small_only ? 2 : 0;  // dense wavefronts: 64-request tiles for march_warp_kernel; sparse: <= 16 for march_small_kernel
+    const bool mid = exact_mode && !small_only && F.exact_mid;
+    R.small_tiles = small_only ? 2 : (mid ? 4 : 0);  // dense wavefronts: <= 32-request tiles for march_mid_kernel (or 64 for march_warp_kernel); sparse: <= 16 for march_small_kernel
     if (filter_pass) KNF_TRY(launch_scan_scatter2(F, Rf, R, live_upper, st));
     else KNF_TRY(launch_scan_scatter(F, R, live_upper, st));
     cudaStream_t st_exact = st;
@@ -590,6 +593,8 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
         A.max_inner = F.sparse_max_inner;
         A.keep_div = F.sparse_keep_div;
         march_small_kernel<<<mlp_grid(F, live_upper, kSmallCtasPerSm), 32, sizeof(SdfSmallSmem), st_exact>>>(A);
+      } else if (mid) {
+        march_mid_kernel<<<mlp_grid(F, live_upper, kMidCtasPerSm), 32, sizeof(SdfMidSmem), st_exact>>>(A);
       } else {
         march_warp_kernel<<<mlp_grid(F, live_upper), 32, sizeof(SdfKernelSmem), st_exact>>>(A);
       }

@@ -80,6 +80,7 @@ struct Field {
   int sparse_keep_div = 2;   // measured: (16, 4) gains 3 % on the distilled frame and loses 1.3 % on the random-init one; (32, 8) and up lose more
   int sparse_div = 8;                  // a wavefront is sparse when its exact queue holds < n / sparse_div rays (KNF_SPARSE_DIV)
   bool sparse_small_kernel = true;     // exact march: sparse wavefronts by march_small_kernel (KNF_SPARSE_SMALL=0 disables)
+  bool exact_mid = true;               // dense exact wavefronts by march_mid_kernel (32-request tiles, 13 CTAs per SM) instead of march_warp_kernel (KNF_EXACT_MID=0)
   int scan_split = 65536;              // grids with more cells scan in chunks over many CTAs (two launches) instead of one CTA per queue (KNF_SCAN_SPLIT)
   int filter_grid_ctas = 6;            // CTAs per SM the tcgen05 filter's grid asks for (KNF_FILTER_GRID; fewer leaves room for the concurrent exact kernel)
   int filter_skip_cap = 1 << 20;       // cap on the certified steps taken after one evaluation (KNF_FILTER_SKIP_CAP)

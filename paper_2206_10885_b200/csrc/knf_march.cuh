@@ -54,15 +54,18 @@ __device__ __forceinline__ void march_emit(const RouteBuffers& Q, int* live, boo
   route_emit_cell(Q, emit, slot, x, y, z, cell);
 }
 
-// One tile visit of the exact kernel.  SMALL = false: up to 64 rays, two per lane (panel columns 2 lane, 2 lane + 1);
-// SMALL = true: up to 16 rays, one in each of lanes 0..15 (panel column = lane), evaluated by the 4 x 4 register
-// tiles of knf_mlp.cuh -- a quarter of the work for the sparse tiles that dominate once the decision filter has
-// taken the crawling rays away.
-template <bool SMALL, class SmemT, int PLD>
+// One tile visit of the exact kernel.  PTS = 64: up to 64 rays, two per lane (panel columns 2 lane, 2 lane + 1), 8 x 8
+// register tiles; PTS = 32 / 16: one ray per lane (panel column = lane; lanes 0..15 for 16), evaluated by the 4 x 8 /
+// 4 x 4 register tiles of knf_mlp.cuh -- the mid shape trades register-tile size for resident warps in dense wavefronts,
+// the small one is a quarter of the work for the sparse tiles that dominate once the decision filter has taken the
+// crawling rays away.  Same chains, same bits in every shape.
+template <int PTS, class SmemT, int PLD>
 __device__ __forceinline__ void march_exact_tile(const MarchTileArgs& A, SmemT& S, const Tile& tile, int lane,
                                                  uint32_t& parity, unsigned long long& evals, unsigned long long& slots) {
   using Blob = SdfBlob;
+  constexpr bool SMALL = PTS < 64;  // one ray per lane
   static_assert(SMALL || PLD == kPanelLd, "the 64-point path needs the full panel");
+  static_assert(PTS == 64 || PTS == 32 || PTS == 16, "tile shapes: 64, 32 or 16 requests");
   constexpr int NQ = SMALL ? 1 : 2;
   const MlpParams& P = A.P;
   float* X = S.x;
@@ -85,7 +88,7 @@ __device__ __forceinline__ void march_exact_tile(const MarchTileArgs& A, SmemT& 
   }
   if (PLD == kPanelLd) {
     zero_pad_rows<kSdfIn>(X, lane);
-  } else if (lane < kSmallTilePts) {
+  } else if (lane < PTS) {
 #pragma unroll
     for (int r = kSdfIn; r < pad_k(kSdfIn); r++) X[r * PLD + lane] = 0.f;
   }
@@ -108,7 +111,7 @@ __device__ __forceinline__ void march_exact_tile(const MarchTileArgs& A, SmemT& 
 
   for (int inner = 0;; inner++) {
     if (SMALL) {
-      if (lane < kSmallTilePts) encode_into<kSdfFreqs, PLD>(X, 0, lane, px[0], py[0], pz[0]);
+      if (lane < PTS) encode_into<kSdfFreqs, PLD>(X, 0, lane, px[0], py[0], pz[0]);
     } else {
 #pragma unroll
       for (int q = 0; q < NQ; q++) encode_into<kSdfFreqs>(X, 0, col[q], px[q], py[q], pz[q]);
@@ -120,8 +123,9 @@ __device__ __forceinline__ void march_exact_tile(const MarchTileArgs& A, SmemT& 
     }
     float dist[NQ];
     if (SMALL) {
-      hidden_layers_small<kSdfIn, kSdfOutPad, ACT_SOFTPLUS, PLD>(X, S.w, lane);
-      dist[0] = lane < kSmallTilePts ? output_distance_col<kSdfOutPad, PLD>(X, S.w + Blob::w3, S.w + Blob::b3, lane) : 0.0f;
+      if (PTS == 32) hidden_layers_mid<kSdfIn, kSdfOutPad, ACT_SOFTPLUS, PLD>(X, S.w, lane);
+      else hidden_layers_small<kSdfIn, kSdfOutPad, ACT_SOFTPLUS, PLD>(X, S.w, lane);
+      dist[0] = lane < PTS ? output_distance_col<kSdfOutPad, PLD>(X, S.w + Blob::w3, S.w + Blob::b3, lane) : 0.0f;
     } else if (PLD == kPanelLd) {
       hidden_layers<kSdfIn, kSdfOutPad, ACT_SOFTPLUS>(X, S.w, lane);
       const float2 d2 = output_distance<kSdfOutPad>(X, S.w + Blob::w3, S.w + Blob::b3, lane);
@@ -129,7 +133,7 @@ __device__ __forceinline__ void march_exact_tile(const MarchTileArgs& A, SmemT& 
       dist[NQ - 1] = d2.y;
     }
     evals += (lane == 0) ? (unsigned long long)n_active : 0ull;
-    slots += SMALL ? kSmallTilePts : kWarpPts;
+    slots += PTS;
 
     // ---- the march step for the lane's rays -----------------------------------------------------------
     int code[NQ], cell[NQ];
@@ -195,10 +199,10 @@ static __global__ void __launch_bounds__(32, kWarpCtasPerSm) march_warp_kernel(M
     const Tile tile = P.tiles[t];
     fetch_weights<Blob>(S.w, P.blobs, tile.cell, &S.bar, lane);
 #ifdef KNF_MIXED_TILE_KERNEL
-    if (tile.count <= kSmallTilePts) march_exact_tile<true, Smem, kPanelLd>(A, S, tile, lane, parity, evals, slots);
+    if (tile.count <= kSmallTilePts) march_exact_tile<16, Smem, kPanelLd>(A, S, tile, lane, parity, evals, slots);
     else
 #endif
-      march_exact_tile<false, Smem, kPanelLd>(A, S, tile, lane, parity, evals, slots);  // one tile shape per kernel: half the instruction footprint
+      march_exact_tile<64, Smem, kPanelLd>(A, S, tile, lane, parity, evals, slots);  // one tile shape per kernel: half the instruction footprint
     __syncwarp();  // every lane is done reading S.w and the panel before the next tile overwrites them
   }
   if (lane == 0 && evals && A.eval_counter) {
@@ -233,7 +237,41 @@ static __global__ void __launch_bounds__(32, kSmallCtasPerSm) march_small_kernel
     if (t >= n_tiles) break;
     const Tile tile = P.tiles[t];
     fetch_weights<Blob>(S.w, P.blobs, tile.cell, &S.bar, lane);
-    march_exact_tile<true, SdfSmallSmem, kSmallPanelLd>(A, S, tile, lane, parity, evals, slots);
+    march_exact_tile<16, SdfSmallSmem, kSmallPanelLd>(A, S, tile, lane, parity, evals, slots);
+    __syncwarp();
+  }
+  if (lane == 0 && evals && A.eval_counter) {
+    atomicAdd(A.eval_counter, evals);
+    atomicAdd(A.eval_counter + 2, slots);
+  }
+}
+
+// The exact kernel for DENSE wavefronts in the mid shape: tiles of <= 32 requests (RouteBuffers::small_tiles = 4), 4 x 8
+// register tiles, 16.8 KB of shared memory, 13 one-warp CTAs per SM (march_warp_kernel: 192 registers, 8 per SM).
+#ifndef KNF_MID_CTAS_PER_SM
+#define KNF_MID_CTAS_PER_SM 13
+#endif
+constexpr int kMidCtasPerSm = KNF_MID_CTAS_PER_SM;
+static __global__ void __launch_bounds__(32, kMidCtasPerSm) march_mid_kernel(MarchTileArgs A) {
+  using Blob = SdfBlob;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SdfMidSmem& S = *reinterpret_cast<SdfMidSmem*>(smem_raw);
+  const int lane = threadIdx.x;
+  if (lane == 0) {
+    mbar_init(&S.bar, 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  const MlpParams& P = A.P;
+  const int n_tiles = P.ctr->n_tiles;
+  uint32_t parity = 0;
+  unsigned long long evals = 0, slots = 0;
+  for (;;) {
+    const int t = next_tile(P.ctr, lane);
+    if (t >= n_tiles) break;
+    const Tile tile = P.tiles[t];
+    fetch_weights<Blob>(S.w, P.blobs, tile.cell, &S.bar, lane);
+    march_exact_tile<32, SdfMidSmem, kMidPanelLd>(A, S, tile, lane, parity, evals, slots);
     __syncwarp();
   }
   if (lane == 0 && evals && A.eval_counter) {

@@ -291,6 +291,96 @@ __device__ __forceinline__ void hidden_layers_small(float* __restrict__ X, const
   }
 }
 
+
+// ---- the same arithmetic for a MID tile (<= 32 points, panel column = lane) ----------------------------------------
+// Dense wavefronts of the exact march: a lane accumulates 4 points x 8 neurons (8 point groups x 4 neuron groups), 32
+// accumulator registers instead of the 128 of the 8 x 8 tiles, so 13 one-warp CTAs share an SM instead of 8.  Every
+// output is still the k-ordered FMA chain from zero followed by the rounded bias add: same bits as the other shapes.
+constexpr int kMidTilePts = 32;
+constexpr int kMidPanelLd = kMidTilePts + 4;  // 36
+
+template <int K, int PLD>
+__device__ __forceinline__ void layer_4x8(const float* __restrict__ In, const float* __restrict__ Wt, int pg, int ng, float2 (&acc)[2][8]) {
+  static_assert(K % 8 == 0, "pad K to a multiple of 8");
+#pragma unroll
+  for (int i = 0; i < 2; i++)
+#pragma unroll
+    for (int j = 0; j < 8; j++) acc[i][j] = make_float2(0.0f, 0.0f);
+  const float* xp = In + pg * 4;
+  const float* wp = Wt + ng * 8;
+#pragma unroll 1
+  for (int k0 = 0; k0 < K; k0 += 8) {
+#pragma unroll
+    for (int kk = 0; kk < 8; kk++) {
+      const float4 x = *reinterpret_cast<const float4*>(xp + (k0 + kk) * PLD);
+      const float4 wa = *reinterpret_cast<const float4*>(wp + (k0 + kk) * kHidden);
+      const float4 wb = *reinterpret_cast<const float4*>(wp + (k0 + kk) * kHidden + 4);
+      const float2 x01 = make_float2(x.x, x.y), x23 = make_float2(x.z, x.w);
+      const float ws[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        acc[0][j] = __ffma2_rn(x01, splat(ws[j]), acc[0][j]);
+        acc[1][j] = __ffma2_rn(x23, splat(ws[j]), acc[1][j]);
+      }
+    }
+    asm volatile("" ::: "memory");  // (as in layer_8x8: no operand prefetch across the back-edge)
+  }
+}
+
+template <int ACT, int PLD>
+__device__ __forceinline__ void store_hidden_mid(float2 (&acc)[2][8], const float* __restrict__ bias, float* __restrict__ Out, int pg, int ng) {
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    const int neuron = ng * 8 + j;
+    const float2 b = splat(bias[neuron]);
+    float2 v0 = __fadd2_rn(acc[0][j], b), v1 = __fadd2_rn(acc[1][j], b);
+    if (ACT == ACT_RELU) {
+      v0 = make_float2(fmaxf(v0.x, 0.0f), fmaxf(v0.y, 0.0f));
+      v1 = make_float2(fmaxf(v1.x, 0.0f), fmaxf(v1.y, 0.0f));
+    }
+    *reinterpret_cast<float4*>(Out + neuron * PLD + pg * 4) = make_float4(v0.x, v0.y, v1.x, v1.y);
+  }
+}
+
+// In-place softplus over panel rows 0..31, columns 0..31: lane owns columns 2 (lane & 15), +1 of rows (lane >> 4) + 2 i.
+template <int PLD>
+static __device__ __noinline__ void softplus_panel_mid(float* __restrict__ panel, int lane) {
+  float* base = panel + (lane >> 4) * PLD + 2 * (lane & 15);
+#pragma unroll 1
+  for (int i0 = 0; i0 < 16; i0 += 4) {
+    float2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) v[u] = *reinterpret_cast<float2*>(base + 2 * (i0 + u) * PLD);
+    softplus_tile<4>(v);
+#pragma unroll
+    for (int u = 0; u < 4; u++) *reinterpret_cast<float2*>(base + 2 * (i0 + u) * PLD) = v[u];
+  }
+}
+
+template <int K1, int N3P, int HIDDEN_ACT, int PLD>
+__device__ __forceinline__ void hidden_layers_mid(float* __restrict__ X, const float* __restrict__ W, int lane) {
+  using Blob = BlobLayout<K1, N3P>;
+  const int pg = lane >> 2;  // 8 point groups of 4 points
+  const int ng = lane & 3;   // 4 neuron groups of 8 neurons
+  float2 acc[2][8];
+  layer_4x8<pad_k(K1), PLD>(X, W + Blob::w1, pg, ng, acc);
+  __syncwarp();
+  store_hidden_mid<HIDDEN_ACT, PLD>(acc, W + Blob::b1, X, pg, ng);
+  __syncwarp();
+  if (HIDDEN_ACT == ACT_SOFTPLUS) {
+    softplus_panel_mid<PLD>(X, lane);
+    __syncwarp();
+  }
+  layer_4x8<kHidden, PLD>(X, W + Blob::w2, pg, ng, acc);
+  __syncwarp();
+  store_hidden_mid<HIDDEN_ACT, PLD>(acc, W + Blob::b2, X, pg, ng);
+  __syncwarp();
+  if (HIDDEN_ACT == ACT_SOFTPLUS) {
+    softplus_panel_mid<PLD>(X, lane);
+    __syncwarp();  // the output layer reads column `lane`, written by other lanes
+  }
+}
+
 // Output 0 (the distance) of the 32 -> N3 layer for panel column p (same chain as output_distance).
 template <int N3P, int PLD>
 __device__ __forceinline__ float output_distance_col(const float* __restrict__ X, const float* __restrict__ W3,
@@ -471,6 +561,15 @@ struct SmallSmem {
   alignas(16) float x[pad_k(K1) * kSmallPanelLd];
   alignas(8) uint64_t bar;
 };
+// ... and of the mid-tile kernel: a 40 x 36 panel -- 16.8 KB, 13 one-warp CTAs per SM.
+template <int K1, int N3P>
+struct MidSmem {
+  using Blob = BlobLayout<K1, N3P>;
+  alignas(16) float w[Blob::floats];
+  alignas(16) float x[pad_k(K1) * kMidPanelLd];
+  alignas(8) uint64_t bar;
+};
+using SdfMidSmem = MidSmem<kSdfIn, kSdfOutPad>;
 using SdfKernelSmem = MlpSmem<kSdfIn, kSdfOutPad>;
 using SdfSmallSmem = SmallSmem<kSdfIn, kSdfOutPad>;
 using ColKernelSmem = MlpSmem<kColIn, kColOutPad>;

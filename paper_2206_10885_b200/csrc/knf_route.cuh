@@ -34,15 +34,16 @@ struct RouteBuffers {
   float4* sorted;     // march queues: sorted position -> (point, ray id in .w): one coalesced load per tile point (nullable)
   const int* live;    // march queues: request slot -> ray id (read by scatter when `sorted` is set)
   int small_tiles;    // 1: cut the last < 49 requests of a cell into tiles of <= 16 (kernels with a small-tile path); 2: every tile <= 16;
-                      // 3: tiles of <= 128 requests, a cell's requests split evenly (knf_tc5.cuh: one request per thread of a 128-thread CTA)
+                      // 4: every tile <= 32 (march_mid_kernel); 3: tiles of <= 128 requests, a cell's requests split evenly (knf_tc5.cuh: one request per thread of a 128-thread CTA)
 };
 
 // How a cell's k requests are cut into tiles: full 64-request tiles, then the remainder r either as one tile
 // (r >= 49, or small tiles off) or as ceil(r / 16) tiles of <= 16 requests.
 constexpr int kSmallTile = 16, kSmallTileMaxRemainder = 48;
-constexpr int kBigTile = 128;
+constexpr int kBigTile = 128, kMidTile = 32;
 __device__ __forceinline__ int tiles_of_cell(int k, int small_tiles) {
   if (small_tiles == 3) return (k + kBigTile - 1) / kBigTile;
+  if (small_tiles == 4) return (k + kMidTile - 1) / kMidTile;
   if (small_tiles == 2) return (k + kSmallTile - 1) / kSmallTile;
   const int full = k / kTilePts, r = k - full * kTilePts;
   if (r == 0) return full;
@@ -292,6 +293,9 @@ __device__ __forceinline__ void route_scatter_body(const RouteBuffers& R, int n_
       const int n = (k + kBigTile - 1) / kBigTile, per = ((k + n - 1) / n + 31) & ~31;
       off = j * per;
       take = min(per, k - off);
+    } else if (R.small_tiles == 4) {
+      off = j * kMidTile;
+      take = min(kMidTile, k - off);
     } else if (R.small_tiles == 2) {
       off = j * kSmallTile;
       take = min(kSmallTile, k - off);
