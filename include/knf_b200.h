@@ -167,6 +167,17 @@ int knf_field_filter_cells_off(knf_field_t f);
  * memory; the default) or "march_mma_kernel<2, true>" (mma.sync; environment KNF_FILTER_KERNEL=mma).  For reports. */
 const char* knf_field_filter_kernel(knf_field_t f);
 
+/* Per-cell, per-axis Lipschitz bounds L_a >= sup |d d / d x_a| of the SDF network behind the decision filter's certified
+ * skipping (no reference counterpart: the reference evaluates every crawl sample, surface.py:217-223; a sample p of a ray
+ * in the cell of an evaluated sample p0 with sum_a L_a |p_a - p0_a| below the room the filter distance left has an exact
+ * distance below -eps, so the reference's step there is taken without evaluating).  `closed_form` receives the bounds the
+ * field was packed with (|w3| |W2| |W1 J_a|), `refined` the bounds after the sub-box bound propagation of
+ * csrc/knf_bounds.cuh, which this call runs if no march has triggered it yet (both n_cells * 3 floats, HOST pointers,
+ * either may be NULL); `refine_ms` (may be NULL) the device time of that refinement, 0 if it ran untimed earlier.
+ * Environment: KNF_LIP_WIDTH (target sub-box width, default 0.004; 0 keeps the closed-form bounds), KNF_LIP_FINE.
+ * KNF_E_UNSUPPORTED for a field without filter blobs. */
+int knf_field_lipschitz(knf_field_t f, float* closed_form, float* refined, float* refine_ms, void* stream);
+
 /* ---- routing: grid.py:176-213 ------------------------------------------------------------ */
 /* grid.cell_index_flat (grid.py:182-185) on fp32 points (fp64 arithmetic, bit-exact). */
 int knf_cell_index(knf_field_t f, const float* pts, int64_t n, int32_t* cell, int mem, void* stream);

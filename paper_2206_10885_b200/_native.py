@@ -133,6 +133,7 @@ _SIGNATURES = {
     "knf_field_filter_delta": [_P],
     "knf_field_filter_cells_off": [_P],
     "knf_field_filter_kernel": [_P],
+    "knf_field_lipschitz": [_P, _P, _P, _P, _P],
     "knf_cell_index": [_P, _P, _I64, _P, _I32, _P],
     "knf_cell_index_f64": [_P, _P, _I64, _P, _I32, _P],
     "knf_route": [_P, _P, _I64, _P, _P, _P, _P, _P, _I32, _P],

@@ -15,6 +15,8 @@
 #define KNF_TC5_LAYOUT_ONLY  // the blob layout, not the kernels (those are compiled in knf_engine.cu)
 #include "knf_tc5.cuh"
 #include "knf_rays.cuh"
+#define KNF_BOUNDS_LAYOUT_ONLY  // the per-cell constants, not the kernels (compiled in knf_engine.cu)
+#include "knf_bounds.cuh"
 
 using namespace knf;
 
@@ -237,7 +239,7 @@ static double filter_delta(int pieces, const float* w1, const float* b1, const f
 // has norm <= |w_raw_a| + sum_o 2^o pi sigma_max([w_sin_o,a | w_cos_o,a]).
 // Returns the three per-axis bounds L_a = |w3| |W2| |column a of W1 J|: |d(p) - d(q)| <= sum_a L_a |p_a - q_a| (triangle
 // inequality over the axes -- tighter than one constant times the Euclidean distance for rays near an axis).
-static void lipschitz_bound(const float* w1, const float* w2, const float* w3, double out[3]) {
+static void lipschitz_bound(const float* w1, const float* w2, const float* w3, double out[3], LipCellConst* cc = nullptr) {
   double n3 = 0.0;
   for (int k = 0; k < kHidden; k++) n3 += (double)w3[k] * (double)w3[k];
   n3 = std::sqrt(n3);
@@ -290,6 +292,29 @@ static void lipschitz_bound(const float* w1, const float* w2, const float* w3, d
       m += std::ldexp(3.14159265358979323846, o) * std::sqrt(lam);
     }
     out[a] = 1.001 * n3 * n2 * m + 1e-12;
+  }
+  if (cc) {  // constants of the sub-box refinement (knf_bounds.cuh), rounded up
+    cc->n3 = n3 * (1.0 + 1e-12);
+    cc->n2 = n2 * 1.0001;
+    double fro = 0.0;
+    for (int i = 0; i < kHidden * kHidden; i++) fro += (double)w2[i] * (double)w2[i];
+    cc->n2f = std::sqrt(fro) * (1.0 + 1e-12);
+    for (int a = 0; a < 3; a++) {
+      double k3 = 0.0;
+      for (int o = 0; o < kSdfFreqs; o++) {
+        double aa = 0.0, bb = 0.0, ab = 0.0;
+        for (int n = 0; n < kHidden; n++) {
+          const double sn = w1[n * kSdfIn + 3 + 6 * o + a], cs = w1[n * kSdfIn + 3 + 6 * o + 3 + a];
+          aa += sn * sn;
+          bb += cs * cs;
+          ab += sn * cs;
+        }
+        const double lam = 0.5 * (aa + bb) + std::sqrt(0.25 * (aa - bb) * (aa - bb) + ab * ab);
+        const double f = std::ldexp(3.14159265358979323846, o);
+        k3 += f * f * f * std::sqrt(lam);
+      }
+      cc->k3[a] = k3 * (1.0 + 1e-9);
+    }
   }
 }
 
@@ -361,7 +386,9 @@ void pack_sdf_mma(int n_cells, const float* const w[3], const float* const b[3],
 // its bias as the weight of the constant-1 feature k = 39.  Then the fp32 constants, the filter bound delta and the Lipschitz
 // bounds (same analysis as pack_sdf_mma<2>: same operand pieces, same number of tensor-core accumulation steps per output).
 void pack_sdf_tc5(int n_cells, const float* const w[3], const float* const b[3], double x_raw, std::vector<uint8_t>& out,
-                  double* delta_max, int* cells_off) {
+                  double* delta_max, int* cells_off, std::vector<LipCellConst>* lip_consts = nullptr, std::vector<float>* lip_out = nullptr) {
+  if (lip_consts) lip_consts->assign((size_t)n_cells, LipCellConst{});
+  if (lip_out) lip_out->assign((size_t)n_cells * 3, 0.0f);
   out.assign((size_t)n_cells * Tc5Blob::bytes, 0);
   for (int c = 0; c < n_cells; c++) {
     uint8_t* blob = out.data() + (size_t)c * Tc5Blob::bytes;
@@ -400,8 +427,11 @@ void pack_sdf_tc5(int n_cells, const float* const w[3], const float* const b[3],
     if (delta_max && std::isfinite(delta_f)) *delta_max = std::max(*delta_max, (double)delta_f);
     if (cells_off && !std::isfinite(delta_f)) *cells_off += 1;
     double lip[3];
-    lipschitz_bound(w1, w2, w3, lip);
-    for (int a = 0; a < 3; a++) f[Tc5Blob::f_lip + a] = std::nextafter((float)lip[a], INFINITY);
+    lipschitz_bound(w1, w2, w3, lip, lip_consts ? &(*lip_consts)[c] : nullptr);
+    for (int a = 0; a < 3; a++) {
+      f[Tc5Blob::f_lip + a] = std::nextafter((float)lip[a], INFINITY);
+      if (lip_out) (*lip_out)[(size_t)c * 3 + a] = f[Tc5Blob::f_lip + a];
+    }
   }
 }
 
@@ -476,7 +506,13 @@ int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
       std::vector<uint8_t> tc5;
       double dmax = 0.0;
       int off = 0;
-      pack_sdf_tc5(F.geom.n_cells, d->sdf_w, d->sdf_b, x_raw, tc5, &dmax, &off);
+      std::vector<LipCellConst> lipc;
+      pack_sdf_tc5(F.geom.n_cells, d->sdf_w, d->sdf_b, x_raw, tc5, &dmax, &off, &lipc, &F.lip_closed_form);
+      KNF_CUDA(cudaMalloc(&F.lip_consts, lipc.size() * sizeof(LipCellConst)));
+      KNF_CUDA(cudaMemcpy(F.lip_consts, lipc.data(), lipc.size() * sizeof(LipCellConst), cudaMemcpyHostToDevice));
+      KNF_CUDA(cudaMalloc(&F.lip_cur, F.lip_closed_form.size() * sizeof(float)));
+      KNF_CUDA(cudaMemcpy(F.lip_cur, F.lip_closed_form.data(), F.lip_closed_form.size() * sizeof(float), cudaMemcpyHostToDevice));
+      KNF_CUDA(cudaMalloc(&F.lip_max, F.lip_closed_form.size() * sizeof(unsigned long long)));
       F.filter_delta_max = std::max(F.filter_delta_max, dmax);  // crawl_below must cover whichever filter kernel runs
       KNF_CUDA(cudaMalloc(&F.sdf_tc5_blobs, tc5.size()));
       KNF_CUDA(cudaMemcpy(F.sdf_tc5_blobs, tc5.data(), tc5.size(), cudaMemcpyHostToDevice));
@@ -491,6 +527,8 @@ int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
     else return fail(KNF_E_INVALID, "KNF_PRECISION must be fp32_chain, tensor_bf16x3 or tensor_fp16x2");
   }
   if (F.precision == KNF_PRECISION_TENSOR_FP16X2 && (!F.fp16_ok || F.filter_cells_off > 0)) F.precision = KNF_PRECISION_TENSOR_BF16X3;  // bf16 pieces keep fp32's range
+  if (const char* env = std::getenv("KNF_LIP_WIDTH")) F.lip_width = std::max(0.0, std::atof(env));
+  if (const char* env = std::getenv("KNF_LIP_FINE")) F.lip_fine = std::max(1, std::min(kLipMaxFine, std::atoi(env)));
   if (const char* env = std::getenv("KNF_FILTER_SKIP")) F.filter_skip = std::max(0, std::min(2, std::atoi(env)));
   if (const char* env = std::getenv("KNF_SPARSE_SMALL")) F.sparse_small_kernel = std::atoi(env) != 0;
   if (const char* env = std::getenv("KNF_FILTER_KEEP")) F.filter_keep_div = std::max(1, std::atoi(env));
@@ -795,6 +833,9 @@ int knf_field_destroy(knf_field_t f) {
     if (f->f.sdf_mma_blobs) cudaFree(f->f.sdf_mma_blobs);
     if (f->f.sdf_mmah_blobs) cudaFree(f->f.sdf_mmah_blobs);
     if (f->f.sdf_tc5_blobs) cudaFree(f->f.sdf_tc5_blobs);
+    if (f->f.lip_consts) cudaFree(f->f.lip_consts);
+    if (f->f.lip_cur) cudaFree(f->f.lip_cur);
+    if (f->f.lip_max) cudaFree(f->f.lip_max);
   }
   delete f;
   if (prev_device >= 0) cudaSetDevice(prev_device);
@@ -885,6 +926,36 @@ const char* knf_field_filter_kernel(knf_field_t f) {
 int knf_field_filter_cells_off(knf_field_t f) {
   KNF_TRY(check_field(f));
   return f->f.fp16_ok ? f->f.filter_cells_off : f->f.geom.n_cells;
+}
+
+int knf_field_lipschitz(knf_field_t f, float* closed_form, float* refined, float* refine_ms, void* stream) {
+  KNF_TRY(check_field(f));
+  Field& F = f->f;
+  if (!F.lip_cur) return fail(KNF_E_UNSUPPORTED, "this field has no decision-filter blobs (weights beyond the fp16 range): no Lipschitz bounds");
+  std::lock_guard<std::mutex> lk(F.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  CallScope call_scope(F, st);
+  KNF_TRY(call_scope.rc);
+  const size_t n = (size_t)F.geom.n_cells * 3;
+  if (closed_form) std::memcpy(closed_form, F.lip_closed_form.data(), n * sizeof(float));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  const bool timed = refine_ms && !F.lip_refined;
+  if (timed) {
+    KNF_CUDA(cudaEventCreate(&e0));
+    KNF_CUDA(cudaEventCreate(&e1));
+    KNF_CUDA(cudaEventRecord(e0, st));
+  }
+  KNF_TRY(ensure_lipschitz_refined(F, st));
+  if (timed) KNF_CUDA(cudaEventRecord(e1, st));
+  if (refined) KNF_CUDA(cudaMemcpyAsync(refined, F.lip_cur, n * sizeof(float), cudaMemcpyDeviceToHost, st));
+  KNF_CUDA(cudaStreamSynchronize(st));
+  if (timed) {
+    KNF_CUDA(cudaEventElapsedTime(&F.lip_ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  if (refine_ms) *refine_ms = F.lip_ms;
+  return 0;
 }
 
 // ---- routing ---------------------------------------------------------------------------------------

@@ -60,6 +60,11 @@ constexpr int kWarpCtasPerSm = KNF_CTAS_PER_SM;  // march_warp_kernel: 21.9 KB o
 #endif
 constexpr int kFwdCtasPerSm = KNF_FWD_CTAS_PER_SM;  // mlp_warp_kernel (batched forward, 125 registers): 10 fit the shared memory; 16.8 M points 3.76 -> 4.19 Gq/s
 
+// Certified skipping (decision filter) measures |p - p0| against per-cell Lipschitz bounds that hold on the cell box extended
+// by a small margin (knf_bounds.cuh); a filter kernel only skips from an evaluated sample p0 that lies within kLipSlack x the
+// cell extent of the cell box (samples routed from outside the grid are clamped into boundary cells and fail this test).
+constexpr float kLipSlack = 1.0e-5f;
+
 struct GridGeom {
   int resolution;
   int n_cells;

@@ -14,6 +14,7 @@
 #include "knf_rays.cuh"
 #include "knf_tail.cuh"
 #include "knf_tc5.cuh"
+#include "knf_bounds.cuh"
 
 namespace knf {
 
@@ -441,6 +442,44 @@ int color_forward_device(Field& F, const float* x, const float* v, const float* 
   return launch_col_mlp(F, R, (size_t)n, v, nrm, z, rgb, st);
 }
 
+// Sub-box refinement of the per-cell Lipschitz bounds (knf_bounds.cuh), once per handle, on the stream of the first march
+// that uses the decision filter: the filter blobs keep the closed-form bounds until the store kernel has run, and both are
+// proven bounds, so there is no window in which a kernel could read an invalid one.
+int ensure_lipschitz_refined(Field& F, cudaStream_t st) {
+  if (F.lip_refined || !F.lip_cur || !F.lip_consts) return 0;
+  F.lip_refined = true;
+  if (!(F.lip_width > 0.0)) return 0;
+  const int N = F.geom.resolution, n_cells = F.geom.n_cells;
+  double cell_w = 0.0, coord = 0.0;
+  for (int a = 0; a < 3; a++) {
+    cell_w = std::max(cell_w, (F.geom.hi[a] - F.geom.lo[a]) / (double)N);
+    coord = std::max(coord, std::max(std::fabs(F.geom.lo[a]), std::fabs(F.geom.hi[a])));
+  }
+  LipArgs A{};
+  A.blobs = F.sdf_blobs;
+  A.cc = F.lip_consts;
+  A.G = F.geom;
+  A.k = (int)std::max(1.0, std::min(64.0, std::ceil(cell_w / F.lip_width)));
+  A.fine = F.lip_fine;
+  // certified skipping requires the evaluated sample p0 within kLipSlack of the cell box (knf_tc5.cuh / knf_march.cuh
+  // `p0_in`): cover that, the fp32 rounding of the kernels' box test and the inner-box margin with room to spare
+  A.margin = 4.0 * (double)kLipSlack * cell_w + 4e-7 * coord;
+  A.out = F.lip_max;
+  KNF_CUDA(cudaMemsetAsync(F.lip_max, 0, (size_t)n_cells * 3 * sizeof(unsigned long long), st));
+  const long long n_sub = (long long)A.k * A.k * A.k;
+  // enough CTAs to fill the GPU several times over, each warp still looping over many sub-boxes of its cell
+  int chunks = (int)std::max<long long>(1, std::min<long long>((n_sub + 8 * kLipWarps - 1) / (8 * kLipWarps), (148 * 16 + n_cells - 1) / n_cells));
+  KNF_CUDA(cudaFuncSetAttribute(lip_bound_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LipSmem)));
+  lip_bound_kernel<<<dim3(n_cells, chunks), 32 * kLipWarps, sizeof(LipSmem), st>>>(A);
+  const bool tc5 = F.sdf_tc5_blobs != nullptr, mma = F.sdf_mmah_blobs != nullptr;
+  lip_store_kernel<<<(n_cells * 3 + 255) / 256, 256, 0, st>>>(
+      F.lip_max, n_cells, F.lip_cur, tc5 ? F.sdf_tc5_blobs : nullptr, Tc5Blob::bytes, Tc5Blob::off_f32 + Tc5Blob::f_lip * 4,
+      mma ? F.sdf_mmah_blobs : nullptr, MmaBlobT<2>::words, MmaBlobT<2>::b3 + kFilterLipSlot);
+  F.stats.kernel_launches += 2;
+  KNF_CUDA(cudaGetLastError());
+  return 0;
+}
+
 int march_device(Field& F, const double* o, const double* d, const double* t_near, const double* t_far, int64_t n,
                  const KnfSettings& s, unsigned char* hit, double* t, double* pos, int* steps, bool want_hit_list,
                  cudaStream_t st) {
@@ -488,6 +527,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
   // (consecutive frames of one field look alike; a wrong hint costs time, never a result)
   if (use_filter && F.filter_mode == 2 && F.filter_hint == 2) use_filter = false;
   const bool probing = use_filter && F.filter_mode == 2 && F.filter_hint == 0;
+  if (use_filter && !probing && F.filter_skip > 0) KNF_TRY(ensure_lipschitz_refined(F, st));  // (a probing march refines once it has seen rays crawl)
   size_t seen_filter = 0, seen_total = 0;
   bool filter_drained = false;  // the filter queue was seen empty after the filter had been switched off
   bool exact_sparse = false;    // last poll: the exact queue holds < 1/16 of the rays -> small-tile-only kernel
@@ -648,6 +688,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
       exact_sparse = (size_t)n_exact * (size_t)F.sparse_div < (size_t)n;
       live_upper = std::max<size_t>((size_t)n_exact + (size_t)n_filter, 1);  // rays only retire: an upper bound for every later queue
       if (probing && w == 0 && (size_t)n_filter * 8 < (size_t)(n_exact + n_filter)) use_filter = false;  // < 1/8 of the live rays crawl
+      if (probing && w == 0 && use_filter && F.filter_skip > 0) KNF_TRY(ensure_lipschitz_refined(F, st));
       if (!use_filter && n_filter == 0) filter_drained = true;
     }
   }

@@ -13,6 +13,8 @@
 
 namespace knf {
 
+struct LipCellConst;  // knf_bounds.cuh
+
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
@@ -75,6 +77,16 @@ struct Field {
   bool fp16_ok = false;
   double filter_delta_max = 0.0;       // largest FINITE per-cell decision-filter bound (knf_api.cu filter_delta)
   float filter_x_raw = 0.0f;           // coordinate magnitude the bounds were derived for (1.001 x the box's largest |coordinate|)
+  // sub-box refinement of the per-cell Lipschitz bounds behind certified skipping (knf_bounds.cuh): run on the device the
+  // first time a march uses the decision filter; until then (and wherever it is no tighter) the closed-form bounds apply
+  LipCellConst* lip_consts = nullptr;        // device, per cell
+  float* lip_cur = nullptr;                  // device, [n_cells][3]: the bounds the filter kernels currently read
+  unsigned long long* lip_max = nullptr;     // device, [n_cells][3]: the refinement's running maxima
+  std::vector<float> lip_closed_form;        // host copy of the closed-form bounds
+  bool lip_refined = false;
+  double lip_width = 0.004;                  // target sub-box width (KNF_LIP_WIDTH; 0: keep the closed-form bounds)
+  int lip_fine = 2;                          // Taylor samples per sub-box interval (KNF_LIP_FINE, 1..4)
+  float lip_ms = 0.f;                        // device time of the refinement (0 until it has run with profiling on)
   int filter_cells_off = 0;            // cells whose activations can leave the fp16 range: delta = +inf, the filter decides nothing there
   int sparse_max_inner = 8;            // residency cap and keep rule of sparse exact wavefronts (KNF_SPARSE_INNER / KNF_SPARSE_KEEP)
   int sparse_keep_div = 2;   // measured: (16, 4) gains 3 % on the distilled frame and loses 1.3 % on the random-init one; (32, 8) and up lose more
@@ -84,7 +96,7 @@ struct Field {
   int scan_split = 65536;              // grids with more cells scan in chunks over many CTAs (two launches) instead of one CTA per queue (KNF_SCAN_SPLIT)
   int filter_grid_ctas = 6;            // CTAs per SM the tcgen05 filter's grid asks for (KNF_FILTER_GRID; fewer leaves room for the concurrent exact kernel)
   int filter_skip_cap = 1 << 20;       // cap on the certified steps taken after one evaluation (KNF_FILTER_SKIP_CAP)
-  int filter_skip = 1;                 // certified (Lipschitz) skipping inside the filter: 0 off, 1 sample by sample, 2 closed-form run (cell-exit DDA + Lipschitz budget) then sample by sample; KNF_FILTER_SKIP
+  int filter_skip = 2;                 // certified (Lipschitz) skipping inside the filter: 0 off, 1 sample by sample, 2 closed-form run (cell-exit DDA + Lipschitz budget) then sample by sample (the default since the refined bounds made runs long); KNF_FILTER_SKIP
   int filter_hint = 0;                 // auto mode: what the previous march on this handle learnt (0 unknown, 1 rays crawl, 2 they do not)
   int filter_mode = 2;                 // decision filter of the exact march: 0 off, 1 on, 2 auto (probe the first wavefront)
   int precision = 0;                  // KNF_PRECISION_*: which SDF tile kernels run
@@ -152,6 +164,7 @@ struct CallScope {
   CallScope& operator=(const CallScope&) = delete;
 };
 int finish_stats(Field& F, cudaStream_t st);            // pull device counters into F.stats (syncs)
+int ensure_lipschitz_refined(Field& F, cudaStream_t st);  // knf_bounds.cuh, once per handle (asynchronous on `st`)
 
 int launch_scan_scatter(Field& F, const RouteBuffers& R, size_t n_upper, cudaStream_t st, int* seg_cell = nullptr,
                         int* seg_start = nullptr, int* n_seg = nullptr);

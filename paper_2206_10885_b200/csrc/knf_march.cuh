@@ -343,7 +343,7 @@ static __global__ void __maxnreg__(KNF_MARCH_MMA_MAXNREG) march_mma_kernel(March
         }
       }
     }
-    float in_lo[3], in_hi[3];
+    float in_lo[3], in_hi[3], lip_pad[3];
     {
       const int N = A.G.resolution;
       const double inv_n = A.inv_resolution;
@@ -353,6 +353,7 @@ static __global__ void __maxnreg__(KNF_MARCH_MMA_MAXNREG) march_mma_kernel(March
         const double ext = A.G.hi[a] - A.G.lo[a];
         in_lo[a] = (float)(A.G.lo[a] + ext * ((double)ci[a] * inv_n) + 1e-6 * ext);
         in_hi[a] = (float)(A.G.lo[a] + ext * ((double)(ci[a] + 1) * inv_n) - 1e-6 * ext);
+        lip_pad[a] = (float)((1e-6 + (double)kLipSlack * inv_n) * ext);  // inner box -> cell box + kLipSlack cell widths
       }
     }
     int n_active = tile.count;
@@ -414,7 +415,11 @@ static __global__ void __maxnreg__(KNF_MARCH_MMA_MAXNREG) march_mma_kernel(March
             // network), so every sample whose bound stays below `room` still has an exact distance below -eps: the
             // reference's evaluation there can only say "keep crawling", and its step is taken without evaluating.
             // (fp32, rounded towards less room: the fp64 pipe is the scarce one in this kernel)
-            const float room = (FILTER && A.max_skip > 0) ? __fmul_rd(__fsub_rd(safe_below_f, q ? dist.y : dist.x), 0.99999f) : 0.0f;
+            // (the bounds hold on the cell box plus a small margin, knf_bounds.cuh: no skipping from a sample clamped into this
+            // cell from outside the grid)
+            const bool p0_in = x0 >= in_lo[0] - lip_pad[0] && x0 <= in_hi[0] + lip_pad[0] && y0 >= in_lo[1] - lip_pad[1] &&
+                               y0 <= in_hi[1] + lip_pad[1] && z0 >= in_lo[2] - lip_pad[2] && z0 <= in_hi[2] + lip_pad[2];
+            const float room = (FILTER && A.max_skip > 0 && p0_in) ? __fmul_rd(__fsub_rd(safe_below_f, q ? dist.y : dist.x), 0.99999f) : 0.0f;
             for (;;) {
               px[q] = __double2float_rn(S.od[0][32 * q + lane] + t_next * S.od[3][32 * q + lane]);
               py[q] = __double2float_rn(S.od[1][32 * q + lane] + t_next * S.od[4][32 * q + lane]);

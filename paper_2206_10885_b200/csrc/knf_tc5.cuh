@@ -273,7 +273,7 @@ static __global__ void __launch_bounds__(kTc5Tile, kTc5CtasPerSm) march_tc5_kern
         cp_async_8(&S.od[3 + a][tid], A.M.d + 3 * (size_t)ray + a);
       }
     }
-    float in_lo[3], in_hi[3];
+    float in_lo[3], in_hi[3], lip_pad[3];
     {
       const int N = A.G.resolution;
       const double inv_n = A.inv_resolution;
@@ -283,6 +283,7 @@ static __global__ void __launch_bounds__(kTc5Tile, kTc5CtasPerSm) march_tc5_kern
         const double ext = A.G.hi[a] - A.G.lo[a];
         in_lo[a] = (float)(A.G.lo[a] + ext * ((double)ci[a] * inv_n) + 1e-6 * ext);
         in_hi[a] = (float)(A.G.lo[a] + ext * ((double)(ci[a] + 1) * inv_n) - 1e-6 * ext);
+        lip_pad[a] = (float)((1e-6 + (double)kLipSlack * inv_n) * ext);  // inner box -> cell box + kLipSlack cell widths
       }
     }
     int n_active = tile.count;
@@ -368,7 +369,11 @@ static __global__ void __launch_bounds__(kTc5Tile, kTc5CtasPerSm) march_tc5_kern
           cell = tile.cell;  // undecided: the same sample goes to the exact queue of this wavefront
         } else if (code != STEP_DONE) {
           const float x0 = px, y0 = py, z0 = pz;  // where d_f was evaluated
-          const float room = A.max_skip > 0 ? __fmul_rd(__fsub_rd(safe_below_f, dist), 0.99999f) : 0.0f;
+          // the Lipschitz bounds hold on the cell box plus a small margin (knf_bounds.cuh): no skipping from a sample that was
+          // clamped into this cell from outside the grid
+          const bool p0_in = x0 >= in_lo[0] - lip_pad[0] && x0 <= in_hi[0] + lip_pad[0] && y0 >= in_lo[1] - lip_pad[1] &&
+                             y0 <= in_hi[1] + lip_pad[1] && z0 >= in_lo[2] - lip_pad[2] && z0 <= in_hi[2] + lip_pad[2];
+          const float room = (A.max_skip > 0 && p0_in) ? __fmul_rd(__fsub_rd(safe_below_f, dist), 0.99999f) : 0.0f;
           const double dt = A.M.step_scale * (A.M.eps / 2);  // the crawl step (surface.py:217-223 with max(d, eps/2) = eps/2)
           // ---- certified skipping, part 1: a run of samples certified in closed form (the ray's cell-exit parameter from
           // the grid DDA and the Lipschitz budget bound the run; no per-sample arithmetic).  Sample j (j = 1 is t_next)

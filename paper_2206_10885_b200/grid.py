@@ -319,6 +319,17 @@ class DeviceField:
             N.check(n)
         return n
 
+    def lipschitz(self):
+        """Per-cell, per-axis Lipschitz bounds behind the decision filter's certified skipping
+        (include/knf_b200.h knf_field_lipschitz): (closed_form, refined, refine_ms), two (n_cells, 3) float32 arrays.
+        Runs the sub-box refinement (csrc/knf_bounds.cuh) if no march has triggered it yet."""
+        n = int(self.config.resolution) ** 3
+        closed = np.empty((n, 3), dtype=np.float32)
+        refined = np.empty((n, 3), dtype=np.float32)
+        ms = C.c_float(0.0)
+        N.check(N.load().knf_field_lipschitz(self.handle, closed.ctypes.data, refined.ctypes.data, C.addressof(ms), N.current_stream(self.device)))
+        return closed, refined, float(ms.value)
+
     def get_precision(self) -> str:
         code = N.load().knf_field_get_precision(self.handle)
         N.check(min(code, 0))

@@ -140,7 +140,7 @@ def test_filter_on_a_32_cubed_field(S, G):
     field = G.field_init(G.GridConfig(resolution=32), seed=2)
     o, d, tn, tf = _camera_rays(96, 96, pos=(0.4, 0.3, 2.4))
     res, st, _ = _march_on_off(S, field, o, d, tn, tf, S.RenderSettings())
-    assert st["filter_evals"] > st["sdf_evals"]
+    assert st["filter_evals"] + st["filter_skipped"] > st["sdf_evals"]  # most samples are decided or certified by the filter
     _vs_oracle("32^3", res, field, o, d, tn, tf, oracle.MarchSettings(), 0.995, 0.99)
 
 
@@ -188,6 +188,79 @@ def test_frames_identical_filter_on_off_vs_oracle(S, G):
     rel = np.abs(fb.depth[both] - ref.depth[both]) / ref.depth[both]
     print(f"128^2 filtered frame vs oracle: hits {agree:.4%}, depth<=1e-4 {np.mean(rel <= 1e-4):.4%}")
     assert agree >= 0.998 and np.mean(rel <= 1e-4) >= 0.998
+
+
+# ---- certified skipping: the per-cell Lipschitz bounds (csrc/knf_bounds.cuh) -----------------------------------------
+
+
+def test_lipschitz_refinement_matches_restatement_and_is_sound(G, monkeypatch):
+    """The device refinement against its float64 NumPy restatement (tests/lip_restatement.py) on a coarse setting the
+    restatement finishes in seconds, the closed form against its restatement, and soundness: on thousands of random
+    points per cell the true |d d / d x_a| stays below the bound the filter kernels read."""
+    import lip_restatement as L
+
+    monkeypatch.setenv("KNF_LIP_WIDTH", "0.02")  # 8^3 grid: k = 13 sub-boxes per axis
+    monkeypatch.setenv("KNF_LIP_FINE", "3")
+    field = G.field_init(G.GridConfig(resolution=8, bbox_min=(-1.0, -1.2, -0.8), bbox_max=(1.0, 0.8, 1.2)), seed=5)
+    rng = np.random.default_rng(1)
+    field.sdf.biases[0] += rng.normal(scale=0.3, size=field.sdf.biases[0].shape).astype(np.float32)
+    field.sdf.biases[1] += rng.normal(scale=0.3, size=field.sdf.biases[1].shape).astype(np.float32)
+    dev = G.DeviceField.upload(field)
+    try:
+        closed, refined, ms = dev.lipschitz()
+        again = dev.lipschitz()[1]
+    finally:
+        dev.close()
+    assert np.array_equal(again, refined) and (refined <= closed).all() and (refined > 0).all()
+    for c in (0, 77, 300, 511):
+        W1, W2, w3 = (np.asarray(field.sdf.weights[k][c], np.float64) for k in range(3))
+        want_closed = L.closed_form(W1, W2, w3[0])
+        assert np.allclose(closed[c], want_closed, rtol=1e-5), (c, closed[c], want_closed)
+        want = np.minimum(L.refine_cell(field, c, 0.02, 3), want_closed)
+        assert np.allclose(refined[c], want, rtol=2e-6), (c, refined[c], want)
+        assert (refined[c] >= want * (1 - 1e-7)).all()  # stored rounded UP
+    print(f"8^3 odd box, width 0.02: closed-form / refined = {np.mean(closed / refined):.2f} (mean), refinement {ms:.1f} ms")
+    monkeypatch.delenv("KNF_LIP_WIDTH")
+    monkeypatch.delenv("KNF_LIP_FINE")
+    field = G.field_init(G.GridConfig(resolution=16), seed=0)
+    dev = G.DeviceField.upload(field)
+    try:
+        closed, refined, ms = dev.lipschitz()
+    finally:
+        dev.close()
+    worst = 0.0
+    for c in np.random.default_rng(2).integers(0, 16 ** 3, 12):
+        g = L.sampled_gradient_max(field, int(c), n=20000, seed=int(c))
+        assert (g <= refined[c]).all(), (c, g, refined[c])
+        worst = max(worst, float((g / refined[c]).max()))
+    ratio = closed / refined
+    print(f"16^3 default width: closed-form / refined mean {ratio.mean():.2f} (min {ratio.min():.2f}, max {ratio.max():.2f}), "
+          f"refinement {ms:.0f} ms, sampled gradient reaches {worst:.3f} of the bound")
+    assert ratio.mean() > 5.0  # the refinement is what makes certified skipping pay
+
+
+@pytest.mark.parametrize("eps,step_scale,bars", [(1e-3, 0.8, (0.99, 0.98)), (0.02, 1.0, (0.97, 0.95)), (1e-4, 0.5, (0.99, 0.98))])
+def test_skipping_on_an_off_centre_box_and_other_step_sizes(S, G, eps, step_scale, bars):
+    """Certified skipping with the refined bounds on a non-cubic, off-centre box, rays that start outside it (samples clamped
+    into boundary cells must not start a skip run) and crawl steps from 2.5e-5 to 0.02: filter off / on / auto bit-identical,
+    closed-form run (KNF_FILTER_SKIP=2, the default) and per-sample skipping alike."""
+    cfg = G.GridConfig(resolution=8, bbox_min=(-1.5, -1.0, -0.5), bbox_max=(1.0, 1.2, 0.8))
+    field = G.field_init(cfg, seed=21)
+    rng = np.random.default_rng(22)
+    n = 5000
+    o = rng.uniform(-2.0, 2.0, size=(n, 3))
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    tn = np.zeros(n)
+    tf = rng.uniform(0.3, 3.0, size=n)
+    settings = S.RenderSettings(eps_hit=eps, step_scale=step_scale, max_steps=160)
+    res, st, _ = _march_on_off(S, field, o, d, tn, tf, settings)
+    assert st["filter_evals"] > 0 and st["filter_skipped"] > 0
+    print(f"eps {eps:g} step_scale {step_scale:g}: filter evals {st['filter_evals']}, certified {st['filter_skipped']}, exact {st['sdf_evals']}")
+    # (bit-identity above is the proof; against the oracle a coarse eps lets more rays of this chaotic field flip a
+    # convergence step on the reference's own small-batch BLAS order, DESIGN.md section 2, hence the wider sanity bar there)
+    _vs_oracle(f"off-centre box eps={eps:g}", res, field, o, d, tn, tf,
+               oracle.MarchSettings(eps_hit=eps, step_scale=step_scale, max_steps=160), *bars)
 
 
 # ---- host-side hazards (ADVICE r1) ------------------------------------------------------------------------------

@@ -276,7 +276,7 @@ def test_decision_filter_is_exact(S, cams, distilled_field):
         print(f"{name}: filter on -> exact {st['sdf_evals']}, filter {st['filter_evals']}, undecided {st['filter_deferred']}, "
               f"certified {st['filter_skipped']} (delta {fs.dev.filter_delta():.3g}); off -> exact {st0['sdf_evals']}")
         if name.startswith("random-init 16"):
-            assert st["filter_evals"] > 5 * st["sdf_evals"]  # the filter carries the crawl
+            assert st["filter_evals"] + st["filter_skipped"] > 5 * st["sdf_evals"]  # the filter carries the crawl (evaluated or certified)
             assert out["auto"][2]["filter_evals"] > 0
         elif name.startswith("distilled"):
             assert out["auto"][2]["filter_evals"] == 0        # auto switches itself off on a real surface
