@@ -398,17 +398,55 @@ static __global__ void __launch_bounds__(kTc5Tile, kTc5CtasPerSm) march_tc5_kern
             const float budget = room - 1.0e-6f * lip_sum;
             if (rise_per_step > 0.0f) run = fminf(run, budget > 0.0f ? __fdividef(budget, rise_per_step) : 0.0f);
             int J = (int)fminf(run * 0.999f, 1.0e6f) - 2;  // samples 1 .. J are certified
-            // the reference's steps through samples 1 .. J, each with its own rounded fp64 addition
-            for (int j = 0; j < J; j++) {
-              rr.steps += 1;
-              rr.t_prev = rr.t;
-              rr.t = rr.t + dt;
-              skipped += 1;
-              if (rr.t > rr.t_far || rr.steps >= A.M.max_steps) {
-                A.M.phase[ray] = PH_DONE;
-                A.M.steps[ray] = rr.steps;
-                code = STEP_DONE;
-                break;
+            // The reference's steps through samples 1 .. J: J rounded fp64 additions t <- fl(t + dt).  Inside one binade
+            // [2^e, 2^(e+1)) every t is a multiple of u = 2^(e-52), so fl(t + dt) = t + D with the SAME D = rn_u(dt) at every
+            // step (unless dt's remainder is an exact tie, where the parity of t / u decides): t_j = t0 + j D, and j D and the
+            // sum are exactly representable.  D = fl(t0 + dt) - t0 is the first of those additions itself.  So the run -- and
+            // the step at which it would pass t_far or exhaust max_steps -- is taken in closed form, bit for bit; a run that
+            // could leave the binade (t crossing a power of two), a tie, or t0 <= 0 takes the loop below instead.
+            if (J > 0) {
+              const double t0 = rr.t;
+              const long long eb = __double_as_longlong(t0) & 0x7ff0000000000000ll;
+              const double top = __longlong_as_double(eb + 0x0010000000000000ll);  // 2^(e+1)
+              const double u = __longlong_as_double(eb - (52ll << 52));            // 2^(e-52)
+              const double D = (t0 + dt) - t0;
+              const bool closed = t0 > 0.0 && eb > (60ll << 52) && D > 0.0 && fabs(dt - D) * 2.0 != u && J < (1 << 20) &&
+                                  t0 + (double)(J + 2) * dt < top;
+              if (closed) {
+                int m = J;
+                bool done = false;
+                const int m_steps = max(1, A.M.max_steps - rr.steps);  // the addition after which steps reaches max_steps
+                if (m_steps <= m) { m = m_steps; done = true; }
+                if (t0 + (double)m * D > rr.t_far) {  // the first m additions pass t_far: find the first that does
+                  int mf = (int)fmin(floor((rr.t_far - t0) / D), 2.0e6) + 1;
+                  mf = max(1, min(mf, m));
+                  while (mf > 1 && t0 + (double)(mf - 1) * D > rr.t_far) mf--;
+                  while (mf < m && !(t0 + (double)mf * D > rr.t_far)) mf++;
+                  m = mf;
+                  done = true;
+                }
+                rr.steps += m;
+                rr.t_prev = t0 + (double)(m - 1) * D;
+                rr.t = t0 + (double)m * D;
+                skipped += (unsigned)m;
+                if (done) {
+                  A.M.phase[ray] = PH_DONE;
+                  A.M.steps[ray] = rr.steps;
+                  code = STEP_DONE;
+                }
+              } else {
+                for (int j = 0; j < J; j++) {
+                  rr.steps += 1;
+                  rr.t_prev = rr.t;
+                  rr.t = rr.t + dt;
+                  skipped += 1;
+                  if (rr.t > rr.t_far || rr.steps >= A.M.max_steps) {
+                    A.M.phase[ray] = PH_DONE;
+                    A.M.steps[ray] = rr.steps;
+                    code = STEP_DONE;
+                    break;
+                  }
+                }
               }
             }
             t_next = rr.t;
