@@ -318,6 +318,28 @@ static void lipschitz_bound(const float* w1, const float* w2, const float* w3, d
   }
 }
 
+// Certified skipping compares the exact kernel's distances at two points of a cell through a Lipschitz bound of the
+// REAL-arithmetic network on the TRUE Fourier features, so the error of the fp32 features themselves (NumPy's float32 sin / cos
+// of fl(pi_f x) at octave 0, then the rounded double-angle recurrence, which roughly doubles the error per octave) enters at
+// both points.  scripts/feature_error.py measures max |fp32 feature - true feature| per octave EXHAUSTIVELY over all
+// 2 130 723 212 float32 inputs with |x| <= 1.001 (profiles/feature_error_r2b.json: 3.5, 9.9, 19.8, 45.4, 108.4, 273.0 units of
+// 2^-24); the constants below are those maxima x 1.25.  The dominant part is the angle error, proportional to |x|, so a larger
+// box scales them by x_raw / 1.001 (an extrapolation, not a measurement).  Through the layers (softplus' <= 1):
+//   |F(phi~) - F(phi)| <= |w3| |W2| sum_k |W1[:, k]|_2 |phi~_k - phi_k|   =: E_phi,
+// and 2 E_phi is added to the cell's filter bound delta, which is what both the filter's decision and the skip budget use.
+constexpr double kFeatureErrU[kSdfFreqs] = {4.5, 12.5, 25.0, 57.0, 136.0, 342.0};
+static double feature_error_allowance(const float* w1, double n3, double n2, double x_raw) {
+  const double unit = std::max(1.0, x_raw / 1.001) * std::ldexp(1.0, -24);
+  double s = 0.0;
+  for (int o = 0; o < kSdfFreqs; o++)
+    for (int c = 0; c < 6; c++) {  // the octave's three sin and three cos columns
+      double nn = 0.0;
+      for (int n = 0; n < kHidden; n++) nn += (double)w1[n * kSdfIn + 3 + 6 * o + c] * (double)w1[n * kSdfIn + 3 + 6 * o + c];
+      s += std::sqrt(nn) * kFeatureErrU[o] * unit;
+    }
+  return n3 * n2 * s * 1.0001;
+}
+
 template <int P>
 void pack_sdf_mma(int n_cells, const float* const w[3], const float* const b[3], double x_raw, std::vector<uint32_t>& out,
                   double* delta_max, int* cells_off = nullptr) {
@@ -366,14 +388,16 @@ void pack_sdf_mma(int n_cells, const float* const w[3], const float* const b[3],
       for (int k = 0; k < kHidden; k++) w3t[k * kSdfOutPad + j] = w3[j * kHidden + k];
     std::memcpy(blob + Blob::w3d, w3, kHidden * sizeof(float));  // row 0 of (9, 32): the distance output
     std::memcpy(blob + Blob::b3, b[2] + (size_t)c * kSdfOut, kSdfOut * sizeof(float));
-    const double delta = filter_delta(P, w1, b[0] + (size_t)c * kHidden, w2, b[1] + (size_t)c * kHidden, w3, b[2] + (size_t)c * kSdfOut, x_raw);
+    double lip[3];
+    LipCellConst lcc{};
+    lipschitz_bound(w1, w2, w3, lip, &lcc);
+    const double delta = filter_delta(P, w1, b[0] + (size_t)c * kHidden, w2, b[1] + (size_t)c * kHidden, w3, b[2] + (size_t)c * kSdfOut, x_raw) +
+                         2.0 * feature_error_allowance(w1, lcc.n3, lcc.n2, x_raw);
     // delta = +inf switches the filter off for this cell: -(eps + inf) = -inf, no distance is ever below it
     const float delta_f = delta < 1e30 ? std::nextafter((float)delta, INFINITY) : INFINITY;
     std::memcpy(blob + Blob::b3 + kFilterDeltaSlot, &delta_f, sizeof(float));
     if (delta_max && std::isfinite(delta_f)) *delta_max = std::max(*delta_max, (double)delta_f);
     if (cells_off && !std::isfinite(delta_f)) *cells_off += 1;
-    double lip[3];
-    lipschitz_bound(w1, w2, w3, lip);
     for (int a = 0; a < 3; a++) {
       const float lip_f = std::nextafter((float)lip[a], INFINITY);
       std::memcpy(blob + Blob::b3 + kFilterLipSlot + a, &lip_f, sizeof(float));
@@ -421,13 +445,15 @@ void pack_sdf_tc5(int n_cells, const float* const w[3], const float* const b[3],
     std::memcpy(f + Tc5Blob::f_b3, b3, kSdfOut * sizeof(float));
     for (int j = 0; j < kSdfOut; j++)
       for (int k = 0; k < kHidden; k++) f[Tc5Blob::f_w3t + k * kSdfOutPad + j] = w3[j * kHidden + k];
-    const double delta = filter_delta(2, w1, b1, w2, b2, w3, b3, x_raw, true, (double)kTc5SoftplusErr);
+    double lip[3];
+    LipCellConst lcc{};
+    lipschitz_bound(w1, w2, w3, lip, &lcc);
+    if (lip_consts) (*lip_consts)[c] = lcc;
+    const double delta = filter_delta(2, w1, b1, w2, b2, w3, b3, x_raw, true, (double)kTc5SoftplusErr) + 2.0 * feature_error_allowance(w1, lcc.n3, lcc.n2, x_raw);
     const float delta_f = delta < 1e30 ? std::nextafter((float)delta, INFINITY) : INFINITY;
     f[Tc5Blob::f_delta] = delta_f;
     if (delta_max && std::isfinite(delta_f)) *delta_max = std::max(*delta_max, (double)delta_f);
     if (cells_off && !std::isfinite(delta_f)) *cells_off += 1;
-    double lip[3];
-    lipschitz_bound(w1, w2, w3, lip, lip_consts ? &(*lip_consts)[c] : nullptr);
     for (int a = 0; a < 3; a++) {
       f[Tc5Blob::f_lip + a] = std::nextafter((float)lip[a], INFINITY);
       if (lip_out) (*lip_out)[(size_t)c * 3 + a] = f[Tc5Blob::f_lip + a];
@@ -541,6 +567,7 @@ int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
   if (const char* env = std::getenv("KNF_FILTER_GRID")) F.filter_grid_ctas = std::max(1, std::atoi(env));
   if (const char* env = std::getenv("KNF_FILTER_SKIP_CAP")) F.filter_skip_cap = std::max(0, std::atoi(env));
   if (const char* env = std::getenv("KNF_OVERLAP")) F.overlap_queues = std::atoi(env) != 0;
+  if (const char* env = std::getenv("KNF_TAIL_SKIP")) F.tail_skip = std::atoi(env) != 0;
   if (const char* env = std::getenv("KNF_TAIL")) F.tail_threshold = std::max(0, std::atoi(env));
   if (const char* env = std::getenv("KNF_FILTER_KERNEL")) {
     const std::string v(env);

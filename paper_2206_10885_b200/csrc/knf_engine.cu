@@ -672,6 +672,14 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
         T.live_b = M.live[2 + nxt]; T.pt_b = Qb.req_pt; T.cell_b = Qb.req_cell; T.ctr_b = Qb.ctr;
         T.cursor = W.tail_cursor.as<int>();
         T.eval_counter = stat_counter(F, 0);
+        T.inv_resolution = A.inv_resolution;
+        T.skip_cap = F.filter_skip_cap;
+        if (use_filter && F.filter_skip > 0 && F.tail_skip && tc5) {  // certified skipping in the tail: delta / L_a from the tcgen05 filter blobs
+          T.fconst = F.sdf_tc5_blobs;
+          T.fconst_stride = Tc5Blob::bytes;
+          T.off_delta = Tc5Blob::off_f32 + Tc5Blob::f_delta * 4;
+          T.off_lip = Tc5Blob::off_f32 + Tc5Blob::f_lip * 4;
+        }
         KNF_CUDA(cudaMemsetAsync(W.tail_cursor.p, 0, 16, st));
         const int rays_left = n_exact + n_filter;
         const int grid = std::max(1, std::min((rays_left + kTailWarps - 1) / kTailWarps, 148 * 8));

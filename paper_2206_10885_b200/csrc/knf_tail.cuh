@@ -12,7 +12,14 @@
 //     evaluated it and results stay bit-identical;
 //   * weights are read straight from the cell's k-major blob (a row of W^T is one coalesced 128-byte load; consecutive
 //     steps of a ray stay in one cell, so the rows come from L1 / L2);
-//   * crawling rays from the filter queue are simply evaluated exactly (the filter only ever answered predicates).
+//   * crawling rays from the filter queue are evaluated exactly too (the filter only ever answered predicates), and CERTIFIED
+//     SKIPPING works here as in the filter kernel, with the exact distance in place of the filter's: from a sample p0 with
+//     d_exact(p0) < -(eps + delta) every further sample p of the ray in the same cell with sum_a L_a |p_a - p0_a| below
+//     -(eps + delta) - d_exact(p0) has an exact distance below -eps (L_a: the cell's proven Lipschitz bounds,
+//     knf_bounds.cuh; delta, the cell's filter bound, contains twice over the exact kernel's own distance to real
+//     arithmetic, which is all that separates d_exact from the function the bounds are about), so the reference's crawl
+//     steps there are taken without evaluating: closed-form run (cell-exit DDA + Lipschitz budget, J rounded fp64 additions
+//     in O(1)) and then sample by sample -- the logic of march_tc5_kernel, one ray per warp.
 #pragma once
 
 #include "knf_common.cuh"
@@ -38,7 +45,56 @@ struct MarchTailArgs {
   const RouteCounters* ctr_b;
   int* cursor;               // zero on entry: next unclaimed ray
   unsigned long long* eval_counter;
+  // certified skipping: per-cell filter constants (delta, L_a) inside the decision-filter blobs; null disables it
+  const unsigned char* fconst;
+  int fconst_stride;         // bytes per cell
+  int off_delta, off_lip;    // byte offsets of delta (1 float) and L_a (3 floats) inside a cell's blob
+  int skip_cap;              // most certified steps taken sample by sample after one evaluation
+  double inv_resolution;
 };
+
+// `m` certified crawl steps of the reference (surface.py:217-223 with max(d, eps / 2) = eps / 2) from the ray's current t:
+// J = n rounded fp64 additions t <- fl(t + dt), taken in closed form inside one binade (see march_tc5_kernel), or one by one.
+// Stops early at the first step that passes t_far or exhausts max_steps (returns true: the ray is done, a miss).
+__device__ __forceinline__ bool crawl_run(RayRegs& R, const MarchState& M, int ray, int n, double dt, unsigned long long& skipped) {
+  if (n <= 0) return false;
+  const double t0 = R.t;
+  const long long eb = __double_as_longlong(t0) & 0x7ff0000000000000ll;
+  const double top = __longlong_as_double(eb + 0x0010000000000000ll);  // 2^(e+1)
+  const double u = __longlong_as_double(eb - (52ll << 52));            // 2^(e-52)
+  const double D = (t0 + dt) - t0;
+  bool done = false;
+  if (t0 > 0.0 && eb > (60ll << 52) && D > 0.0 && fabs(dt - D) * 2.0 != u && n < (1 << 20) && t0 + (double)(n + 2) * dt < top) {
+    int m = n;
+    const int m_steps = max(1, M.max_steps - R.steps);
+    if (m_steps <= m) { m = m_steps; done = true; }
+    if (t0 + (double)m * D > R.t_far) {
+      int mf = (int)fmin(floor((R.t_far - t0) / D), 2.0e6) + 1;
+      mf = max(1, min(mf, m));
+      while (mf > 1 && t0 + (double)(mf - 1) * D > R.t_far) mf--;
+      while (mf < m && !(t0 + (double)mf * D > R.t_far)) mf++;
+      m = mf;
+      done = true;
+    }
+    R.steps += m;
+    R.t_prev = t0 + (double)(m - 1) * D;
+    R.t = t0 + (double)m * D;
+    skipped += (unsigned long long)m;
+  } else {
+    for (int j = 0; j < n && !done; j++) {
+      R.steps += 1;
+      R.t_prev = R.t;
+      R.t = R.t + dt;
+      skipped += 1;
+      done = R.t > R.t_far || R.steps >= M.max_steps;
+    }
+  }
+  if (done) {
+    M.phase[ray] = PH_DONE;
+    M.steps[ray] = R.steps;
+  }
+  return done;
+}
 
 // exact SDF distance at (x, y, z) in `cell`; all 32 lanes call it with the same point, all get the same value
 __device__ __forceinline__ float tail_eval(const float* __restrict__ blob, int lane, float x, float y, float z) {
@@ -89,7 +145,7 @@ constexpr int kTailWarps = 4;
 static __global__ void __launch_bounds__(32 * kTailWarps) march_tail_kernel(MarchTailArgs A) {
   const int lane = threadIdx.x & 31;
   const int n_a = A.ctr_a->n_requests, n_b = A.ctr_b ? A.ctr_b->n_requests : 0;
-  unsigned long long evals = 0;
+  unsigned long long evals = 0, skipped = 0;
   for (;;) {
     int i = 0;
     if (lane == 0) i = atomicAdd(A.cursor, 1);
@@ -102,20 +158,88 @@ static __global__ void __launch_bounds__(32 * kTailWarps) march_tail_kernel(Marc
     int cell = (from_a ? A.cell_a : A.cell_b)[slot];
     RayRegs rr;
     ray_load(rr, A.M, ray);
+    const double dt = A.M.step_scale * (A.M.eps / 2);
     for (;;) {
       const float d = tail_eval(A.blobs + (size_t)cell * SdfBlob::floats, lane, pt.x, pt.y, pt.z);
       evals += 1;
       double t_next = 0.0;
-      const int code = ray_step(rr, A.M, ray, d, t_next, -INFINITY);  // every lane steps its copy of the ray: same writes, same values
+      double safe_below = -INFINITY;
+      const float* fc = nullptr;
+      if (A.fconst) {
+        fc = reinterpret_cast<const float*>(A.fconst + (size_t)cell * A.fconst_stride);
+        safe_below = -(A.M.eps + (double)__ldg(fc + A.off_delta / 4));  // delta = +inf (filter off for the cell): never below
+      }
+      // every lane steps its copy of the ray: same writes, same values
+      int code = ray_step(rr, A.M, ray, d, t_next, safe_below);
       if (code == STEP_DONE) break;
-      // pts = origins + t * dirs in fp64 (surface.py:184), then the fp32 cast of grid.py:375
-      pt.x = __double2float_rn(rr.o[0] + t_next * rr.d[0]);
-      pt.y = __double2float_rn(rr.o[1] + t_next * rr.d[1]);
-      pt.z = __double2float_rn(rr.o[2] + t_next * rr.d[2]);
-      cell = cell_of_quick(pt.x, pt.y, pt.z, A.G.lo, A.G.hi, A.cell_scale, A.G.resolution);
+      bool known_cell = false;
+      if (code == STEP_FILTER) {
+        // ---- certified skipping from p0 = pt, d_exact(p0) = d < -(eps + delta): the logic of march_tc5_kernel ---------------
+        const float lip[3] = {__ldg(fc + A.off_lip / 4), __ldg(fc + A.off_lip / 4 + 1), __ldg(fc + A.off_lip / 4 + 2)};
+        const int N = A.G.resolution;
+        const int ci[3] = {cell / (N * N), (cell / N) % N, cell % N};
+        const float p0[3] = {pt.x, pt.y, pt.z};
+        float in_lo[3], in_hi[3];
+        bool p0_in = true;
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+          const double ext = A.G.hi[a] - A.G.lo[a];
+          in_lo[a] = (float)(A.G.lo[a] + ext * ((double)ci[a] * A.inv_resolution) + 1e-6 * ext);
+          in_hi[a] = (float)(A.G.lo[a] + ext * ((double)(ci[a] + 1) * A.inv_resolution) - 1e-6 * ext);
+          const float pad = (float)((1e-6 + (double)kLipSlack * A.inv_resolution) * ext);
+          p0_in = p0_in && p0[a] >= in_lo[a] - pad && p0[a] <= in_hi[a] + pad;
+        }
+        const float room = p0_in ? __fmul_rd(__fsub_rd(__double2float_rd(safe_below), d), 0.99999f) : 0.0f;
+        const unsigned long long skipped_before = skipped;
+        bool done = false;
+        if (room > 0.0f) {
+          // part 1: closed-form run (per axis |p_j - p0| <= j dt |d_a| (1 + 2^-20) + two fp32 roundings; 2 samples short of
+          // the cell exit and of the Lipschitz budget, scaled by 0.999 against the fp32 arithmetic here)
+          const float dtf = __double2float_ru(dt);
+          float run = 1.0e9f, rise_per_step = 0.0f, lip_sum = 0.0f;
+#pragma unroll
+          for (int a = 0; a < 3; a++) {
+            const float ad = __double2float_ru(fabs(rr.d[a])) * 1.000002f;
+            const float gap = rr.d[a] > 0.0 ? in_hi[a] - p0[a] : p0[a] - in_lo[a];
+            const float stepa = ad * dtf;
+            if (stepa > 0.0f) run = fminf(run, __fdividef(fmaxf(gap, 0.0f), stepa));
+            rise_per_step += lip[a] * stepa;
+            lip_sum += lip[a];
+          }
+          const float budget = room - 1.0e-6f * lip_sum;
+          if (rise_per_step > 0.0f) run = fminf(run, budget > 0.0f ? __fdividef(budget, rise_per_step) : 0.0f);
+          const int J = (int)fminf(run * 0.999f, 1.0e6f) - 2;
+          done = crawl_run(rr, A.M, ray, J, dt, skipped);
+          t_next = rr.t;
+        }
+        // part 2: the remaining samples, one by one (exact point, exact box test, exact rise)
+        for (int it = 0; !done; it++) {
+          pt.x = __double2float_rn(rr.o[0] + t_next * rr.d[0]);
+          pt.y = __double2float_rn(rr.o[1] + t_next * rr.d[1]);
+          pt.z = __double2float_rn(rr.o[2] + t_next * rr.d[2]);
+          known_cell = pt.x > in_lo[0] && pt.x < in_hi[0] && pt.y > in_lo[1] && pt.y < in_hi[1] && pt.z > in_lo[2] && pt.z < in_hi[2];
+          if (!known_cell || it >= A.skip_cap) break;
+          const float rise = lip[0] * (fabsf(pt.x - p0[0]) + 1e-6f) + lip[1] * (fabsf(pt.y - p0[1]) + 1e-6f) + lip[2] * (fabsf(pt.z - p0[2]) + 1e-6f);
+          if (!(rise < room)) break;
+          done = crawl_run(rr, A.M, ray, 1, dt, skipped);
+          t_next = rr.t;
+        }
+        if (done) break;
+        // t_prev moved past samples nobody evaluated: d_prev (exact, at p0) is now only good as a predicate, and a ray that
+        // converges next re-evaluates it at t_prev first (PH_RECHECK), as after filtered steps
+        if (skipped != skipped_before) rr.approx = 1;
+      } else {
+        pt.x = __double2float_rn(rr.o[0] + t_next * rr.d[0]);
+        pt.y = __double2float_rn(rr.o[1] + t_next * rr.d[1]);
+        pt.z = __double2float_rn(rr.o[2] + t_next * rr.d[2]);
+      }
+      if (!known_cell) cell = cell_of_quick(pt.x, pt.y, pt.z, A.G.lo, A.G.hi, A.cell_scale, A.G.resolution);
     }
   }
-  if (lane == 0 && evals && A.eval_counter) atomicAdd(A.eval_counter, evals);
+  if (lane == 0 && evals && A.eval_counter) {
+    atomicAdd(A.eval_counter, evals);
+    if (skipped) atomicAdd(A.eval_counter + 6, skipped);  // certified steps (same counter as the filter kernel's)
+  }
 }
 
 }  // namespace knf
