@@ -294,12 +294,16 @@ __device__ __forceinline__ void softplus_np_f2xN(float2 (&x)[N]) {
   float2 A[N], Al[N], R[N], fN[N], p[N];
   KNF_EACH A[i] = __fadd2_rn(KNF_S2(1.0f), e[i]);
   KNF_EACH Al[i] = __fadd2_rn(__fadd2_rn(KNF_S2(1.0f), make_float2(-A[i].x, -A[i].y)), e[i]);
+  // The routine's integer reduction (ia = bits(A) - 0x3f2aaaab; N = ia >> 23; mantissa re-biased to [2/3, 4/3)) with
+  // A = 1 + e in (1, 2]: N is 1 exactly when bits(A) >= 0x3faaaaab, i.e. A >= 1.3333334f, and then the re-biased mantissa
+  // is A / 2 and the scale 2^-N is 0.5 (else A and 1) -- the same values from one compare, two selects and one exact packed
+  // multiplication by a power of two instead of seven integer operations per element.
   KNF_EACH {
-    const int ia0 = __float_as_int(A[i].x) - 0x3f2aaaab, ia1 = __float_as_int(A[i].y) - 0x3f2aaaab;
-    const int n0 = ia0 & 0xff800000, n1 = ia1 & 0xff800000;  // N << 23, N in {0, 1}
-    fN[i] = make_float2(n0 ? 1.0f : 0.0f, n1 ? 1.0f : 0.0f);
-    const float2 sc = make_float2(__int_as_float(0x3f800000 - n0), __int_as_float(0x3f800000 - n1));
-    const float2 r0 = make_float2(__int_as_float((ia0 & 0x007fffff) + 0x3f2aaaab), __int_as_float((ia1 & 0x007fffff) + 0x3f2aaaab));
+    const float thr = __int_as_float(0x3faaaaab);
+    const bool hi0 = A[i].x >= thr, hi1 = A[i].y >= thr;
+    fN[i] = make_float2(hi0 ? 1.0f : 0.0f, hi1 ? 1.0f : 0.0f);
+    const float2 sc = make_float2(hi0 ? 0.5f : 1.0f, hi1 ? 0.5f : 1.0f);
+    const float2 r0 = __fmul2_rn(A[i], sc);
     R[i] = __fadd2_rn(__fadd2_rn(r0, KNF_S2(-1.0f)), __fmul2_rn(Al[i], sc));
   }
   KNF_EACH p[i] = __ffma2_rn(R[i], KNF_S2(0x1.1b09dap-3f), KNF_S2(-0x1.35b3c6p-3f));
