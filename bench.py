@@ -257,7 +257,7 @@ def workload_config(W, H, world, shard="views"):
                     "(eps 1e-3, 128 steps, scale 0.8), orbit views r=2.5 el=0.2 fov 40deg (BASELINE config 3)",
         "views_per_step": world if shard == "views" else 1,
         "parallelism": (f"view-sharded x{world}" if shard == "views" else f"one frame per step in interleaved 32-row bands x{world}") +
-                       ", field replicated, final all_gather of the colour / depth / normal / hit buffers",
+                       ", field replicated, final all_gather of the colour / depth / normal / hit buffers (overlapped with the next step's render)",
         "preheat": f"{PREHEAT_FRAMES} untimed frames before the warm-up steps (idle B200 clocks need 1-2 s of load to settle)",
         "l2": "no explicit flush: the per-step working set (ray state + request buffers, >400 MB) exceeds the 126 MB L2; "
               "the 45 MB SDF weight blobs are meant to stay L2-resident",
@@ -428,8 +428,11 @@ def main():
     # one all_gather per step moves all four finished buffers: 29 B per pixel packed into one byte tensor
     PIX_BYTES = 12 + 4 + 12 + 1
     tallest = max(sum(b[1] - b[0] for b in kdist.shard_rows_interleaved(H, r, world, BAND)) for r in range(world)) if rows_mode else H
-    packed = torch.empty((tallest * W * PIX_BYTES,), dtype=torch.uint8, device=dev) if use_dist else None
-    gathered = torch.empty((world * tallest * W * PIX_BYTES,), dtype=torch.uint8, device=dev) if use_dist else None
+    # double-buffered: the gather of step s runs on NCCL's stream while step s + 1 renders (frames are independent; the
+    # timed region closes with a barrier + synchronize, so every gather it started has finished inside it)
+    packed = [torch.empty((tallest * W * PIX_BYTES,), dtype=torch.uint8, device=dev) for _ in range(2)] if use_dist else None
+    gathered = [torch.empty((world * tallest * W * PIX_BYTES,), dtype=torch.uint8, device=dev) for _ in range(2)] if use_dist else None
+    pending = [None, None]
 
     def render_mine(view, out):
         at = 0
@@ -441,15 +444,26 @@ def main():
     def resident_step(s):
         render_mine(s if rows_mode else s * world + rank, bufs)
         if use_dist:
+            k = s & 1
+            if pending[k] is not None:
+                pending[k].wait()  # the gather that last used this buffer pair (two steps ago)
             at = 0
             for b in bufs:
                 nb = b.numel() * b.element_size()
-                packed[at : at + nb].copy_(b.reshape(-1).view(torch.uint8))
+                packed[k][at : at + nb].copy_(b.reshape(-1).view(torch.uint8))
                 at += nb
-            dist.all_gather_into_tensor(gathered, packed, async_op=False)
+            pending[k] = dist.all_gather_into_tensor(gathered[k], packed[k], async_op=True)
+
+    def drain():
+        # make the current stream wait for the gathers still in flight (so an event recorded next covers them)
+        for k in range(2):
+            if pending[k] is not None:
+                pending[k].wait()
+                pending[k] = None
 
     def barrier():
         if use_dist:
+            drain()
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -472,6 +486,7 @@ def main():
         e0.record()
         for s in range(args.steps):
             resident_step(args.warmup + s)
+        drain()
         e1.record()
         barrier()
         ms = e0.elapsed_time(e1)
