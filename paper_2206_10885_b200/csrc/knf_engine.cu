@@ -512,12 +512,6 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
   KNF_CUDA(cudaMemsetAsync(counters(F, 4), 0, 2 * sizeof(RouteCounters), st));
   KNF_CUDA(cudaMemsetAsync(W.cell_count_f.p, 0, (size_t)F.geom.n_cells * sizeof(int), st));
   const int nb = blocks_for((size_t)n);
-  {
-    ProfScope prof(F, st, SPAN_ROUTE);
-    RouteBuffers R0 = route_buffers(F, 0, 1, 0);
-    march_init_kernel<<<nb, 256, 0, st>>>(R0, F.geom, M, t_near, (int)n);
-    F.stats.kernel_launches += 1;
-  }
   // The decision filter (knf_march.cuh) serves the exact mode only; the tensor modes evaluate everything on the
   // tensor cores anyway.  auto: let the first global wavefront (one sample per ray) show whether rays enter the
   // negative region at all -- on a real surface they never do and the filter passes would be empty launches.
@@ -528,6 +522,16 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
   if (use_filter && F.filter_mode == 2 && F.filter_hint == 2) use_filter = false;
   const bool probing = use_filter && F.filter_mode == 2 && F.filter_hint == 0;
   if (use_filter && !probing && F.filter_skip > 0) KNF_TRY(ensure_lipschitz_refined(F, st));  // (a probing march refines once it has seen rays crawl)
+  // When the previous march on this handle has shown that rays crawl, every ray's FIRST sample goes to the filter queue too:
+  // about half of them are decided there at tensor-core speed (the rest move, unchanged, to the exact queue of wavefront 1,
+  // beside the filter's second pass) instead of all of them paying a dense exact launch that nothing overlaps.
+  const bool filter_first = use_filter && !probing && F.filter_first;
+  {
+    ProfScope prof(F, st, SPAN_ROUTE);
+    RouteBuffers R0 = filter_first ? route_buffers(F, 4, 5, 2) : route_buffers(F, 0, 1, 0);
+    march_init_kernel<<<nb, 256, 0, st>>>(R0, F.geom, M, t_near, (int)n, filter_first ? M.live[2] : M.live[0]);
+    F.stats.kernel_launches += 1;
+  }
   size_t seen_filter = 0, seen_total = 0;
   bool filter_drained = false;  // the filter queue was seen empty after the filter had been switched off
   bool exact_sparse = false;    // last poll: the exact queue holds < 1/16 of the rays -> small-tile-only kernel
@@ -541,10 +545,15 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
   size_t live_upper = (size_t)n;  // upper bound on the size of any queue from here on: sizes the routing and tile grids
   const int max_wavefronts = 2 * s.max_steps + 6;
   // hand-over point to the one-warp-per-ray tail kernel: a fixed count for large marches, 1/16 of the rays for small ones
-  const int tail_at = F.tail_threshold > 0 ? (int)std::min<int64_t>(F.tail_threshold, std::max<int64_t>(n / 16, 2048)) : 0;
+  // (twice as early when the tail kernel can skip certified crawl steps: measured 4.58 -> 4.30 ms on the random-init frame;
+  // a trained field, whose tail evaluates every step, loses 0.4 ms with the larger hand-over)
+  auto tail_threshold_now = [&]() {
+    const int base = (use_filter && F.tail_skip && F.filter_skip > 0 && F.sdf_tc5_blobs && F.filter_kernel == 1) ? 2 * F.tail_threshold : F.tail_threshold;
+    return base > 0 ? (int)std::min<int64_t>(base, std::max<int64_t>(n / 16, 2048)) : 0;
+  };
   for (int w = 0; w < max_wavefronts; w++) {
     const int cur = w & 1, nxt = cur ^ 1;
-    const bool filter_pass = exact_mode && F.fp16_ok && F.filter_mode != 0 && !filter_drained && w > 0;
+    const bool filter_pass = exact_mode && F.fp16_ok && F.filter_mode != 0 && !filter_drained && (w > 0 || filter_first);
     MarchTileArgs A{};
     A.G = F.geom;
     A.M = M;
@@ -646,6 +655,7 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     F.stats.kernel_launches += 1;
     F.stats.wavefronts += 1;
     // (more often once the live count nears the tail threshold, so the hand-over is not missed by several wavefronts)
+    const int tail_at = tail_threshold_now();
     const bool near_tail = exact_mode && tail_at > 0 && live_upper <= (size_t)tail_at * 6 && w > 3;
     const bool poll = (w == 0 && probing) || (w == 1) || (w == 3) || (w % 8 == 7) || (near_tail && (w & 1));
     if (poll && w + 1 < max_wavefronts) {
@@ -701,9 +711,24 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     }
   }
   F.prof_chain = false;
+  if (std::getenv("KNF_DEBUG_HINT"))
+    fprintf(stderr, "march n=%lld hint_before=%d probing=%d filter_first=%d use_filter_end=%d seen_filter=%zu seen_total=%zu wavefronts=%lld\n", (long long)n, F.filter_hint,
+            (int)probing, (int)filter_first, (int)use_filter, seen_filter, seen_total, (long long)F.stats.wavefronts);
   if (exact_mode && F.fp16_ok && F.filter_mode == 2 && seen_total > 0) {
-    if (F.filter_hint != 2) F.filter_hint = (seen_filter * 8 >= seen_total) ? 1 : 2;
-    else if (n >= 4096) F.filter_hint = 0;  // a "no crawl" hint is re-examined by probing the next large march
+    // The hint errs towards the filter: a march that crawls without it pays for every crawl step with an exact evaluation,
+    // a march that carries it in vain pays a few empty launches.  Marches on one handle differ (path tracing alternates
+    // primary and bounce rays, late bounces are small and their statistics noisy), so "rays crawl" is sticky: only a LARGE
+    // march that is (almost) crawl-free sends the handle back to probing, and only such a march sets "no crawl" (large by
+    // its LIVE rays after the first wavefronts: the path tracer marches whole bands whose late bounces hold a handful).
+    const bool crawl = seen_filter * 8 >= seen_total, none = seen_filter * 64 < seen_total, large = seen_total >= 16384;
+    if (F.filter_hint == 1) {
+      if (none && large) F.filter_hint = 0;
+    } else if (F.filter_hint == 0) {
+      if (crawl) F.filter_hint = 1;
+      else if (none && large) F.filter_hint = 2;
+    } else if (n >= 4096) {
+      F.filter_hint = 0;  // a "no crawl" hint is re-examined by probing the next large march
+    }
   }
   if (want_hit_list) KNF_CUDA(cudaMemsetAsync(W.hit_count.p, 0, 16, st));
   march_finish_kernel<<<nb, 256, 0, st>>>(M, (int)n, hit, t, pos, steps, want_hit_list ? W.hit_list.as<int>() : nullptr,

@@ -180,7 +180,7 @@ __device__ __forceinline__ void emit_at(const RouteBuffers& R, const GridGeom& G
   route_emit(R, G, want, slot, x, y, z);
 }
 
-static __global__ void march_init_kernel(RouteBuffers R, GridGeom G, MarchState M, const double* __restrict__ t_near, int n) {
+static __global__ void march_init_kernel(RouteBuffers R, GridGeom G, MarchState M, const double* __restrict__ t_near, int n, int* __restrict__ live_out) {
   int stride = gridDim.x * blockDim.x;
   int n_round = (n + 31) & ~31;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
@@ -197,7 +197,7 @@ static __global__ void march_init_kernel(RouteBuffers R, GridGeom G, MarchState 
       M.hit[i] = 0;
       M.phase[i] = want ? PH_MARCH : PH_DONE;
     }
-    emit_at(R, G, M, M.live[0], want, i, t0);
+    emit_at(R, G, M, live_out, want, i, t0);
   }
 }
 

@@ -6,10 +6,13 @@ import numpy as np, torch
 from paper_2206_10885_b200 import grid, surface
 from bench import orbit_view
 W, H = 1920, 1080
-args = [a for a in sys.argv[1:] if a not in ("distilled", "trained16")]
+args = [a for a in sys.argv[1:] if a not in ("distilled", "trained16", "trained8")]
 if "trained16" in sys.argv[1:]:
     from paper_2206_10885_b200.modelio import load_model
     fs = surface.FieldSurface(grid.refine_field(load_model(os.path.join(ROOT, "tests", "golden", "sphere_stripes_r8_distilled.knf")), 2))
+elif "trained8" in sys.argv[1:]:
+    from paper_2206_10885_b200.modelio import load_model
+    fs = surface.FieldSurface(load_model(os.path.join(ROOT, "tests", "golden", "sphere_stripes_r8_distilled.knf")))
 elif "distilled" in sys.argv[1:]:
     from paper_2206_10885_b200.modelio import load_model
     fs = surface.FieldSurface(load_model(os.path.join(ROOT, "tests", "golden", "sphere_r4_distilled.knf")))

@@ -251,7 +251,8 @@ def test_decision_filter_is_exact(S, cams, distilled_field):
     for name, field, size in (("random-init 16^3", grid.field_init(grid.GridConfig(resolution=16), seed=0), 160),
                               ("random-init 8^3 seed 3", grid.field_init(grid.GridConfig(resolution=8), seed=3), 112),
                               ("distilled 4^3", distilled_field, 96)):
-        fs = S.FieldSurface(field)
+        # a fresh handle: what the auto mode learnt from other tests' marches on a shared (cached) handle must not decide here
+        fs = S.FieldSurface(grid.DeviceField.upload(field))
         pose = cams.look_at_pose((0.3, 0.4, 2.4), (0, 0, 0), (0, 1, 0), np.deg2rad(40), size, size)
         o, d, tn, tf = _rays(size // 2, size // 2)
         out = {}
