@@ -153,6 +153,7 @@ static __global__ void __launch_bounds__(32 * kLipWarps) lip_bound_kernel(LipArg
   const double pi = 3.141592653589793238462643383279;
   const double w3l = S.w3[lane], aw3l = fabs(w3l);
   double best[3] = {0.0, 0.0, 0.0};
+  bool bad = false;
 
   const int n_sub = k * k * k;
   for (int s = blockIdx.y * kLipWarps + warp; s < n_sub; s += gridDim.y * kLipWarps) {
@@ -266,15 +267,19 @@ static __global__ void __launch_bounds__(32 * kLipWarps) lip_bound_kernel(LipArg
         const double base = fabs(s1) + h * fabs(s1p) + s23;
         const double tot_a = base + nrw * cc.n2 * (sqrt(s4) + h * sqrt(s4p)) + rem_a;
         const double tot_b = base + s4b + rem_b;
-        best[a] = fmax(best[a], fmin(tot_a, tot_b));
+        const double cand = fmin(tot_a, tot_b);
+        bad = bad || !(cand == cand);  // fmax would drop a NaN silently: a sub-box without a bound must void the cell's refinement
+        best[a] = fmax(best[a], cand);
       }
     }
     __syncwarp();
   }
   if (lane == 0) {
 #pragma unroll
-    for (int a = 0; a < 3; a++)
+    for (int a = 0; a < 3; a++) {
+      if (bad) best[a] = __longlong_as_double(0x7ff0000000000000ll);  // +inf: lip_store_kernel keeps the closed-form bound
       if (best[a] > 0.0) atomicMax(A.out + (size_t)cell * 3 + a, (unsigned long long)__double_as_longlong(best[a]));
+    }
   }
 }
 
