@@ -300,6 +300,8 @@ int finish_stats(Field& F, cudaStream_t st) {
   F.stats.filter_deferred = (int64_t)host[5];
   F.stats.filter_skipped = (int64_t)host[6];
   F.stats.filter_lane_slots = (int64_t)host[7];
+  if (std::getenv("KNF_DEBUG_TAIL"))
+    fprintf(stderr, "march_tail_kernel since the last stats reset: %llu rays, %llu evaluations\n", host[9], host[8]);
 #ifdef KNF_TC5_TIMING
   {
     static const char* names[10] = {"tile setup", "encode+split+store", "barriers", "layer-1 MMA wait", "h1 epilogue", "layer-2 MMA wait", "h2 epilogue+output",
@@ -692,10 +694,27 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
         }
         KNF_CUDA(cudaMemsetAsync(W.tail_cursor.p, 0, 16, st));
         const int rays_left = n_exact + n_filter;
-        const int grid = std::max(1, std::min((rays_left + kTailWarps - 1) / kTailWarps, 148 * 8));
+        const int rays_per_cta = kTailWarps * (32 / kTailGroup);  // a group of kTailGroup lanes per ray
+        const int grid = std::max(1, std::min((rays_left + rays_per_cta - 1) / rays_per_cta, 148 * 8));
+        static const bool debug_tail = std::getenv("KNF_DEBUG_TAIL") != nullptr;
+        cudaEvent_t dbg0 = nullptr, dbg1 = nullptr;
+        if (debug_tail) {
+          cudaEventCreate(&dbg0);
+          cudaEventCreate(&dbg1);
+          cudaEventRecord(dbg0, st);
+        }
         {
           ProfScope prof(F, st, SPAN_SDF_MLP);
           march_tail_kernel<<<grid, 32 * kTailWarps, 0, st>>>(T);
+        }
+        if (debug_tail) {
+          cudaEventRecord(dbg1, st);
+          cudaEventSynchronize(dbg1);
+          float tms = 0.f;
+          cudaEventElapsedTime(&tms, dbg0, dbg1);
+          fprintf(stderr, "march_tail_kernel: %d rays handed over at wavefront %d, %.3f ms\n", rays_left, w, tms);
+          cudaEventDestroy(dbg0);
+          cudaEventDestroy(dbg1);
         }
         F.stats.kernel_launches += 1;
         // the pending queues were consumed without a routing pass: leave their per-cell counts as a pass would

@@ -5,13 +5,16 @@
 // last ~17 of 34 wavefronts of the 1080p frame hold < 2 % of its evaluations and take ~1.5 ms of its ~10).  Once the live
 // rays drop below a threshold the engine hands ALL of them -- both queues -- to this kernel instead:
 //
-//   * a warp takes one ray and steps it until it is done (hit, miss, or out of steps): no routing, no queues;
-//   * lane j owns hidden unit j: its layer-1 / layer-2 pre-activation is the k-ordered fp32 FMA chain from zero plus the
-//     rounded bias add, NumPy's softplus bit for bit, and the distance is the k-ordered chain over the 32 hidden units --
+//   * a group of 8 lanes takes one ray and steps it until it is done (hit, miss, or out of steps), then claims the next: no
+//     routing, no queues; the four groups of a warp evaluate in lock step and run their march steps side by side;
+//   * lane q of a group owns hidden units 4 q .. 4 q + 3: each pre-activation is the k-ordered fp32 FMA chain from zero plus
+//     the rounded bias add, NumPy's softplus bit for bit, and the distance is the k-ordered chain over the 32 hidden units --
 //     the very arithmetic of the tile kernels (knf_mlp.cuh), so a sample's distance does not depend on which kernel
-//     evaluated it and results stay bit-identical;
-//   * weights are read straight from the cell's k-major blob (a row of W^T is one coalesced 128-byte load; consecutive
-//     steps of a ray stay in one cell, so the rows come from L1 / L2);
+//     evaluated it and results stay bit-identical.  (Round 2 started with one ray per warp, lane = hidden unit: every
+//     instruction served one evaluation -- ~900 warp instructions each, ten times the tile kernels' cost -- and the kernel
+//     was issue-bound at 0.5 ms for 47 k rays; four rays per warp share every instruction of the evaluation);
+//   * weights are read straight from the cell's k-major blob (a row of W^T is one coalesced 128-byte load per group;
+//     consecutive steps of a ray stay in one cell, so the rows come from L1 / L2);
 //   * crawling rays from the filter queue are evaluated exactly too (the filter only ever answered predicates), and CERTIFIED
 //     SKIPPING works here as in the filter kernel, with the exact distance in place of the filter's: from a sample p0 with
 //     d_exact(p0) < -(eps + delta) every further sample p of the ray in the same cell with sum_a L_a |p_a - p0_a| below
@@ -96,11 +99,16 @@ __device__ __forceinline__ bool crawl_run(RayRegs& R, const MarchState& M, int r
   return done;
 }
 
-// exact SDF distance at (x, y, z) in `cell`; all 32 lanes call it with the same point, all get the same value
-__device__ __forceinline__ float tail_eval(const float* __restrict__ blob, int lane, float x, float y, float z) {
+constexpr int kTailGroup = 8;   // lanes per ray
+constexpr int kTailUnits = kHidden / kTailGroup;  // hidden units per lane
+static_assert(kTailUnits == 4, "tail_eval is written for four hidden units per lane (float4 weight rows)");
+
+// exact SDF distance at (x, y, z) in the cell whose blob is `blob`: the 8 lanes [gbase, gbase + 8) call it with the same
+// point and all get the same value; the four groups of a warp call it together (the shuffles are warp-wide)
+__device__ __forceinline__ float tail_eval(const float* __restrict__ blob, int q, int gbase, float x, float y, float z) {
   using Blob = SdfBlob;
   const float pi_f = 3.14159274101257324e+00f;  // float32(np.pi)
-  // nn.fourier_encode, operation for operation (every lane computes the 39 features of the shared point)
+  // nn.fourier_encode, operation for operation (every lane computes the 39 features of its group's point)
   float f[kSdfIn];
   f[0] = x; f[1] = y; f[2] = z;
   float s[3], c[3];
@@ -119,48 +127,90 @@ __device__ __forceinline__ float tail_eval(const float* __restrict__ blob, int l
       s[a] = ns;
     }
   }
-  // layer 1: lane = hidden unit; acc = fma(x_k, W1[j][k], acc), k ascending, from zero; then the rounded bias add
-  const float* w1 = blob + Blob::w1 + lane;
-  float acc = 0.0f;
+  // layer 1: acc_j = fma(x_k, W1[j][k], acc_j), k ascending, from zero, for the lane's units j = 4 q + u; then the rounded bias add
+  const float4* w1 = reinterpret_cast<const float4*>(blob + Blob::w1) + q;  // row k of W1^T: 32 floats = 8 float4, the lane's is number q
+  float acc[kTailUnits] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-  for (int k = 0; k < kSdfIn; k++) acc = __fmaf_rn(f[k], __ldg(w1 + k * kHidden), acc);
-  float2 h = softplus_np_f2(splat(__fadd_rn(acc, __ldg(blob + Blob::b1 + lane))));
-  const float h1 = h.x;
-  // layer 2: h1[k] comes from lane k
-  const float* w2 = blob + Blob::w2 + lane;
-  acc = 0.0f;
+  for (int k = 0; k < kSdfIn; k++) {
+    const float4 w = __ldg(w1 + k * (kHidden / 4));
+    acc[0] = __fmaf_rn(f[k], w.x, acc[0]);
+    acc[1] = __fmaf_rn(f[k], w.y, acc[1]);
+    acc[2] = __fmaf_rn(f[k], w.z, acc[2]);
+    acc[3] = __fmaf_rn(f[k], w.w, acc[3]);
+  }
+  float4 b = __ldg(reinterpret_cast<const float4*>(blob + Blob::b1) + q);
+  float2 h[2] = {make_float2(__fadd_rn(acc[0], b.x), __fadd_rn(acc[1], b.y)), make_float2(__fadd_rn(acc[2], b.z), __fadd_rn(acc[3], b.w))};
+  softplus_np_f2xN<2>(h);
+  const float h1[kTailUnits] = {h[0].x, h[0].y, h[1].x, h[1].y};
+  // layer 2: h1[k] comes from lane k / 4 of the group, component k % 4
+  const float4* w2 = reinterpret_cast<const float4*>(blob + Blob::w2) + q;
+  acc[0] = acc[1] = acc[2] = acc[3] = 0.0f;
 #pragma unroll
-  for (int k = 0; k < kHidden; k++) acc = __fmaf_rn(__shfl_sync(0xffffffffu, h1, k), __ldg(w2 + k * kHidden), acc);
-  h = softplus_np_f2(splat(__fadd_rn(acc, __ldg(blob + Blob::b2 + lane))));
-  const float h2 = h.x;
-  // output 0: the distance
+  for (int sl = 0; sl < kTailGroup; sl++)
+#pragma unroll
+    for (int u = 0; u < kTailUnits; u++) {
+      const float hv = __shfl_sync(0xffffffffu, h1[u], gbase + sl);
+      const float4 w = __ldg(w2 + (kTailUnits * sl + u) * (kHidden / 4));
+      acc[0] = __fmaf_rn(hv, w.x, acc[0]);
+      acc[1] = __fmaf_rn(hv, w.y, acc[1]);
+      acc[2] = __fmaf_rn(hv, w.z, acc[2]);
+      acc[3] = __fmaf_rn(hv, w.w, acc[3]);
+    }
+  b = __ldg(reinterpret_cast<const float4*>(blob + Blob::b2) + q);
+  h[0] = make_float2(__fadd_rn(acc[0], b.x), __fadd_rn(acc[1], b.y));
+  h[1] = make_float2(__fadd_rn(acc[2], b.z), __fadd_rn(acc[3], b.w));
+  softplus_np_f2xN<2>(h);
+  const float h2[kTailUnits] = {h[0].x, h[0].y, h[1].x, h[1].y};
+  // output 0: the distance, the k-ordered chain over the 32 hidden units (every lane of the group runs it)
   const float* w3 = blob + Blob::w3;
-  acc = 0.0f;
+  float d = 0.0f;
 #pragma unroll
-  for (int k = 0; k < kHidden; k++) acc = __fmaf_rn(__shfl_sync(0xffffffffu, h2, k), __ldg(w3 + k * kSdfOutPad), acc);
-  return __fadd_rn(acc, __ldg(blob + Blob::b3));
+  for (int sl = 0; sl < kTailGroup; sl++)
+#pragma unroll
+    for (int u = 0; u < kTailUnits; u++) {
+      const float hv = __shfl_sync(0xffffffffu, h2[u], gbase + sl);
+      d = __fmaf_rn(hv, __ldg(w3 + (kTailUnits * sl + u) * kSdfOutPad), d);
+    }
+  return __fadd_rn(d, __ldg(blob + Blob::b3));
 }
 
+#ifndef KNF_TAIL_MIN_BLOCKS
+#define KNF_TAIL_MIN_BLOCKS 3
+#endif
 constexpr int kTailWarps = 4;
-static __global__ void __launch_bounds__(32 * kTailWarps) march_tail_kernel(MarchTailArgs A) {
-  const int lane = threadIdx.x & 31;
+static __global__ void __launch_bounds__(32 * kTailWarps, KNF_TAIL_MIN_BLOCKS) march_tail_kernel(MarchTailArgs A) {
+  const int lane = threadIdx.x & 31, q = lane & (kTailGroup - 1), gbase = lane & ~(kTailGroup - 1);
   const int n_a = A.ctr_a->n_requests, n_b = A.ctr_b ? A.ctr_b->n_requests : 0;
-  unsigned long long evals = 0, skipped = 0;
+  const double dt = A.M.step_scale * (A.M.eps / 2);
+  unsigned long long evals = 0, skipped = 0, rays_done = 0;  // per group (counted in its lane 0)
+  bool have = false, exhausted = false;  // the group holds a live ray / the queue has run dry
+  int ray = 0, cell = 0;
+  float4 pt = make_float4(0.f, 0.f, 0.f, 0.f);
+  RayRegs rr;
   for (;;) {
-    int i = 0;
-    if (lane == 0) i = atomicAdd(A.cursor, 1);
-    i = __shfl_sync(0xffffffffu, i, 0);
-    if (i >= n_a + n_b) break;
-    const bool from_a = i < n_a;
-    const int slot = from_a ? i : i - n_a;
-    const int ray = (from_a ? A.live_a : A.live_b)[slot];
-    float4 pt = (from_a ? A.pt_a : A.pt_b)[slot];
-    int cell = (from_a ? A.cell_a : A.cell_b)[slot];
-    RayRegs rr;
-    ray_load(rr, A.M, ray);
-    const double dt = A.M.step_scale * (A.M.eps / 2);
-    for (;;) {
-      const float d = tail_eval(A.blobs + (size_t)cell * SdfBlob::floats, lane, pt.x, pt.y, pt.z);
+    // ---- groups without a ray claim the next one --------------------------------------------------------------------
+    int i = -1;
+    if (!have && !exhausted && q == 0) i = atomicAdd(A.cursor, 1);
+    i = __shfl_sync(0xffffffffu, i, gbase);
+    if (!have && !exhausted) {
+      if (i < n_a + n_b) {
+        const bool from_a = i < n_a;
+        const int slot = from_a ? i : i - n_a;
+        ray = (from_a ? A.live_a : A.live_b)[slot];
+        pt = (from_a ? A.pt_a : A.pt_b)[slot];
+        cell = (from_a ? A.cell_a : A.cell_b)[slot];
+        ray_load(rr, A.M, ray);
+        rays_done += 1;
+        have = true;
+      } else {
+        exhausted = true;
+      }
+    }
+    if (!__any_sync(0xffffffffu, have)) break;
+    // ---- one exact evaluation per group, in lock step (a group without a ray evaluates cell 0 at the origin: finite, ignored)
+    const float d = tail_eval(A.blobs + (size_t)(have ? cell : 0) * SdfBlob::floats, q, gbase, have ? pt.x : 0.f, have ? pt.y : 0.f,
+                              have ? pt.z : 0.f);
+    if (have) {
       evals += 1;
       double t_next = 0.0;
       double safe_below = -INFINITY;
@@ -169,10 +219,9 @@ static __global__ void __launch_bounds__(32 * kTailWarps) march_tail_kernel(Marc
         fc = reinterpret_cast<const float*>(A.fconst + (size_t)cell * A.fconst_stride);
         safe_below = -(A.M.eps + (double)__ldg(fc + A.off_delta / 4));  // delta = +inf (filter off for the cell): never below
       }
-      // every lane steps its copy of the ray: same writes, same values
-      int code = ray_step(rr, A.M, ray, d, t_next, safe_below);
-      if (code == STEP_DONE) break;
-      bool known_cell = false;
+      // every lane of the group steps its copy of the ray: same writes, same values
+      const int code = ray_step(rr, A.M, ray, d, t_next, safe_below);
+      bool done = code == STEP_DONE, known_cell = false;
       if (code == STEP_FILTER) {
         // ---- certified skipping from p0 = pt, d_exact(p0) = d < -(eps + delta): the logic of march_tc5_kernel ---------------
         const float lip[3] = {__ldg(fc + A.off_lip / 4), __ldg(fc + A.off_lip / 4 + 1), __ldg(fc + A.off_lip / 4 + 2)};
@@ -191,7 +240,6 @@ static __global__ void __launch_bounds__(32 * kTailWarps) march_tail_kernel(Marc
         }
         const float room = p0_in ? __fmul_rd(__fsub_rd(__double2float_rd(safe_below), d), 0.99999f) : 0.0f;
         const unsigned long long skipped_before = skipped;
-        bool done = false;
         if (room > 0.0f) {
           // part 1: closed-form run (per axis |p_j - p0| <= j dt |d_a| (1 + 2^-20) + two fp32 roundings; 2 samples short of
           // the cell exit and of the Lipschitz budget, scaled by 0.999 against the fp32 arithmetic here)
@@ -224,21 +272,33 @@ static __global__ void __launch_bounds__(32 * kTailWarps) march_tail_kernel(Marc
           done = crawl_run(rr, A.M, ray, 1, dt, skipped);
           t_next = rr.t;
         }
-        if (done) break;
         // t_prev moved past samples nobody evaluated: d_prev (exact, at p0) is now only good as a predicate, and a ray that
         // converges next re-evaluates it at t_prev first (PH_RECHECK), as after filtered steps
         if (skipped != skipped_before) rr.approx = 1;
-      } else {
+      } else if (!done) {
         pt.x = __double2float_rn(rr.o[0] + t_next * rr.d[0]);
         pt.y = __double2float_rn(rr.o[1] + t_next * rr.d[1]);
         pt.z = __double2float_rn(rr.o[2] + t_next * rr.d[2]);
       }
-      if (!known_cell) cell = cell_of_quick(pt.x, pt.y, pt.z, A.G.lo, A.G.hi, A.cell_scale, A.G.resolution);
+      if (done) have = false;
+      else if (!known_cell) cell = cell_of_quick(pt.x, pt.y, pt.z, A.G.lo, A.G.hi, A.cell_scale, A.G.resolution);
     }
+    __syncwarp();
   }
-  if (lane == 0 && evals && A.eval_counter) {
-    atomicAdd(A.eval_counter, evals);
-    if (skipped) atomicAdd(A.eval_counter + 6, skipped);  // certified steps (same counter as the filter kernel's)
+  if (A.eval_counter) {
+    if (q != 0) evals = skipped = rays_done = 0;  // one count per group
+#pragma unroll
+    for (int off = 16; off >= kTailGroup; off >>= 1) {
+      evals += __shfl_xor_sync(0xffffffffu, evals, off);
+      skipped += __shfl_xor_sync(0xffffffffu, skipped, off);
+      rays_done += __shfl_xor_sync(0xffffffffu, rays_done, off);
+    }
+    if (lane == 0 && evals) {
+      atomicAdd(A.eval_counter, evals);
+      atomicAdd(A.eval_counter + 8, evals);  // diagnostics (KNF_DEBUG_TAIL): the tail's own evaluations and rays
+      atomicAdd(A.eval_counter + 9, rays_done);
+      if (skipped) atomicAdd(A.eval_counter + 6, skipped);  // certified steps (same counter as the filter kernel's)
+    }
   }
 }
 
