@@ -225,7 +225,11 @@ def run_reference(args, rank, world):
     sample_rps_one = w * h / min(one)
     full = None
     if os.environ.get("BENCH_REF_FULL", "1") != "0":
-        threads_full = ncpu if sample_rps_all >= 1.3 * sample_rps_one else 1  # threads barely help the reference (GIL + BLAS oversubscription) and hurt on large bands
+        # The reference's own threading (KNF_THREADS row bands, each calling multi-threaded BLAS) helps on small rasters and HURTS on
+        # the full frame: measured on this pool, 16 threads give 1.5x on the 480x270 sample but 0.5x at 1920x1080 (155-168 s vs
+        # 83 s, profiles/bench_r2_reference.json / bench_reference_r2_final2.json).  The full frame is rendered with the setting
+        # that is the reference's best there: all threads only if they at least double the sample rate.
+        threads_full = ncpu if sample_rps_all >= 2.0 * sample_rps_one else 1
         dt, kind, hitf = cpu_frame_seconds(W, H, args.warmup, threads_full)
         full = {"seconds": dt, "threads": threads_full, "hit_fraction": hitf, "fps": 1.0 / dt, "krays_per_s": W * H / dt / 1e3}
     fps = full["fps"] if full else max(sample_rps_all, sample_rps_one) / (W * H)

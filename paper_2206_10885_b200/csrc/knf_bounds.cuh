@@ -58,8 +58,10 @@ constexpr int kLipMaxFine = 4;
 
 #ifndef KNF_BOUNDS_LAYOUT_ONLY
 struct LipWarpScratch {
-  double phi_c[40], phi_r[40];
-  double va[kHidden], vb[kHidden], vc[kHidden], vd[kHidden];
+  // (centre, radius) / paired vectors interleaved: every broadcast read of a pair is one 16-byte shared-memory wavefront
+  double2 phi[40];          // .x centre, .y radius
+  double2 vab[kHidden];     // layer 2: (h1c, h1r); then (c2 w3, r2 |w3|)
+  double2 vcd[kHidden];     // (c1 o g, c1 o g')
   double trig[3 * kLipMaxFine][2 * kSdfFreqs];  // [axis * fine + i][2 o] = sin(2^o pi x_i), [2 o + 1] = cos
 };
 
@@ -119,7 +121,7 @@ __device__ __forceinline__ void lip_act_range(double zc, double zr, double& sgc,
   spr = 0.5 * (hu - hl) * (1.0 + 1e-12) + 1e-13;
 }
 
-static __global__ void __launch_bounds__(32 * kLipWarps) lip_bound_kernel(LipArgs A) {
+static __global__ void __launch_bounds__(32 * kLipWarps, 2) lip_bound_kernel(LipArgs A) {
   extern __shared__ __align__(16) unsigned char lip_smem_raw[];
   LipSmem& S = *reinterpret_cast<LipSmem*>(lip_smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -165,12 +167,10 @@ static __global__ void __launch_bounds__(32 * kLipWarps) lip_bound_kernel(LipArg
       const double xlo = elo[a] + wsub[a] * (double)si[a], xhi = elo[a] + wsub[a] * (double)(si[a] + 1);
       double sc, sr, cc2, cr;
       lip_trig_range(f * xlo, f * xhi, sc, sr, cc2, cr);
-      W.phi_c[3 + 6 * o + a] = sc; W.phi_r[3 + 6 * o + a] = sr;
-      W.phi_c[6 + 6 * o + a] = cc2; W.phi_r[6 + 6 * o + a] = cr;
-      if (lane < 3) {  // the raw coordinate (a == lane)
-        W.phi_c[lane] = elo[lane] + wsub[lane] * ((double)si[lane] + 0.5);
-        W.phi_r[lane] = 0.5 * wsub[lane] * (1.0 + 1e-12) + 1e-13;
-      }
+      W.phi[3 + 6 * o + a] = make_double2(sc, sr);
+      W.phi[6 + 6 * o + a] = make_double2(cc2, cr);
+      if (lane < 3)  // the raw coordinate (a == lane)
+        W.phi[lane] = make_double2(elo[lane] + wsub[lane] * ((double)si[lane] + 0.5), 0.5 * wsub[lane] * (1.0 + 1e-12) + 1e-13);
     } else if (lane < 18 + 3 * fine) {
       // Taylor sample points of g_a: sin / cos of 2^o pi x_i by one sincos and the double-angle recurrence
       const int q = lane - 18, a = q / fine, i = q % fine;
@@ -192,37 +192,38 @@ static __global__ void __launch_bounds__(32 * kLipWarps) lip_bound_kernel(LipArg
 #pragma unroll 13
     for (int kk = 0; kk < kSdfIn; kk++) {
       const double w = S.w1t[kk * kHidden + lane];
-      z1c = fma(w, W.phi_c[kk], z1c);
-      z1r = fma(fabs(w), W.phi_r[kk], z1r);
+      const double2 ph = W.phi[kk];
+      z1c = fma(w, ph.x, z1c);
+      z1r = fma(fabs(w), ph.y, z1r);
     }
     z1r = fma(1e-12, fabs(z1c) + z1r, z1r) + 1e-13;
     double c1, r1, h1c, h1r;
     lip_act_range(z1c, z1r, c1, r1, h1c, h1r);
-    W.va[lane] = h1c;
-    W.vb[lane] = h1r;
+    W.vab[lane] = make_double2(h1c, h1r);
     __syncwarp();
     // ---- layer 2 ---------------------------------------------------------------------------------------------------
     double z2c = S.b2[lane], z2r = 0.0;
 #pragma unroll 8
     for (int n = 0; n < kHidden; n++) {
       const double w = S.w2t[n * kHidden + lane];
-      z2c = fma(w, W.va[n], z2c);
-      z2r = fma(fabs(w), W.vb[n], z2r);
+      const double2 hh = W.vab[n];
+      z2c = fma(w, hh.x, z2c);
+      z2r = fma(fabs(w), hh.y, z2r);
     }
     z2r = fma(1e-12, fabs(z2c) + z2r, z2r) + 1e-13;
     double c2, r2, h2c_unused, h2r_unused;
     lip_act_range(z2c, z2r, c2, r2, h2c_unused, h2r_unused);
     const double rw = r2 * aw3l;  // r2_m |w3_m|
     __syncwarp();
-    W.va[lane] = c2 * w3l;
-    W.vb[lane] = rw;
+    W.vab[lane] = make_double2(c2 * w3l, rw);
     __syncwarp();
     double vt = 0.0, q = 0.0;  // v~_n = sum_m W2[m][n] c2_m w3_m ; q_n = sum_m |W2[m][n]| r2_m |w3_m|
 #pragma unroll 8
     for (int m = 0; m < kHidden; m++) {
       const double w = S.w2r[m * kHidden + lane];
-      vt = fma(w, W.va[m], vt);
-      q = fma(fabs(w), W.vb[m], q);
+      const double2 uu = W.vab[m];
+      vt = fma(w, uu.x, vt);
+      q = fma(fabs(w), uu.y, q);
     }
     const double nrw = sqrt(lip_warp_sum(rw * rw));
     const double avt_r1 = fabs(vt) * r1;
@@ -246,15 +247,15 @@ static __global__ void __launch_bounds__(32 * kLipWarps) lip_bound_kernel(LipArg
         }
         __syncwarp();
         const double cg = c1 * g, cgp = c1 * gp;
-        W.vc[lane] = cg;
-        W.vd[lane] = cgp;
+        W.vcd[lane] = make_double2(cg, cgp);
         __syncwarp();
         double u = 0.0, up = 0.0;  // (W2 (c1 o g))_m, lane = m
 #pragma unroll 8
         for (int n = 0; n < kHidden; n++) {
           const double w = S.w2t[n * kHidden + lane];
-          u = fma(w, W.vc[n], u);
-          up = fma(w, W.vd[n], up);
+          const double2 cc12 = W.vcd[n];
+          u = fma(w, cc12.x, u);
+          up = fma(w, cc12.y, up);
         }
         const double rg = r1 * fabs(g), rgp = r1 * fabs(gp);
         // lane-wise terms of the sums (the Taylor combination Phi(g) + h Phi(g') is formed before reducing where it is linear)
