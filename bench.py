@@ -574,10 +574,11 @@ def main():
             "tensor_issued_tflops": (stats["filter_evals"] * 15360 / (stats["filter_ms"] * 1e-3) / 1e12) if stats["filter_ms"] > 0 else None,
             "evals_per_s": filter_evals_per_s,
             "binding_pipe": {"name": "instruction issue (CUDA-core work around the MMAs: 64 softplus, 71 operand splits, 39 Fourier features, the fp64 march step and the certified-skip runs)",
-                             "issue_slots_busy_ncu": 0.61, "fma_pipe_busy_ncu": 0.38, "alu_pipe_busy_ncu": 0.36, "xu_pipe_busy_ncu": 0.29, "tensor_pipe_busy_ncu": 0.09,
+                             "issue_slots_busy_ncu": 0.51, "fma_pipe_busy_ncu": 0.35, "alu_pipe_busy_ncu": 0.27, "xu_pipe_busy_ncu": 0.27, "tensor_pipe_busy_ncu": 0.09,
+                             "top_stalls_per_issue_ncu": {"barrier": 2.72, "wait": 1.68, "long_scoreboard": 1.49},
                              "xu_roof_evals_per_s": xu_peak_evals, "frac_of_xu_roof": (filter_evals_per_s / xu_peak_evals) if filter_evals_per_s else None,
-                             "note": "ncu --set full of a dense launch (profiles/ncu_r2b_tc5_filter.summary.txt): ~1200 CUDA-core instructions per evaluation surround 10 "
-                                     "tcgen05.mma per 128 evaluations, and since the refined Lipschitz bounds each evaluation is followed by ~11 certified crawl steps "
+                             "note": "ncu --set full of a dense launch (profiles/ncu_r2_final2_tc5_filter.summary.txt): ~1200 CUDA-core instructions per evaluation surround 10 "
+                                     "tcgen05.mma per 128 evaluations, and since the refined Lipschitz bounds each evaluation is followed by ~9 certified crawl steps "
                                      "(closed-form run + per-sample checks) that cost issue slots and no flop -- the fraction of tensor peak is not what limits this kernel"},
             "certified_steps_per_evaluation": stats["filter_skipped"] / max(stats["filter_evals"], 1),
             "note": "achieved = filter evaluations x 5120 algorithmic flop / summed CUDA-event time of the filter launches; each evaluation issues 3 fp16 piece products "
