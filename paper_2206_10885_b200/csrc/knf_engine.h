@@ -90,7 +90,7 @@ struct Field {
   int filter_cells_off = 0;            // cells whose activations can leave the fp16 range: delta = +inf, the filter decides nothing there
   int sparse_max_inner = 8;            // residency cap and keep rule of sparse exact wavefronts (KNF_SPARSE_INNER / KNF_SPARSE_KEEP)
   int sparse_keep_div = 2;   // measured: (16, 4) gains 3 % on the distilled frame and loses 1.3 % on the random-init one; (32, 8) and up lose more
-  int sparse_div = 8;                  // a wavefront is sparse when its exact queue holds < n / sparse_div rays (KNF_SPARSE_DIV)
+  int sparse_div = 6;                  // a wavefront is sparse when its exact queue holds < n / sparse_div rays (KNF_SPARSE_DIV; 8 until round 2b: 6 / 4 / 3 take 3 % off the trained 16^3 frame and leave the others unchanged)
   bool sparse_small_kernel = true;     // exact march: sparse wavefronts by march_small_kernel (KNF_SPARSE_SMALL=0 disables)
   bool exact_mid = true;               // dense exact wavefronts by march_mid_kernel (32-request tiles, 13 CTAs per SM) instead of march_warp_kernel (KNF_EXACT_MID=0)
   int scan_split = 65536;              // grids with more cells scan in chunks over many CTAs (two launches) instead of one CTA per queue (KNF_SCAN_SPLIT)
