@@ -111,7 +111,7 @@ __device__ __forceinline__ void march_exact_tile(const MarchTileArgs& A, SmemT& 
 
   for (int inner = 0;; inner++) {
     if (SMALL) {
-      if (lane < PTS) encode_into<kSdfFreqs, PLD>(X, 0, lane, px[0], py[0], pz[0]);
+      if (lane < PTS) encode_into_swz<kSdfFreqs, PLD>(X, lane, px[0], py[0], pz[0]);
     } else {
 #pragma unroll
       for (int q = 0; q < NQ; q++) encode_into<kSdfFreqs>(X, 0, col[q], px[q], py[q], pz[q]);

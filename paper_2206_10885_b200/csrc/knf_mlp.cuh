@@ -160,6 +160,49 @@ static __device__ __noinline__ void softplus_panel(float* __restrict__ panel, in
   }
 }
 
+// Column swizzle of the compact panels (mid: 32 columns, small: 16).  A lane of the register-tiled layers stores its
+// pre-activations as float4 at (row = neuron, columns 4 pg ..): with the plain layout the row strides 8 * 36 and 4 * 20 words
+// are multiples of 32 and 16 banks, so the lanes of one 8-lane store phase that differ only in their neuron group hit the same
+// banks -- 4-way conflicts on every STS.128 of store_hidden_mid / _small (ncu: 16 % of the mid kernel's shared-memory
+// wavefronts were excess).  XOR-ing the float4-column index with a function of row / 8 spreads them over all banks; every
+// reader and writer of these panels goes through panel_col (the in-place softplus does not care where a column lives).
+template <int PLD>
+__device__ __forceinline__ int panel_col4(int row, int c4) { return c4; }  // physical float4-column of logical float4-column c4 in `row` (other strides: plain)
+constexpr int kMidPanelLdFwd = 36, kSmallPanelLdFwd = 20;  // (= kMidPanelLd / kSmallPanelLd, defined with their tile shapes below)
+template <>
+__device__ __forceinline__ int panel_col4<kMidPanelLdFwd>(int row, int c4) { return c4 ^ (((row >> 3) & 3) << 1); }
+template <>
+__device__ __forceinline__ int panel_col4<kSmallPanelLdFwd>(int row, int c4) { return c4 ^ ((row >> 3) & 3); }
+template <int PLD>
+__device__ __forceinline__ int panel_col(int row, int p) { return 4 * panel_col4<PLD>(row, p >> 2) + (p & 3); }
+
+// nn.fourier_encode (nn.py:66-93) of a 3-vector into rows [0, 3 + 6*L) of a swizzled compact panel at logical column p.
+template <int L, int PLD>
+static __device__ __noinline__ void encode_into_swz(float* __restrict__ panel, int p, float x, float y, float z) {
+  const float pi_f = 3.14159274101257324e+00f;  // float32(np.pi)
+  panel[0 * PLD + panel_col<PLD>(0, p)] = x;
+  panel[1 * PLD + panel_col<PLD>(1, p)] = y;
+  panel[2 * PLD + panel_col<PLD>(2, p)] = z;
+  float s[3], c[3];
+  np_sincosf(__fmul_rn(pi_f, x), s[0], c[0]);
+  np_sincosf(__fmul_rn(pi_f, y), s[1], c[1]);
+  np_sincosf(__fmul_rn(pi_f, z), s[2], c[2]);
+#pragma unroll
+  for (int o = 0; o < L; o++) {
+    const int r = 3 + 6 * o;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      panel[(r + a) * PLD + panel_col<PLD>(r + a, p)] = s[a];
+      panel[(r + 3 + a) * PLD + panel_col<PLD>(r + 3 + a, p)] = c[a];
+      float two_s = __fmul_rn(2.0f, s[a]);
+      float ns = __fmul_rn(two_s, c[a]);                      // 2 s c
+      float nc = __fsub_rn(1.0f, __fmul_rn(two_s, s[a]));     // 1 - 2 s s
+      s[a] = ns;
+      c[a] = nc;
+    }
+  }
+}
+
 // nn.fourier_encode (nn.py:66-93) of a 3-vector into panel rows [row0, row0 + 3 + 6*L) at column p.
 // __noinline__ (one copy per instantiation): three sin/cos evaluations and the recurrence are ~300 instructions, and
 // the exact kernel used to inline them three times.
@@ -205,6 +248,7 @@ __device__ __forceinline__ void zero_pad_rows(float* __restrict__ X, int lane) {
 constexpr int kSmallTilePts = 16;
 
 constexpr int kSmallPanelLd = kSmallTilePts + 4;  // 20: row stride of the compact panel of the small-tile kernel
+static_assert(kSmallPanelLd == kSmallPanelLdFwd, "panel_col4 is specialised for this stride");
 
 template <int K, int PLD>
 __device__ __forceinline__ void layer_4x4(const float* __restrict__ In, const float* __restrict__ Wt, int pg, int ng,
@@ -215,10 +259,10 @@ __device__ __forceinline__ void layer_4x4(const float* __restrict__ In, const fl
   for (int i = 0; i < 2; i++)
 #pragma unroll
     for (int j = 0; j < 4; j++) acc[i][j] = make_float2(0.0f, 0.0f);
-  const float* xp = In + pg * 4;
   const float* wp = Wt + ng * 4;
 #pragma unroll 1
   for (int k0 = 0; k0 < K; k0 += 8) {
+    const float* xp = In + 4 * panel_col4<PLD>(k0, pg);  // (rows k0 .. k0 + 7 share one swizzle)
 #pragma unroll
     for (int kk = 0; kk < 8; kk++) {
       const float4 x = *reinterpret_cast<const float4*>(xp + (k0 + kk) * kPanelLd);
@@ -247,7 +291,7 @@ __device__ __forceinline__ void store_hidden_small(float2 (&acc)[2][4], const fl
       v0 = make_float2(fmaxf(v0.x, 0.0f), fmaxf(v0.y, 0.0f));
       v1 = make_float2(fmaxf(v1.x, 0.0f), fmaxf(v1.y, 0.0f));
     }
-    *reinterpret_cast<float4*>(Out + neuron * kPanelLd + pg * 4) = make_float4(v0.x, v0.y, v1.x, v1.y);
+    *reinterpret_cast<float4*>(Out + neuron * kPanelLd + 4 * panel_col4<PLD>(neuron, pg)) = make_float4(v0.x, v0.y, v1.x, v1.y);
   }
 }
 
@@ -298,6 +342,7 @@ __device__ __forceinline__ void hidden_layers_small(float* __restrict__ X, const
 // output is still the k-ordered FMA chain from zero followed by the rounded bias add: same bits as the other shapes.
 constexpr int kMidTilePts = 32;
 constexpr int kMidPanelLd = kMidTilePts + 4;  // 36
+static_assert(kMidPanelLd == kMidPanelLdFwd, "panel_col4 is specialised for this stride");
 
 template <int K, int PLD>
 __device__ __forceinline__ void layer_4x8(const float* __restrict__ In, const float* __restrict__ Wt, int pg, int ng, float2 (&acc)[2][8]) {
@@ -306,10 +351,10 @@ __device__ __forceinline__ void layer_4x8(const float* __restrict__ In, const fl
   for (int i = 0; i < 2; i++)
 #pragma unroll
     for (int j = 0; j < 8; j++) acc[i][j] = make_float2(0.0f, 0.0f);
-  const float* xp = In + pg * 4;
   const float* wp = Wt + ng * 8;
 #pragma unroll 1
   for (int k0 = 0; k0 < K; k0 += 8) {
+    const float* xp = In + 4 * panel_col4<PLD>(k0, pg);  // (rows k0 .. k0 + 7 share one swizzle)
 #pragma unroll
     for (int kk = 0; kk < 8; kk++) {
       const float4 x = *reinterpret_cast<const float4*>(xp + (k0 + kk) * PLD);
@@ -338,7 +383,7 @@ __device__ __forceinline__ void store_hidden_mid(float2 (&acc)[2][8], const floa
       v0 = make_float2(fmaxf(v0.x, 0.0f), fmaxf(v0.y, 0.0f));
       v1 = make_float2(fmaxf(v1.x, 0.0f), fmaxf(v1.y, 0.0f));
     }
-    *reinterpret_cast<float4*>(Out + neuron * PLD + pg * 4) = make_float4(v0.x, v0.y, v1.x, v1.y);
+    *reinterpret_cast<float4*>(Out + neuron * PLD + 4 * panel_col4<PLD>(neuron, pg)) = make_float4(v0.x, v0.y, v1.x, v1.y);
   }
 }
 
@@ -387,8 +432,12 @@ __device__ __forceinline__ float output_distance_col(const float* __restrict__ X
                                                      const float* __restrict__ B3, int p) {
   constexpr int kPanelLd = PLD;
   float d = 0.0f;
-#pragma unroll 8
-  for (int k = 0; k < kHidden; k++) d = __fmaf_rn(X[k * kPanelLd + p], W3[k * N3P], d);
+#pragma unroll
+  for (int k0 = 0; k0 < kHidden; k0 += 8) {
+    const int pc = panel_col<PLD>(k0, p);  // the swizzled column of rows k0 .. k0 + 7
+#pragma unroll
+    for (int kk = 0; kk < 8; kk++) d = __fmaf_rn(X[(k0 + kk) * kPanelLd + pc], W3[(k0 + kk) * N3P], d);
+  }
   return __fadd_rn(d, B3[0]);
 }
 
