@@ -567,6 +567,8 @@ int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
   if (const char* env = std::getenv("KNF_FILTER_GRID")) F.filter_grid_ctas = std::max(1, std::atoi(env));
   if (const char* env = std::getenv("KNF_FILTER_SKIP_CAP")) F.filter_skip_cap = std::max(0, std::atoi(env));
   if (const char* env = std::getenv("KNF_OVERLAP")) F.overlap_queues = std::atoi(env) != 0;
+  if (const char* env = std::getenv("KNF_EXACT_GRID")) F.exact_grid_ctas = std::max(0, std::atoi(env));
+  if (const char* env = std::getenv("KNF_EXACT_FIRST")) F.exact_first = std::atoi(env) != 0;
   if (const char* env = std::getenv("KNF_FILTER_FIRST")) F.filter_first = std::atoi(env) != 0;
   if (const char* env = std::getenv("KNF_TAIL_SKIP")) F.tail_skip = std::atoi(env) != 0;
   if (const char* env = std::getenv("KNF_TAIL")) F.tail_threshold = std::max(0, std::atoi(env));

@@ -542,6 +542,18 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
   // sample, or -- a filter-queue ray whose sample the filter cannot decide -- moves to the next exact queue unchanged and
   // advances there, so 2 * max_steps + 6 bounds the count; tile residency usually finishes in far fewer, which the host
   // learns by polling the request counts.
+  // KNF_DEBUG_TIMELINE=1: events at the phase boundaries of every wavefront, printed (relative to the march's start) after the march
+  static const bool debug_timeline = std::getenv("KNF_DEBUG_TIMELINE") != nullptr;
+  struct Mark { const char* what; int w; cudaEvent_t ev; };
+  std::vector<Mark> marks;
+  auto mark = [&](const char* what, int w, cudaStream_t s_) {
+    if (!debug_timeline) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s_);
+    marks.push_back({what, w, e});
+  };
+  mark("start", -1, st);
   F.prof_chain = true;  // spans inside the loop are back to back on `st`: one shared event between neighbours
   F.prof_last_end = (size_t)-1;
   size_t live_upper = (size_t)n;  // upper bound on the size of any queue from here on: sizes the routing and tile grids
@@ -589,15 +601,17 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     const bool small_only = exact_mode && exact_sparse && F.sparse_small_kernel;
     const bool mid = exact_mode && !small_only && F.exact_mid;
     R.small_tiles = small_only ? 2 : (mid ? 4 : 0);  // dense wavefronts: <= 32-request tiles for march_mid_kernel (or 64 for march_warp_kernel); sparse: <= 16 for march_small_kernel
+    mark("wavefront", w, st);
     if (filter_pass) KNF_TRY(launch_scan_scatter2(F, Rf, R, live_upper, st));
     else KNF_TRY(launch_scan_scatter(F, R, live_upper, st));
+    mark("routed", w, st);
     cudaStream_t st_exact = st;
     if (filter_pass && F.overlap_queues && F.side_stream) {
       KNF_CUDA(cudaEventRecord(F.ev_fork, st));
       KNF_CUDA(cudaStreamWaitEvent(F.side_stream, F.ev_fork, 0));
       st_exact = F.side_stream;
     }
-    if (filter_pass) {
+    auto launch_filter = [&]() -> int {
       MarchTileArgs Af = A;
       Af.P.blobs = reinterpret_cast<const float*>(F.sdf_mmah_blobs);
       Af.P.perm = Rf.perm;
@@ -622,14 +636,22 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
         }
       }
       F.stats.kernel_launches += 1;
-    }
-    A.P.blobs = F.sdf_blobs;
-    A.P.perm = R.perm;
-    A.P.tiles = R.tiles;
-    A.P.ctr = R.ctr;
-    A.P.req_pt = R.req_pt;
-    A.P.sorted = R.sorted;
-    A.live_in = M.live[cur];
+      mark("filter done", w, st);
+      return 0;
+    };
+    // the exact queue's launch; beside a filter pass its grid may be capped (KNF_EXACT_GRID CTAs per SM) so that both kernels'
+    // CTAs are resident together instead of the first-launched one holding every register of the SM until it drains
+    const bool beside_filter = filter_pass && st_exact != st;
+    auto exact_ctas = [&](int full) { return beside_filter && F.exact_grid_ctas > 0 ? std::min(full, F.exact_grid_ctas) : full; };
+    auto launch_exact = [&]() -> int {
+    MarchTileArgs& Ax = A;
+    Ax.P.blobs = F.sdf_blobs;
+    Ax.P.perm = R.perm;
+    Ax.P.tiles = R.tiles;
+    Ax.P.ctr = R.ctr;
+    Ax.P.req_pt = R.req_pt;
+    Ax.P.sorted = R.sorted;
+    Ax.live_in = M.live[cur];
     {
       ProfScope prof(F, st_exact, SPAN_SDF_MLP);
       if (F.precision == KNF_PRECISION_TENSOR_BF16X3) {
@@ -643,12 +665,22 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
         // rather than paying another routing round trip (the long tail of a frame is a chain of such round trips)
         A.max_inner = F.sparse_max_inner;
         A.keep_div = F.sparse_keep_div;
-        march_small_kernel<<<mlp_grid(F, live_upper, kSmallCtasPerSm), 32, sizeof(SdfSmallSmem), st_exact>>>(A);
+        march_small_kernel<<<mlp_grid(F, live_upper, exact_ctas(kSmallCtasPerSm)), 32, sizeof(SdfSmallSmem), st_exact>>>(A);
       } else if (mid) {
-        march_mid_kernel<<<mlp_grid(F, live_upper, kMidCtasPerSm), 32, sizeof(SdfMidSmem), st_exact>>>(A);
+        march_mid_kernel<<<mlp_grid(F, live_upper, exact_ctas(kMidCtasPerSm)), 32, sizeof(SdfMidSmem), st_exact>>>(A);
       } else {
         march_warp_kernel<<<mlp_grid(F, live_upper), 32, sizeof(SdfKernelSmem), st_exact>>>(A);
       }
+    }
+    mark("exact done", w, st_exact);
+    return 0;
+    };
+    if (filter_pass && beside_filter && F.exact_first) {
+      KNF_TRY(launch_exact());
+      KNF_TRY(launch_filter());
+    } else {
+      if (filter_pass) KNF_TRY(launch_filter());
+      KNF_TRY(launch_exact());
     }
     if (st_exact != st) {
       KNF_CUDA(cudaEventRecord(F.ev_join, st_exact));
@@ -730,6 +762,22 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
     }
   }
   F.prof_chain = false;
+  if (debug_timeline) {
+    mark("march end", -1, st);
+    cudaStreamSynchronize(st);
+    if (F.side_stream) cudaStreamSynchronize(F.side_stream);
+    fprintf(stderr, "timeline of a march of %lld rays (ms since start):", (long long)n);
+    int last_w = -2;
+    for (size_t i = 1; i < marks.size(); i++) {
+      float ms_ = 0.f;
+      cudaEventElapsedTime(&ms_, marks[0].ev, marks[i].ev);
+      if (marks[i].w != last_w) fprintf(stderr, "\n  w%-3d", marks[i].w);
+      last_w = marks[i].w;
+      fprintf(stderr, " %s %.3f |", marks[i].what, ms_);
+    }
+    fprintf(stderr, "\n");
+    for (Mark& m : marks) cudaEventDestroy(m.ev);
+  }
   if (std::getenv("KNF_DEBUG_HINT"))
     fprintf(stderr, "march n=%lld hint_before=%d probing=%d filter_first=%d use_filter_end=%d seen_filter=%zu seen_total=%zu wavefronts=%lld\n", (long long)n, F.filter_hint,
             (int)probing, (int)filter_first, (int)use_filter, seen_filter, seen_total, (long long)F.stats.wavefronts);

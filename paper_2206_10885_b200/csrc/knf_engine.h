@@ -120,6 +120,8 @@ struct Field {
   cudaStream_t side_stream = nullptr;    // the exact queue's tile kernels run here, beside the filter kernel on the caller's stream
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int tail_threshold = 24576;            // hand the march to march_tail_kernel (one warp per ray) once this few rays are live (twice as many when the tail can skip certified crawl steps); 0: never (KNF_TAIL)
+  int exact_grid_ctas = 0;               // cap on the exact kernels' CTAs per SM while a filter pass runs beside them (KNF_EXACT_GRID; 0: none)
+  bool exact_first = false;              // launch the exact queue's kernel before the filter's (KNF_EXACT_FIRST)
   bool filter_first = true;              // first samples through the filter queue once the handle knows its rays crawl (KNF_FILTER_FIRST=0: always the exact queue)
   bool tail_skip = true;                 // certified skipping inside march_tail_kernel (KNF_TAIL_SKIP=0 disables)
   bool overlap_queues = true;            // KNF_OVERLAP=0: one stream, filter then exact (the round-1 schedule)
