@@ -569,6 +569,7 @@ int create_from_stacks(const KnfFieldDesc* d, int device, knf_field_t* out) {
   if (const char* env = std::getenv("KNF_OVERLAP")) F.overlap_queues = std::atoi(env) != 0;
   if (const char* env = std::getenv("KNF_EXACT_GRID")) F.exact_grid_ctas = std::max(0, std::atoi(env));
   if (const char* env = std::getenv("KNF_EXACT_FIRST")) F.exact_first = std::atoi(env) != 0;
+  if (const char* env = std::getenv("KNF_FIRST_SPLIT")) F.first_split_eighths = std::max(0, std::min(8, std::atoi(env)));
   if (const char* env = std::getenv("KNF_FILTER_FIRST")) F.filter_first = std::atoi(env) != 0;
   if (const char* env = std::getenv("KNF_TAIL_SKIP")) F.tail_skip = std::atoi(env) != 0;
   if (const char* env = std::getenv("KNF_TAIL")) F.tail_threshold = std::max(0, std::atoi(env));

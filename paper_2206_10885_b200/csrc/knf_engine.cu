@@ -531,7 +531,8 @@ int march_device(Field& F, const double* o, const double* d, const double* t_nea
   {
     ProfScope prof(F, st, SPAN_ROUTE);
     RouteBuffers R0 = filter_first ? route_buffers(F, 4, 5, 2) : route_buffers(F, 0, 1, 0);
-    march_init_kernel<<<nb, 256, 0, st>>>(R0, F.geom, M, t_near, (int)n, filter_first ? M.live[2] : M.live[0]);
+    march_init_kernel<<<nb, 256, 0, st>>>(R0, F.geom, M, t_near, (int)n, filter_first ? M.live[2] : M.live[0], route_buffers(F, 0, 1, 0), M.live[0],
+                                          filter_first ? F.first_split_eighths : 0);
     F.stats.kernel_launches += 1;
   }
   size_t seen_filter = 0, seen_total = 0;

@@ -122,6 +122,7 @@ struct Field {
   int tail_threshold = 24576;            // hand the march to march_tail_kernel (one warp per ray) once this few rays are live (twice as many when the tail can skip certified crawl steps); 0: never (KNF_TAIL)
   int exact_grid_ctas = 0;               // cap on the exact kernels' CTAs per SM while a filter pass runs beside them (KNF_EXACT_GRID; 0: none)
   bool exact_first = false;              // launch the exact queue's kernel before the filter's (KNF_EXACT_FIRST)
+  int first_split_eighths = 0;           // with filter_first: this many of every 8 ray blocks start in the exact queue instead (KNF_FIRST_SPLIT)
   bool filter_first = true;              // first samples through the filter queue once the handle knows its rays crawl (KNF_FILTER_FIRST=0: always the exact queue)
   bool tail_skip = true;                 // certified skipping inside march_tail_kernel (KNF_TAIL_SKIP=0 disables)
   bool overlap_queues = true;            // KNF_OVERLAP=0: one stream, filter then exact (the round-1 schedule)

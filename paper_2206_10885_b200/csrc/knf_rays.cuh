@@ -180,7 +180,11 @@ __device__ __forceinline__ void emit_at(const RouteBuffers& R, const GridGeom& G
   route_emit(R, G, want, slot, x, y, z);
 }
 
-static __global__ void march_init_kernel(RouteBuffers R, GridGeom G, MarchState M, const double* __restrict__ t_near, int n, int* __restrict__ live_out) {
+// First samples go to queue R (its live list: live_out); with `exact_eighths` > 0 that many of every 8 consecutive 32-ray blocks
+// go to the second queue R2 / live_out2 instead (the exact queue when R is the filter queue: both kernels of wavefront 0 then
+// have work, instead of the filter evaluating every first sample alone and handing three quarters of them on undecided).
+static __global__ void march_init_kernel(RouteBuffers R, GridGeom G, MarchState M, const double* __restrict__ t_near, int n, int* __restrict__ live_out,
+                                         RouteBuffers R2, int* __restrict__ live_out2, int exact_eighths) {
   int stride = gridDim.x * blockDim.x;
   int n_round = (n + 31) & ~31;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
@@ -197,7 +201,9 @@ static __global__ void march_init_kernel(RouteBuffers R, GridGeom G, MarchState 
       M.hit[i] = 0;
       M.phase[i] = want ? PH_MARCH : PH_DONE;
     }
-    emit_at(R, G, M, live_out, want, i, t0);
+    const bool second = exact_eighths > 0 && ((i >> 5) & 7) < exact_eighths;  // warp-uniform: i >> 5 is the same for the whole warp
+    if (exact_eighths > 0 && second) emit_at(R2, G, M, live_out2, want, i, t0);
+    else emit_at(R, G, M, live_out, want, i, t0);
   }
 }
 
