@@ -239,6 +239,21 @@ def test_lipschitz_refinement_matches_restatement_and_is_sound(G, monkeypatch):
     assert ratio.mean() > 5.0  # the refinement is what makes certified skipping pay
 
 
+def test_lipschitz_accessor_without_filter_blobs(G):
+    """A field whose hidden-layer weights leave the fp16 range has no decision-filter blobs and therefore no Lipschitz bounds to
+    report: knf_field_lipschitz says so (KNF_E_UNSUPPORTED) instead of returning stale or zero bounds."""
+    from paper_2206_10885_b200 import _native as N
+
+    field = G.field_init(G.GridConfig(resolution=4), seed=3)
+    field.sdf.weights[1][0, 0, 0] = np.float32(7.0e4)  # beyond the fp16 operand pieces
+    dev = G.DeviceField.upload(field)
+    try:
+        with pytest.raises(N.KnfUnsupported):
+            dev.lipschitz()
+    finally:
+        dev.close()
+
+
 @pytest.mark.parametrize("eps,step_scale,bars", [(1e-3, 0.8, (0.99, 0.98)), (0.02, 1.0, (0.97, 0.95)), (1e-4, 0.5, (0.99, 0.98))])
 def test_skipping_on_an_off_centre_box_and_other_step_sizes(S, G, eps, step_scale, bars):
     """Certified skipping with the refined bounds on a non-cubic, off-centre box, rays that start outside it (samples clamped
